@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark: Δ-stepping SSSP on B200 (BASELINE.json metric: time/source and GTEPS = m/time;
+achieved HBM GB/s vs peak; bucket / launch / grid-sync counts with and without fusion).
+
+Default workload (N=1): BASELINE.json configs[1] — the 4096x4096 road-like grid (config 2),
+centre source, one single-source query per step. With --gpus N (torchrun, one rank per GPU)
+every rank runs its own replica of the same query (single-source SSSP does not shard:
+DESIGN.md "Multi-GPU"), value = N*m / max-over-ranks time ("scaling": "weak").
+--config 5: the 64-source batch, sources sharded over ranks, rows gathered with NCCL.
+
+--impl reference: the oracle (CPU Dijkstra, oracle/) timed on the host on the same
+workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import gen  # noqa: E402
+
+METRIC = "Δ-stepping SSSP GTEPS (m / time per source)"
+UNIT = "GTEPS"
+DEFAULT_DELTA = {1: 1000, 2: 1 << 15, 3: 2, 4: 2, 5: 1 << 15}
+WORKLOAD = {
+    1: "cfg1: 256x256 4-neighbour grid, w~U[1,1000) seed 1, src 0",
+    2: "cfg2: road-like 4096x4096 grid (5% lattice edges deleted, 1% diagonals), w~U[1,10000) seed 2, "
+       "centre source 8390656",
+    3: "cfg3: RMAT-22 ef16 (.57,.19,.19,.05) symmetrized, w~U[1,22) seed 3, max-degree source",
+    4: "cfg4: RMAT-26 ef16 symmetrized, w~U[1,26) seed 4, max-degree source",
+    5: "cfg5: 64 sources (seed 5) on the cfg2 road-like grid, sharded over GPUs, rows gathered",
+}
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 6 for k in range(4)
+                          if r[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def reached_stats(g, dist_u32):
+    reached = dist_u32 != 0xFFFFFFFF
+    n_r = int(reached.sum())
+    m_r = int(np.diff(g.offsets)[reached].sum())
+    return n_r, m_r
+
+
+def b_alg(g, n_r, m_r, nsrc=1):
+    """B_alg = 12·m_r + 16·n_r + 4·n per source (col 4 + w 4 + dist[v] 4 per
+    reached edge; offsets 8 + dist[u] 4 + one improving write 4 per reached vertex; init/output)."""
+    return nsrc * (12 * m_r + 16 * n_r + 4 * g.n)
+
+
+def load_traffic(cfg, delta):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        j = json.load(open(p))
+        return j.get(f"cfg{cfg}_delta{delta}")
+    except Exception:
+        return None
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import oracle
+    cfg = args.config
+    g = gen.config_graph(cfg)
+    srcs = gen.config_sources(cfg, g, 64) if cfg == 5 else [gen.config_source(cfg, g)]
+    src = int(srcs[0])
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        d, rc = oracle.dijkstra(g, src)
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            times.append(t1 - t0)
+    t = statistics.mean(times)
+    v = g.m / t / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": WORKLOAD[cfg], "source": src, "n": g.n, "m": g.m},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"one full binary-heap Dijkstra per step from source {src} "
+                                       f"(single-threaded C, oracle/oracle.c)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(g, src, budget_s=12.0):
+    """Oracle timed on the host (rank 0, N=1 only): whole Dijkstra queries from the same
+    source until ~budget_s of CPU work (at least one)."""
+    import oracle
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        oracle.dijkstra(g, src)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget_s or len(times) >= 5:
+            break
+    t = statistics.mean(times)
+    return {"value": g.m / t / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{len(times)} full single-threaded Dijkstra queries from source {src} "
+                      f"(oracle/oracle.c), mean {t:.3f} s each"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--delta", type=int, default=0)
+    ap.add_argument("--threshold", type=int, default=0)
+    ap.add_argument("--no-fusion", action="store_true")
+    ap.add_argument("--max-ctas", type=int, default=0)
+    ap.add_argument("--group-ctas", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-compare", action="store_true", help="skip the fusion on/off counter comparison")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1911_07260_b200 import gi
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = args.config
+    delta = args.delta or DEFAULT_DELTA[cfg]
+    g = gen.config_graph(cfg)
+    t0 = time.perf_counter()
+    G = gi.Graph.from_csr(g, device=local)
+    torch.cuda.synchronize()
+    t_upload = time.perf_counter() - t0
+    stream = torch.cuda.current_stream()
+    opts = dict(fusion=not args.no_fusion, threshold=args.threshold, max_ctas=args.max_ctas,
+                group_ctas=args.group_ctas, stream=stream)
+
+    if cfg == 5:
+        srcs_all = gen.config_sources(5, g, 64)
+        per = len(srcs_all) // world
+        srcs = torch.from_numpy(srcs_all[rank * per:(rank + 1) * per].copy())
+        out = torch.empty((per, g.n), dtype=torch.int32, device="cuda")
+        gathered = torch.empty((per * world, g.n), dtype=torch.int32, device="cuda") if world > 1 else out
+
+        def step():
+            st = gi.gi_sssp_batch(G, srcs, delta, out, gi.make_options(**opts))
+            if world > 1:
+                dist.all_gather_into_tensor(gathered, out)
+            return st
+        units_per_step = len(srcs_all) * g.m  # whole job: all 64 sources
+        launches_per_step = 1
+    else:
+        src = gen.config_source(cfg, g)
+        out = torch.empty(g.n, dtype=torch.int32, device="cuda")
+
+        def step():
+            return gi.gi_sssp_delta(G, src, delta, out, gi.make_options(**opts))
+        units_per_step = world * g.m
+        launches_per_step = 1
+
+    for _ in range(max(args.warmup, 3) if args.warmup >= 3 else args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    kernel_ms = []
+    stats = []
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        st = step()
+        s0 = st if cfg != 5 else st[0]
+        kernel_ms.append(s0.gpu_ms)
+        stats.append(st)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    kms = statistics.mean(kernel_ms)
+    if world > 1:
+        t = torch.tensor([ms, kms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, kms = float(t[0]), float(t[1])
+    value = units_per_step / (ms * 1e-3) / 1e9
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant (only) kernel: sssp_persistent ----
+    d_host = gi.as_uint32(out if cfg != 5 else out[0])
+    n_r, m_r = reached_stats(g, d_host)
+    nsrc_local = 1 if cfg != 5 else out.shape[0]
+    if cfg == 5:
+        rows = gi.as_uint32(out)
+        bytes_alg = sum(b_alg(g, *reached_stats(g, rows[i])) for i in range(rows.shape[0]))
+    else:
+        bytes_alg = b_alg(g, n_r, m_r)
+    peak, peak_src = measured_peak()
+    achieved = bytes_alg / (kms * 1e-3) / 1e9
+    traffic = load_traffic(cfg, delta)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "sssp_persistent", "kernel_ms": kms,
+                "bytes_alg_per_launch": bytes_alg, "peak_source": peak_src,
+                "note": "latency/sync-bound on road graphs: see DESIGN.md sync floor"}
+
+    s_last = stats[-1] if cfg != 5 else stats[-1][0]
+    counters = {k: getattr(s_last, k) for k in ("buckets", "rounds", "grid_syncs", "kernel_launches",
+                                                  "fused_subrounds", "spills", "vertices_processed",
+                                                  "edges_relaxed", "empty_extractions", "far_scanned",
+                                                  "ctas", "threads_per_cta", "groups")}
+
+    # ---- fusion on vs off (untimed comparison run, same Δ) ----
+    compare = None
+    if not args.no_compare and cfg != 5:
+        compare = {}
+        for fu in (True, False):
+            o2 = dict(opts)
+            o2["fusion"] = fu
+            sts = [gi.gi_sssp_delta(G, src, delta, out, gi.make_options(**o2)) for _ in range(3)]
+            s = sts[-1]
+            compare["fused" if fu else "unfused"] = {
+                "gpu_ms": statistics.median([x.gpu_ms for x in sts]), "buckets": s.buckets,
+                "rounds": s.rounds, "grid_syncs": s.grid_syncs, "kernel_launches": s.kernel_launches,
+                "fused_subrounds": s.fused_subrounds, "spills": s.spills}
+
+    # ---- e2e through the public C ABI with HOST buffers (pinned), copies inside ----
+    e2e = None
+    if cfg != 5:
+        host_out = torch.empty(g.n, dtype=torch.int32, pin_memory=True)
+        host_src = torch.tensor([src], dtype=torch.int32).pin_memory()
+        times = []
+        o_e2e = dict(opts)
+        o_e2e.pop("stream")
+        for i in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            s_val = int(host_src[0])  # source id read from pinned host memory (4 bytes H2D inside the call)
+            gi.gi_sssp_delta(G, s_val, delta, host_out.numpy(), gi.make_options(**o_e2e))
+            t1 = time.perf_counter()
+            if i >= args.warmup:
+                times.append(t1 - t0)
+        te = statistics.mean(times)
+        e2e = {"value": world * g.m / te / 1e9, "unit": UNIT, "h2d_bytes_per_step": 4,
+               "d2h_bytes_per_step": 4 * g.n, "ms_per_step": te * 1e3,
+               "api": "gi_sssp_delta_ex with a pinned host dist_out (library stages + copies back)"}
+        assert np.array_equal(host_out.numpy().view(np.uint32), d_host)
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(g, int(src if cfg != 5 else srcs_all[0]))
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": WORKLOAD[cfg], "config": cfg, "delta": delta, "fusion": not args.no_fusion,
+                   "threshold": args.threshold or "default", "n": g.n, "m": g.m, "n_reached": n_r,
+                   "m_reached": m_r, "time_per_source_ms": ms / (64 / world if cfg == 5 else 1),
+                   "l2": f"inputs larger than L2 (CSR {(g.offsets.nbytes + 8 * g.m) / 1e6:.0f} MB > 126 MB); "
+                         "dist re-initialised every step",
+                   "parallelism": f"{'sources sharded' if cfg == 5 else 'replica'} x{world}",
+                   "graph_upload_s": t_upload},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks, "counters": counters, "fusion_compare": compare,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

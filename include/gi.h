@@ -1,0 +1,148 @@
+/*
+ * gi.h — C ABI of the B200-native Δ-stepping SSSP library (libgi.so).
+ *
+ * Operation (the paper's hot path): single-source shortest paths by Δ-stepping
+ * with priority coarsening p' = ⌊p/Δ⌋ (§2), bucket i holding the
+ * vertices with tentative distance in [iΔ,(i+1)Δ) (§6.1); the
+ * smallest non-empty bucket is processed next, relaxing every out-edge
+ * Dist[dst] = min(Dist[dst], Dist[src] + w) (Fig. alg:lazy_delta_stepping,
+ * PAPER.md:409-434). Updates to FUTURE buckets are buffered lazily, one bucket
+ * update per vertex; updates into the CURRENT bucket go
+ * to a CTA-local bin that is drained without a global barrier while it stays
+ * below a threshold — bucket fusion (Fig. alg:eager_delta_stepping_merge,
+ * PAPER.md:514-558, §3.3). The result is the exact SSSP distance vector
+ * (PAPER.md:156-165), identical for every Δ, option, and CTA count.
+ *
+ * Types: vertex ids int32 (n <= 2^31-1), edge offsets int64, weights uint32,
+ * distances uint32 with UINT32_MAX = unreached (the paper's
+ * INT_MAX sentinel, is replaced). Any vertex whose true distance is
+ * >= UINT32_MAX makes the call return GI_ERR_OVERFLOW.
+ *
+ * Errors: every entry point returns a gi_status; no exception or abort crosses
+ * the boundary. On a non-OK status gi_last_error() returns a thread-local,
+ * human-readable message, and the contents of any output buffer are unspecified.
+ *
+ * Threading: a gi_graph is immutable after creation; any number of host threads
+ * may run queries on one graph concurrently (each call takes its own workspace).
+ */
+#ifndef GI_H_
+#define GI_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GI_VERSION 100 /* 1.0.0 */
+
+typedef struct gi_graph gi_graph; /* opaque; owns device copies of the CSR */
+
+typedef enum {
+  GI_OK = 0,
+  GI_ERR_INVALID_ARGUMENT = 1, /* NULL pointer, delta == 0, nsrc < 0, bad option */
+  GI_ERR_OUT_OF_RANGE = 2,     /* source id not in [0, n) */
+  GI_ERR_INVALID_GRAPH = 3,    /* n/m out of range, offsets[0] != 0, offsets not non-decreasing,
+                                  offsets[n] != m, or a column id not in [0, n) */
+  GI_ERR_OUT_OF_MEMORY = 4,    /* device or host allocation failed */
+  GI_ERR_CUDA = 5,             /* CUDA runtime error, no device, or device not sm_100 */
+  GI_ERR_OVERFLOW = 6,         /* a reachable vertex has distance >= UINT32_MAX */
+  GI_ERR_UNSUPPORTED = 7
+} gi_status;
+
+/* Create a graph on CUDA device `device` from a CSR:
+ *   row_offsets int64[n+1] (row_offsets[0] = 0, non-decreasing, row_offsets[n] = m),
+ *   col_idx     int32[m]   (0 <= col < n; out-neighbours of row v are
+ *                           col_idx[row_offsets[v] .. row_offsets[v+1]) ),
+ *   weights     uint32[m]  (weight of the matching col_idx entry; 0 allowed,
+ *                           parallel edges and self-loops allowed).
+ * Each pointer may be host memory or device memory on `device` (detected with
+ * cudaPointerGetAttributes). The arrays are COPIED; the caller keeps ownership and
+ * may free them when the call returns. 1 <= n <= 2^31-1, 0 <= m < 2^62.
+ * On success *out owns the graph until gi_graph_destroy(). */
+gi_status gi_graph_create(int64_t n, int64_t m, const int64_t* row_offsets, const int32_t* col_idx,
+                          const uint32_t* weights, int device, gi_graph** out);
+
+/* Release a graph and every cached workspace. NULL-safe. Must not race with a
+ * query on the same graph. */
+void gi_graph_destroy(gi_graph* g);
+
+/* n, m and device of a graph; any out pointer may be NULL. */
+gi_status gi_graph_info(const gi_graph* g, int64_t* n, int64_t* m, int32_t* device);
+
+/* Single-source Δ-stepping SSSP.
+ *   src      source vertex, 0 <= src < n, else GI_ERR_OUT_OF_RANGE;
+ *   delta    coarsening factor Δ >= 1 (Δ = 0 -> GI_ERR_INVALID_ARGUMENT);
+ *   dist_out uint32[n], caller-allocated; device memory on the graph's device
+ *            (zero-copy, computed in place) or host memory (staged through a device
+ *            buffer). dist_out[v] = δ(src, v), UINT32_MAX if unreachable.
+ * Synchronous: returns after dist_out is complete. */
+gi_status gi_sssp_delta(const gi_graph* g, int32_t src, uint32_t delta, uint32_t* dist_out);
+
+/* Batch of independent single-source queries (north_star):
+ *   srcs     int32[nsrc] (host or device memory); duplicates allowed;
+ *   nsrc     >= 0 (0 is a no-op returning GI_OK; < 0 -> GI_ERR_INVALID_ARGUMENT);
+ *   dist_out uint32[nsrc][n] row-major, host or device: row i = distances from srcs[i].
+ * Several queries run concurrently on disjoint CTA groups of one GPU. */
+gi_status gi_sssp_batch(const gi_graph* g, const int32_t* srcs, int32_t nsrc, uint32_t delta,
+                        uint32_t* dist_out);
+
+/* ---- extended interface (options + statistics) ---------------------------------- */
+
+typedef struct {
+  uint32_t struct_size;      /* = sizeof(gi_options) (ABI check) */
+  int32_t fusion;            /* 1: bucket fusion (default); 0: one group-wide barrier per relax round */
+  uint32_t fusion_threshold; /* T: a CTA-local current-bucket bin of size >= T spills to the global
+                                frontier (PAPER.md:539 strict '<'); 0 = library default */
+  int32_t max_ctas;          /* cap on persistent CTAs per query group (0 = all co-resident) */
+  uint32_t deg_warp_min;     /* out-degree >= this -> one warp per vertex (0 = default 32) */
+  uint32_t deg_cta_min;      /* out-degree >= this -> whole CTA per vertex (0 = default) */
+  int32_t group_ctas;        /* batch only: CTAs per concurrent query group (0 = auto) */
+  void* cuda_stream;         /* cudaStream_t to run on (NULL = library stream); calls still
+                                synchronise that stream before returning */
+} gi_options;
+
+/* Counters of one query (SURVEY §8(a) "Counter definitions"). */
+typedef struct {
+  uint64_t buckets;            /* extractions that yielded >= 1 live vertex (incl. the source's) */
+  uint64_t rounds;             /* group-wide relax passes that begin after a group barrier */
+  uint64_t grid_syncs;         /* group-wide barriers executed by the persistent kernel */
+  uint64_t kernel_launches;    /* device kernel launches issued for this query */
+  uint64_t fused_subrounds;    /* sum over CTAs of local-bin drain iterations (0 without fusion) */
+  uint64_t spills;             /* local bins flushed to the global frontier (size >= T) */
+  uint64_t vertices_processed; /* non-stale frontier entries whose out-edges were relaxed */
+  uint64_t edges_relaxed;      /* out-edges scanned */
+  uint64_t empty_extractions;  /* extractions whose bucket held only stale entries */
+  uint64_t far_scanned;        /* far-pile (overflow bucket) entries scanned by extractions */
+  float gpu_ms;                /* device time of the query (CUDA events, whole call for batch) */
+  int32_t ctas;                /* persistent CTAs in the query's group */
+  int32_t threads_per_cta;
+  int32_t groups;              /* concurrent query groups (1 for single source) */
+} gi_stats;
+
+/* Fill *opt with defaults (fusion on, library-default threshold, all CTAs). */
+void gi_options_default(gi_options* opt);
+
+/* gi_sssp_delta with options (NULL = defaults) and statistics (NULL = not wanted). */
+gi_status gi_sssp_delta_ex(const gi_graph* g, int32_t src, uint32_t delta, const gi_options* opt,
+                           uint32_t* dist_out, gi_stats* stats);
+
+/* gi_sssp_batch with options and per-source statistics (per_src: gi_stats[nsrc] or NULL;
+ * each entry's gpu_ms is the whole batch's device time). */
+gi_status gi_sssp_batch_ex(const gi_graph* g, const int32_t* srcs, int32_t nsrc, uint32_t delta,
+                           const gi_options* opt, uint32_t* dist_out, gi_stats* per_src);
+
+/* Thread-local description of the last non-OK status returned on this thread. */
+const char* gi_last_error(void);
+
+/* Static name of a status code. */
+const char* gi_status_string(gi_status s);
+
+/* GI_VERSION of the loaded library. */
+int32_t gi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GI_H_ */

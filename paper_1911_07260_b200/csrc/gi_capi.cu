@@ -1,0 +1,487 @@
+// gi_capi.cu — C ABI (include/gi.h) and host engine: graph residency, validation,
+// workspace pool, launch policy, statistics.
+#include "gi.h"
+#include "gi_internal.h"
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+using namespace gi;
+
+namespace {
+
+thread_local std::string t_last_error;
+
+gi_status fail(gi_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_last_error = std::string(gi_status_string(s)) + ": " + buf;
+  return s;
+}
+
+gi_status cuda_fail(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation) return fail(GI_ERR_OUT_OF_MEMORY, "%s: %s", what, cudaGetErrorString(e));
+  return fail(GI_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define GI_CUDA(call, what)                       \
+  do {                                            \
+    cudaError_t e_ = (call);                      \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+// Is p device memory on `device`? (host / unregistered -> false)
+bool is_device_ptr(const void* p, int device, bool* wrong_device) {
+  *wrong_device = false;
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) { cudaGetLastError(); return false; }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+    if (at.device != device) *wrong_device = true;
+    return true;
+  }
+  return false;
+}
+
+// A group workspace and the device mirror of its pointers.
+struct Workspace {
+  int64_t n = 0;
+  int cap_groups = 0;
+  std::vector<void*> allocs;
+  std::vector<GroupWs> h_groups;
+  GroupWs* d_groups = nullptr;
+  QStats* d_qstats = nullptr;
+  int qcap = 0;
+  int32_t* d_srcs = nullptr;
+  int srccap = 0;
+  uint32_t* d_stage = nullptr;  // staging for host dist_out
+  size_t stagecap = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  ~Workspace() {
+    for (void* p : allocs) cudaFree(p);
+    if (d_groups) cudaFree(d_groups);
+    if (d_qstats) cudaFree(d_qstats);
+    if (d_srcs) cudaFree(d_srcs);
+    if (d_stage) cudaFree(d_stage);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+}  // namespace
+
+struct gi_graph {
+  int device = 0;
+  int64_t n = 0, m = 0;
+  int64_t* d_off = nullptr;
+  uint2* d_edges = nullptr;
+  int sm_count = 0;
+  int bps_fused = 0, bps_plain = 0;  // co-resident CTAs per SM
+  std::mutex mu;
+  std::vector<std::unique_ptr<Workspace>> pool;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <typename T>
+gi_status dmalloc(T** p, size_t count, std::vector<void*>* track, const char* what) {
+  void* q = nullptr;
+  GI_CUDA(cudaMalloc(&q, count * sizeof(T) + 16), what);
+  *p = (T*)q;
+  if (track) track->push_back(q);
+  return GI_OK;
+}
+
+// Make a workspace with >= k groups, >= nsrc stats slots.
+gi_status ws_prepare(gi_graph* g, Workspace* w, int k, int nsrc) {
+  const int64_t n = g->n;
+  const size_t nwords = (size_t)((n + 31) / 32);
+  w->n = n;
+  if (!w->stream) {
+    GI_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    GI_CUDA(cudaEventCreate(&w->ev0), "cudaEventCreate");
+    GI_CUDA(cudaEventCreate(&w->ev1), "cudaEventCreate");
+  }
+  if (w->cap_groups < k) {
+    for (int gi_ = w->cap_groups; gi_ < k; ++gi_) {
+      GroupWs gw;
+      gi_status s;
+      if ((s = dmalloc(&gw.farbits, nwords, &w->allocs, "alloc farbits"))) return s;
+      if ((s = dmalloc(&gw.qbits[0], nwords, &w->allocs, "alloc qbits"))) return s;
+      if ((s = dmalloc(&gw.qbits[1], nwords, &w->allocs, "alloc qbits"))) return s;
+      if ((s = dmalloc(&gw.ovfbits, nwords, &w->allocs, "alloc ovfbits"))) return s;
+      if ((s = dmalloc(&gw.far[0], (size_t)n, &w->allocs, "alloc far"))) return s;
+      if ((s = dmalloc(&gw.far[1], (size_t)n, &w->allocs, "alloc far"))) return s;
+      if ((s = dmalloc(&gw.q[0], (size_t)n, &w->allocs, "alloc q"))) return s;
+      if ((s = dmalloc(&gw.q[1], (size_t)n, &w->allocs, "alloc q"))) return s;
+      if ((s = dmalloc(&gw.ctl, 1, &w->allocs, "alloc ctl"))) return s;
+      // bitmaps start (and, after every completed query, end) all-zero
+      GI_CUDA(cudaMemsetAsync(gw.farbits, 0, nwords * 4, w->stream), "memset");
+      GI_CUDA(cudaMemsetAsync(gw.qbits[0], 0, nwords * 4, w->stream), "memset");
+      GI_CUDA(cudaMemsetAsync(gw.qbits[1], 0, nwords * 4, w->stream), "memset");
+      GI_CUDA(cudaMemsetAsync(gw.ovfbits, 0, nwords * 4, w->stream), "memset");
+      GI_CUDA(cudaMemsetAsync(gw.ctl, 0, sizeof(Ctl), w->stream), "memset");
+      w->h_groups.push_back(gw);
+    }
+    if (w->d_groups) cudaFree(w->d_groups);
+    w->d_groups = nullptr;
+    GI_CUDA(cudaMalloc(&w->d_groups, sizeof(GroupWs) * k), "alloc groups");
+    GI_CUDA(cudaMemcpyAsync(w->d_groups, w->h_groups.data(), sizeof(GroupWs) * k, cudaMemcpyHostToDevice,
+                            w->stream), "copy groups");
+    w->cap_groups = k;
+  }
+  if (w->qcap < nsrc) {
+    if (w->d_qstats) cudaFree(w->d_qstats);
+    w->d_qstats = nullptr;
+    GI_CUDA(cudaMalloc(&w->d_qstats, sizeof(QStats) * nsrc), "alloc qstats");
+    w->qcap = nsrc;
+  }
+  if (w->srccap < nsrc) {
+    if (w->d_srcs) cudaFree(w->d_srcs);
+    w->d_srcs = nullptr;
+    GI_CUDA(cudaMalloc(&w->d_srcs, sizeof(int32_t) * nsrc), "alloc srcs");
+    w->srccap = nsrc;
+  }
+  return GI_OK;
+}
+
+Workspace* ws_acquire(gi_graph* g) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  if (!g->pool.empty()) {
+    Workspace* w = g->pool.back().release();
+    g->pool.pop_back();
+    return w;
+  }
+  return new Workspace();
+}
+
+void ws_release(gi_graph* g, Workspace* w, bool healthy) {
+  if (!healthy) {  // a failed query may leave dirty bitmaps: drop the workspace
+    delete w;
+    return;
+  }
+  std::lock_guard<std::mutex> lk(g->mu);
+  g->pool.emplace_back(w);
+}
+
+void fill_stats(gi_stats* st, const QStats& q, float ms, int ctas, int groups) {
+  st->buckets = q.buckets;
+  st->rounds = q.rounds;
+  st->grid_syncs = q.phases;
+  st->kernel_launches = 1;
+  st->fused_subrounds = q.subrounds;
+  st->spills = q.spills;
+  st->vertices_processed = q.vertices;
+  st->edges_relaxed = q.edges;
+  st->empty_extractions = q.empty_extr;
+  st->far_scanned = q.far_scanned;
+  st->gpu_ms = ms;
+  st->ctas = ctas;
+  st->threads_per_cta = kBlock;
+  st->groups = groups;
+}
+
+gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, uint32_t delta,
+                      const gi_options* opt_in, uint32_t* dist_out, gi_stats* stats, bool batch) {
+  gi_graph* g = const_cast<gi_graph*>(cg_);
+  if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "graph is NULL");
+  if (nsrc < 0) return fail(GI_ERR_INVALID_ARGUMENT, "nsrc < 0");
+  if (nsrc == 0) return GI_OK;
+  if (!srcs || !dist_out) return fail(GI_ERR_INVALID_ARGUMENT, "NULL srcs or dist_out");
+  if (delta == 0) return fail(GI_ERR_INVALID_ARGUMENT, "delta must be >= 1");
+  gi_options opt;
+  gi_options_default(&opt);
+  if (opt_in) {
+    if (opt_in->struct_size != sizeof(gi_options))
+      return fail(GI_ERR_INVALID_ARGUMENT, "gi_options.struct_size mismatch");
+    opt = *opt_in;
+  }
+  if (opt.max_ctas < 0 || opt.group_ctas < 0) return fail(GI_ERR_INVALID_ARGUMENT, "negative CTA count");
+  DeviceGuard dg(g->device);
+
+  // sources -> host copy for range checks
+  std::vector<int32_t> hsrc(nsrc);
+  bool wrongdev = false;
+  if (is_device_ptr(srcs, g->device, &wrongdev)) {
+    if (wrongdev) return fail(GI_ERR_INVALID_ARGUMENT, "srcs on another device");
+    GI_CUDA(cudaMemcpy(hsrc.data(), srcs, sizeof(int32_t) * nsrc, cudaMemcpyDeviceToHost), "copy srcs");
+  } else {
+    memcpy(hsrc.data(), srcs, sizeof(int32_t) * nsrc);
+  }
+  for (int i = 0; i < nsrc; ++i)
+    if (hsrc[i] < 0 || hsrc[i] >= g->n)
+      return fail(GI_ERR_OUT_OF_RANGE, "source %d not in [0, %lld)", hsrc[i], (long long)g->n);
+  const bool dev_out = is_device_ptr(dist_out, g->device, &wrongdev);
+  if (wrongdev) return fail(GI_ERR_INVALID_ARGUMENT, "dist_out on another device");
+
+  const bool fused = opt.fusion != 0;
+  const int bps = fused ? g->bps_fused : g->bps_plain;
+  int total = g->sm_count * bps;
+  // group sizing: single source -> one group of every CTA (capped by max_ctas);
+  // batch -> several groups in flight, each of group_ctas CTAs
+  int G, ngroups;
+  if (!batch || nsrc == 1) {
+    G = total;
+    if (opt.max_ctas > 0 && opt.max_ctas < G) G = opt.max_ctas;
+    ngroups = 1;
+  } else {
+    G = opt.group_ctas > 0 ? opt.group_ctas : 16;
+    if (opt.max_ctas > 0 && opt.max_ctas < G) G = opt.max_ctas;
+    if (G > total) G = total;
+    ngroups = total / G;
+    if (ngroups > nsrc) ngroups = nsrc;
+    if (ngroups < 1) ngroups = 1;
+  }
+
+  Workspace* w = ws_acquire(g);
+  gi_status s = ws_prepare(g, w, ngroups, nsrc);
+  if (s) { ws_release(g, w, false); return s; }
+  cudaStream_t st = opt.cuda_stream ? (cudaStream_t)opt.cuda_stream : w->stream;
+  if (opt.cuda_stream) {
+    // setup work queued on the workspace stream must precede the caller's stream
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventRecord(e, w->stream);
+    cudaStreamWaitEvent(st, e, 0);
+    cudaEventDestroy(e);
+  }
+
+  uint32_t* d_dist = dist_out;
+  const size_t total_elems = (size_t)nsrc * (size_t)g->n;
+  auto bail = [&](cudaError_t e, const char* what) {
+    cudaStreamSynchronize(st);
+    ws_release(g, w, false);
+    return cuda_fail(e, what);
+  };
+  cudaError_t e;
+  if (!dev_out) {
+    if (w->stagecap < total_elems) {
+      if (w->d_stage) cudaFree(w->d_stage);
+      w->d_stage = nullptr;
+      w->stagecap = 0;
+      if ((e = cudaMalloc(&w->d_stage, total_elems * 4)) != cudaSuccess) return bail(e, "alloc dist stage");
+      w->stagecap = total_elems;
+    }
+    d_dist = w->d_stage;
+  }
+  if ((e = cudaMemcpyAsync(w->d_srcs, hsrc.data(), sizeof(int32_t) * nsrc, cudaMemcpyHostToDevice, st)))
+    return bail(e, "copy srcs");
+  if ((e = cudaMemsetAsync(w->d_qstats, 0, sizeof(QStats) * nsrc, st))) return bail(e, "memset qstats");
+
+  KArgs a;
+  a.off = g->d_off;
+  a.edges = g->d_edges;
+  a.n = g->n;
+  a.nwords = (uint32_t)((g->n + 31) / 32);
+  a.srcs = w->d_srcs;
+  a.nsrc = nsrc;
+  a.dist = d_dist;
+  a.groups = w->d_groups;
+  a.qstats = w->d_qstats;
+  a.ngroups = ngroups;
+  a.group_size = G;
+  a.div = make_fastdiv(delta);
+  a.T = opt.fusion_threshold ? opt.fusion_threshold : kDefaultT;
+  if (a.T > (uint32_t)kBinCap) a.T = kBinCap;
+  a.deg_warp_min = opt.deg_warp_min ? opt.deg_warp_min : kDefaultWarpMin;
+  a.deg_cta_min = opt.deg_cta_min ? opt.deg_cta_min : kDefaultCtaMin;
+
+  if ((e = cudaEventRecord(w->ev0, st))) return bail(e, "event");
+  if ((e = launch_sssp(a, fused, G * ngroups, st))) return bail(e, "launch sssp_persistent");
+  if ((e = cudaEventRecord(w->ev1, st))) return bail(e, "event");
+  std::vector<QStats> hq(nsrc);
+  if ((e = cudaMemcpyAsync(hq.data(), w->d_qstats, sizeof(QStats) * nsrc, cudaMemcpyDeviceToHost, st)))
+    return bail(e, "copy stats");
+  if (!dev_out) {
+    if ((e = cudaMemcpyAsync(dist_out, d_dist, total_elems * 4, cudaMemcpyDeviceToHost, st)))
+      return bail(e, "copy dist");
+  }
+  if ((e = cudaStreamSynchronize(st))) return bail(e, "sssp kernel");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, w->ev0, w->ev1);
+  ws_release(g, w, true);
+
+  bool ovf = false;
+  for (int i = 0; i < nsrc; ++i) {
+    if (hq[i].overflow) ovf = true;
+    if (stats) fill_stats(&stats[i], hq[i], ms, G, ngroups);
+  }
+  if (ovf) return fail(GI_ERR_OVERFLOW, "a reachable vertex has distance >= UINT32_MAX");
+  return GI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gi_status_string(gi_status s) {
+  switch (s) {
+    case GI_OK: return "GI_OK";
+    case GI_ERR_INVALID_ARGUMENT: return "GI_ERR_INVALID_ARGUMENT";
+    case GI_ERR_OUT_OF_RANGE: return "GI_ERR_OUT_OF_RANGE";
+    case GI_ERR_INVALID_GRAPH: return "GI_ERR_INVALID_GRAPH";
+    case GI_ERR_OUT_OF_MEMORY: return "GI_ERR_OUT_OF_MEMORY";
+    case GI_ERR_CUDA: return "GI_ERR_CUDA";
+    case GI_ERR_OVERFLOW: return "GI_ERR_OVERFLOW";
+    case GI_ERR_UNSUPPORTED: return "GI_ERR_UNSUPPORTED";
+  }
+  return "GI_ERR_UNKNOWN";
+}
+
+const char* gi_last_error(void) { return t_last_error.c_str(); }
+
+int32_t gi_version(void) { return GI_VERSION; }
+
+void gi_options_default(gi_options* opt) {
+  if (!opt) return;
+  memset(opt, 0, sizeof(*opt));
+  opt->struct_size = sizeof(gi_options);
+  opt->fusion = 1;
+}
+
+gi_status gi_graph_create(int64_t n, int64_t m, const int64_t* row_offsets, const int32_t* col_idx,
+                          const uint32_t* weights, int device, gi_graph** out) {
+  if (!out) return fail(GI_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (n < 1 || n > 0x7FFFFFFFll) return fail(GI_ERR_INVALID_GRAPH, "n=%lld not in [1, 2^31-1]", (long long)n);
+  if (m < 0 || m >= (1ll << 62)) return fail(GI_ERR_INVALID_GRAPH, "m=%lld out of range", (long long)m);
+  if (!row_offsets || (m > 0 && (!col_idx || !weights)))
+    return fail(GI_ERR_INVALID_ARGUMENT, "NULL CSR array");
+  int ndev = 0;
+  GI_CUDA(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) return fail(GI_ERR_CUDA, "device %d not present (%d devices)", device, ndev);
+  cudaDeviceProp prop;
+  GI_CUDA(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(GI_ERR_CUDA, "device %d is sm_%d%d; this library is built for sm_100a only", device, prop.major,
+                prop.minor);
+  DeviceGuard dg(device);
+
+  std::unique_ptr<gi_graph> g(new gi_graph());
+  g->device = device;
+  g->n = n;
+  g->m = m;
+  g->sm_count = prop.multiProcessorCount;
+  GI_CUDA(query_occupancy(true, &g->bps_fused), "occupancy");
+  GI_CUDA(query_occupancy(false, &g->bps_plain), "occupancy");
+  if (g->bps_fused < 1 || g->bps_plain < 1) return fail(GI_ERR_CUDA, "persistent kernel cannot be resident");
+
+  cudaStream_t st;
+  GI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } sg{st};
+
+  uint32_t* d_bad = nullptr;
+  GI_CUDA(cudaMalloc(&d_bad, 4), "alloc");
+  struct FreeGuard { void* p; ~FreeGuard() { cudaFree(p); } } fb{d_bad};
+  GI_CUDA(cudaMemsetAsync(d_bad, 0, 4, st), "memset");
+
+  bool wrong = false;
+  GI_CUDA(cudaMalloc(&g->d_off, sizeof(int64_t) * (n + 1)), "alloc offsets");
+  const bool off_dev = is_device_ptr(row_offsets, device, &wrong);
+  if (wrong) return fail(GI_ERR_INVALID_ARGUMENT, "row_offsets on another device");
+  GI_CUDA(cudaMemcpyAsync(g->d_off, row_offsets, sizeof(int64_t) * (n + 1),
+                          off_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st), "copy offsets");
+  GI_CUDA(launch_validate_offsets(g->d_off, n, m, d_bad, st), "validate offsets");
+
+  GI_CUDA(cudaMalloc(&g->d_edges, sizeof(uint2) * (m > 0 ? m : 1)), "alloc edges");
+  if (m > 0) {
+    const bool c_dev = is_device_ptr(col_idx, device, &wrong);
+    if (wrong) return fail(GI_ERR_INVALID_ARGUMENT, "col_idx on another device");
+    const bool w_dev = is_device_ptr(weights, device, &wrong);
+    if (wrong) return fail(GI_ERR_INVALID_ARGUMENT, "weights on another device");
+    if (c_dev && w_dev) {
+      GI_CUDA(launch_interleave(col_idx, weights, g->d_edges, m, n, d_bad, st), "interleave");
+    } else {
+      // stage host arrays through device chunks
+      const int64_t chunk = std::min<int64_t>(m, 64ll << 20);
+      int32_t* dc = nullptr;
+      uint32_t* dw = nullptr;
+      GI_CUDA(cudaMalloc(&dc, chunk * 4), "alloc stage");
+      FreeGuard fc{dc};
+      GI_CUDA(cudaMalloc(&dw, chunk * 4), "alloc stage");
+      FreeGuard fw{dw};
+      for (int64_t p = 0; p < m; p += chunk) {
+        const int64_t k = std::min(chunk, m - p);
+        GI_CUDA(cudaMemcpyAsync(dc, col_idx + p, k * 4, c_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                st), "copy cols");
+        GI_CUDA(cudaMemcpyAsync(dw, weights + p, k * 4, w_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                st), "copy weights");
+        GI_CUDA(launch_interleave(dc, dw, g->d_edges + p, k, n, d_bad, st), "interleave");
+      }
+      GI_CUDA(cudaStreamSynchronize(st), "graph upload");
+    }
+  }
+  uint32_t bad = 0;
+  GI_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st), "copy flag");
+  GI_CUDA(cudaStreamSynchronize(st), "graph validation");
+  if (bad) {
+    cudaFree(g->d_off);
+    cudaFree(g->d_edges);
+    return fail(GI_ERR_INVALID_GRAPH, "offsets not a valid CSR (offsets[0]=0, non-decreasing, offsets[n]=m) "
+                                      "or a column id outside [0, n)");
+  }
+  *out = g.release();
+  return GI_OK;
+}
+
+void gi_graph_destroy(gi_graph* g) {
+  if (!g) return;
+  {
+    DeviceGuard dg(g->device);
+    g->pool.clear();
+    cudaFree(g->d_off);
+    cudaFree(g->d_edges);
+  }
+  delete g;
+}
+
+gi_status gi_graph_info(const gi_graph* g, int64_t* n, int64_t* m, int32_t* device) {
+  if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "graph is NULL");
+  if (n) *n = g->n;
+  if (m) *m = g->m;
+  if (device) *device = g->device;
+  return GI_OK;
+}
+
+gi_status gi_sssp_delta_ex(const gi_graph* g, int32_t src, uint32_t delta, const gi_options* opt,
+                           uint32_t* dist_out, gi_stats* stats) {
+  return run_queries(g, &src, 1, delta, opt, dist_out, stats, false);
+}
+
+gi_status gi_sssp_delta(const gi_graph* g, int32_t src, uint32_t delta, uint32_t* dist_out) {
+  return gi_sssp_delta_ex(g, src, delta, nullptr, dist_out, nullptr);
+}
+
+gi_status gi_sssp_batch_ex(const gi_graph* g, const int32_t* srcs, int32_t nsrc, uint32_t delta,
+                           const gi_options* opt, uint32_t* dist_out, gi_stats* per_src) {
+  return run_queries(g, srcs, nsrc, delta, opt, dist_out, per_src, true);
+}
+
+gi_status gi_sssp_batch(const gi_graph* g, const int32_t* srcs, int32_t nsrc, uint32_t delta,
+                        uint32_t* dist_out) {
+  return gi_sssp_batch_ex(g, srcs, nsrc, delta, nullptr, dist_out, nullptr);
+}
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// gi_internal.h — structures shared by the sm_100a kernels and the host engine.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gi {
+
+constexpr uint32_t kInf = 0xFFFFFFFFu;
+constexpr int kBlock = 512;          // threads per persistent CTA
+constexpr int kBinCap = 2048;        // entries per CTA-local bin (uint2 {v, d}); two bins per CTA
+constexpr uint32_t kDefaultT = 1024; // fusion threshold default (vertices per CTA bin)
+constexpr uint32_t kDefaultWarpMin = 32;
+constexpr uint32_t kDefaultCtaMin = 2048;
+
+// Division by the invariant Δ (Granlund & Montgomery 1994, round-up method):
+// q = (t + ((x - t) >> s1)) >> s2 with t = umulhi(mul, x).
+struct FastDiv {
+  uint32_t mul, s1, s2, d;
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  uint32_t l = 0;
+  while (l < 32 && (1ull << l) < d) ++l;  // l = ceil(log2 d)
+  f.mul = (uint32_t)((((1ull << l) - d) << 32) / d + 1);
+  f.s1 = l > 0 ? 1 : 0;
+  f.s2 = l > 0 ? l - 1 : 0;
+  f.d = d;
+  return f;
+}
+
+// Per-query control block (device). Counters rotate mod 3 so that a slot is
+// reset only after every CTA has read it.
+struct alignas(128) Ctl {
+  uint32_t qcount[3];   // global frontier sizes, by phase mod 3
+  uint32_t fcount[3];   // far-pile (overflow bucket) sizes, by extraction mod 3
+  uint32_t fmin[3];     // lower bound of the min live far bucket, by extraction mod 3
+  uint32_t xlive[3];    // live vertices extracted, by extraction mod 3
+  uint32_t ovf_cand;    // some candidate distance >= UINT32_MAX was produced
+  uint32_t pad0[19];
+  uint32_t bar_count;   // group barrier arrival counter (own 128 B line)
+  uint32_t pad1[31];
+  uint32_t bar_gen;     // group barrier generation (own 128 B line)
+  uint32_t pad2[31];
+};
+
+// Per-source result record (device, copied back to gi_stats).
+struct QStats {
+  unsigned long long buckets, rounds, phases, subrounds, spills, vertices, edges, empty_extr,
+      far_scanned;
+  uint32_t overflow;
+  uint32_t pad;
+};
+
+// One query group's workspace (device pointers).
+struct GroupWs {
+  uint32_t* farbits;  // [nwords] "in far pile" dedup bits (lazy buffer reduction)
+  uint32_t* qbits[2]; // [nwords] "in global frontier" dedup bits, by phase parity
+  uint32_t* ovfbits;  // [nwords] vertices that received an overflowing candidate
+  int32_t* far[2];    // [n] far pile, double-buffered across extractions
+  int32_t* q[2];      // [n] global frontier, double-buffered across phases
+  Ctl* ctl;
+};
+
+struct KArgs {
+  const int64_t* off;   // [n+1]
+  const uint2* edges;   // [m] {col, w} interleaved
+  int64_t n;
+  uint32_t nwords;
+  const int32_t* srcs;  // [nsrc] device
+  int32_t nsrc;
+  uint32_t* dist;       // [nsrc][n] device
+  GroupWs* groups;      // [ngroups] device
+  QStats* qstats;       // [nsrc] device
+  int32_t ngroups;
+  int32_t group_size;   // CTAs per group
+  FastDiv div;
+  uint32_t T;           // fusion threshold (<= kBinCap)
+  uint32_t deg_warp_min, deg_cta_min;
+};
+
+// Host-side launchers (gi_kernels.cu).
+cudaError_t launch_sssp(const KArgs& a, bool fused, int grid, cudaStream_t st);
+cudaError_t query_occupancy(bool fused, int* blocks_per_sm);
+cudaError_t launch_interleave(const int32_t* cols, const uint32_t* w, uint2* edges, int64_t count,
+                              int64_t n, uint32_t* bad_flag, cudaStream_t st);
+cudaError_t launch_validate_offsets(const int64_t* off, int64_t n, int64_t m, uint32_t* bad_flag,
+                                    cudaStream_t st);
+int smem_bytes();
+
+}  // namespace gi

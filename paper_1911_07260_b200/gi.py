@@ -1,0 +1,213 @@
+"""Thin ctypes binding over libgi.so (include/gi.h): argument marshalling only.
+
+Every step of the SSSP path runs in the library's sm_100a kernels; this module only
+converts torch tensors / numpy arrays to pointers. There is no CPU fallback: if the
+shared library is missing the import fails loudly.
+
+torch has no full uint32 support, so distances are returned as int32 tensors holding
+the uint32 bit pattern (UINT32_MAX reads as -1); ``as_uint32`` converts on the host.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_PKG, "libgi.so")
+
+if not os.path.exists(_SO):
+    raise ImportError(f"libgi.so not built at {_SO}: run __graft_entry__.build() "
+                      "(the CUDA path has no fallback)")
+_lib = ctypes.CDLL(_SO)
+
+GI_OK = 0
+STATUS = {0: "GI_OK", 1: "GI_ERR_INVALID_ARGUMENT", 2: "GI_ERR_OUT_OF_RANGE", 3: "GI_ERR_INVALID_GRAPH",
+          4: "GI_ERR_OUT_OF_MEMORY", 5: "GI_ERR_CUDA", 6: "GI_ERR_OVERFLOW", 7: "GI_ERR_UNSUPPORTED"}
+EXPORTS = ["gi_graph_create", "gi_graph_destroy", "gi_graph_info", "gi_sssp_delta", "gi_sssp_batch",
+           "gi_options_default", "gi_sssp_delta_ex", "gi_sssp_batch_ex", "gi_last_error",
+           "gi_status_string", "gi_version"]
+
+
+class GiError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(msg)
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class OverflowDistance(GiError):
+    pass
+
+
+class gi_options(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_uint32), ("fusion", ctypes.c_int32),
+                ("fusion_threshold", ctypes.c_uint32), ("max_ctas", ctypes.c_int32),
+                ("deg_warp_min", ctypes.c_uint32), ("deg_cta_min", ctypes.c_uint32),
+                ("group_ctas", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p)]
+
+
+class gi_stats(ctypes.Structure):
+    _fields_ = [("buckets", ctypes.c_uint64), ("rounds", ctypes.c_uint64), ("grid_syncs", ctypes.c_uint64),
+                ("kernel_launches", ctypes.c_uint64), ("fused_subrounds", ctypes.c_uint64),
+                ("spills", ctypes.c_uint64), ("vertices_processed", ctypes.c_uint64),
+                ("edges_relaxed", ctypes.c_uint64), ("empty_extractions", ctypes.c_uint64),
+                ("far_scanned", ctypes.c_uint64), ("gpu_ms", ctypes.c_float), ("ctas", ctypes.c_int32),
+                ("threads_per_cta", ctypes.c_int32), ("groups", ctypes.c_int32)]
+
+    def to_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_vp, _i64, _i32, _u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32
+_lib.gi_graph_create.argtypes = [_i64, _i64, _vp, _vp, _vp, ctypes.c_int, ctypes.POINTER(_vp)]
+_lib.gi_graph_destroy.argtypes = [_vp]
+_lib.gi_graph_destroy.restype = None
+_lib.gi_graph_info.argtypes = [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i32)]
+_lib.gi_sssp_delta.argtypes = [_vp, _i32, _u32, _vp]
+_lib.gi_sssp_batch.argtypes = [_vp, _vp, _i32, _u32, _vp]
+_lib.gi_options_default.argtypes = [ctypes.POINTER(gi_options)]
+_lib.gi_options_default.restype = None
+_lib.gi_sssp_delta_ex.argtypes = [_vp, _i32, _u32, ctypes.POINTER(gi_options), _vp, ctypes.POINTER(gi_stats)]
+_lib.gi_sssp_batch_ex.argtypes = [_vp, _vp, _i32, _u32, ctypes.POINTER(gi_options), _vp, ctypes.POINTER(gi_stats)]
+_lib.gi_last_error.restype = ctypes.c_char_p
+_lib.gi_status_string.argtypes = [ctypes.c_int]
+_lib.gi_status_string.restype = ctypes.c_char_p
+_lib.gi_version.restype = _i32
+for _f in ("gi_graph_create", "gi_graph_info", "gi_sssp_delta", "gi_sssp_batch", "gi_sssp_delta_ex",
+           "gi_sssp_batch_ex"):
+    getattr(_lib, _f).restype = ctypes.c_int
+
+
+def _check(rc):
+    if rc != GI_OK:
+        msg = (_lib.gi_last_error() or b"").decode()
+        if rc == 6:
+            raise OverflowDistance(rc, msg)
+        raise GiError(rc, msg)
+
+
+def lib():
+    return _lib
+
+
+def version() -> int:
+    return int(_lib.gi_version())
+
+
+def _ptr(x):
+    """data pointer of a torch tensor / numpy array (must be contiguous)."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return x.data_ptr()
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return x.ctypes.data
+    raise TypeError(type(x))
+
+
+def make_options(fusion=True, threshold=0, max_ctas=0, deg_warp_min=0, deg_cta_min=0, group_ctas=0,
+                 stream=None) -> gi_options:
+    o = gi_options()
+    _lib.gi_options_default(ctypes.byref(o))
+    o.fusion = 1 if fusion else 0
+    o.fusion_threshold = threshold
+    o.max_ctas = max_ctas
+    o.deg_warp_min = deg_warp_min
+    o.deg_cta_min = deg_cta_min
+    o.group_ctas = group_ctas
+    if stream is not None:
+        o.cuda_stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    return o
+
+
+class Graph:
+    """Device-resident CSR graph (gi_graph_create). Arrays may be numpy (host) or torch
+    (host or CUDA) — int64 offsets[n+1], int32 cols[m], uint32/int32 weights[m]."""
+
+    def __init__(self, offsets, cols, weights, device: int = 0):
+        n = int(offsets.shape[0]) - 1
+        m = int(cols.shape[0])
+        if isinstance(weights, np.ndarray) and weights.dtype != np.uint32:
+            weights = weights.astype(np.uint32)
+        h = _vp()
+        _check(_lib.gi_graph_create(n, m, _ptr(offsets), _ptr(cols) if m else None,
+                                    _ptr(weights) if m else None, device, ctypes.byref(h)))
+        self._h = h
+        self.n, self.m, self.device = n, m, device
+
+    @classmethod
+    def from_csr(cls, csr, device: int = 0):
+        return cls(csr.offsets, csr.cols, csr.w, device)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        n, m, d = _i64(), _i64(), _i32()
+        _check(_lib.gi_graph_info(self._h, ctypes.byref(n), ctypes.byref(m), ctypes.byref(d)))
+        return n.value, m.value, d.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.gi_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gi_sssp_delta(g: Graph, src: int, delta: int, dist_out, options: gi_options | None = None,
+                  want_stats: bool = True):
+    """C-ABI gi_sssp_delta_ex. dist_out: torch int32/uint32 CUDA tensor [n] or numpy uint32 [n]."""
+    st = gi_stats() if want_stats else None
+    _check(_lib.gi_sssp_delta_ex(g.handle, int(src), int(delta), ctypes.byref(options) if options else None,
+                                 _ptr(dist_out), ctypes.byref(st) if st is not None else None))
+    return st
+
+
+def gi_sssp_batch(g: Graph, srcs, delta: int, dist_out, options: gi_options | None = None,
+                  want_stats: bool = True):
+    """C-ABI gi_sssp_batch_ex. srcs: int32 array/tensor [k]; dist_out [k, n]."""
+    k = int(srcs.shape[0])
+    st = (gi_stats * max(k, 1))() if want_stats else None
+    _check(_lib.gi_sssp_batch_ex(g.handle, _ptr(srcs), k, int(delta),
+                                 ctypes.byref(options) if options else None, _ptr(dist_out), st))
+    return st
+
+
+def sssp(g: Graph, src: int, delta: int, out=None, **opts):
+    """Single-source Δ-stepping on the graph's device. Returns (dist int32 tensor [n]
+    holding uint32 bits, stats dict)."""
+    import torch
+    if out is None:
+        out = torch.empty(g.n, dtype=torch.int32, device=f"cuda:{g.device}")
+    st = gi_sssp_delta(g, src, delta, out, make_options(**opts) if opts else None)
+    return out, st.to_dict()
+
+
+def sssp_batch(g: Graph, srcs, delta: int, out=None, **opts):
+    import torch
+    if not hasattr(srcs, "data_ptr") and not isinstance(srcs, np.ndarray):
+        srcs = np.asarray(srcs, dtype=np.int32)
+    k = int(srcs.shape[0])
+    if out is None:
+        out = torch.empty((k, g.n), dtype=torch.int32, device=f"cuda:{g.device}")
+    st = gi_sssp_batch(g, srcs, delta, out, make_options(**opts) if opts else None)
+    return out, [st[i].to_dict() for i in range(k)]
+
+
+def as_uint32(t) -> np.ndarray:
+    """int32 tensor/array holding uint32 bits -> numpy uint32 (host)."""
+    if hasattr(t, "cpu"):
+        t = t.cpu().numpy()
+    return np.asarray(t).view(np.uint32)

@@ -1,0 +1,213 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Bar (north_star): bit-exact uint32 distances for every vertex, unreached = UINT32_MAX.
+Counters are checked only where a closed form pins them.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = json.load(open(os.path.join(HERE, "golden", "hand_examples.json")))["examples"]
+INF = 0xFFFFFFFF
+
+
+@pytest.fixture(scope="module")
+def gi():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1911_07260_b200 import _build
+    _build.build_lib()
+    from paper_1911_07260_b200 import gi as m
+    return m
+
+
+def run(gi, G, src, delta, **opts):
+    d, st = gi.sssp(G, src, delta, **opts)
+    return gi.as_uint32(d), st
+
+
+OPTS = [dict(fusion=True), dict(fusion=False), dict(fusion=True, threshold=2),
+        dict(fusion=True, max_ctas=1), dict(fusion=False, max_ctas=3),
+        dict(fusion=True, deg_warp_min=2, deg_cta_min=3)]
+
+
+@pytest.mark.parametrize("ex", GOLDEN, ids=[e["name"] for e in GOLDEN])
+def test_hand_examples(gi, ex):
+    g = gen.from_edges(ex["n"], ex["edges"])
+    G = gi.Graph.from_csr(g)
+    for o in OPTS:
+        if ex.get("status") == "overflow":
+            with pytest.raises(gi.OverflowDistance):
+                run(gi, G, ex["src"], ex["delta"], **o)
+            continue
+        d, st = run(gi, G, ex["src"], ex["delta"], **o)
+        assert d.tolist() == ex["dist"], o
+        assert st["buckets"] == ex["buckets"], (o, st)
+
+
+def test_spec_corpus(gi):
+    """SPEC.md:508 acceptance corpus: 100 uniform_random graphs n=64, m=512, [1,1000), 3 sources."""
+    for seed in range(100):
+        g = gen.uniform_random(64, 512, 1, 1000, seed)
+        G = gi.Graph.from_csr(g)
+        for s in (0, 31, 63):
+            ref, _ = oracle.dijkstra(g, s)
+            for o, delta in ((dict(fusion=True), 100), (dict(fusion=False), 100), (dict(fusion=True), 1),
+                             (dict(fusion=True, threshold=4), 2000)):
+                d, _ = run(gi, G, s, delta, **o)
+                assert np.array_equal(d, ref), (seed, s, o, delta)
+
+
+def test_random_small_with_zero_weights_multi_edges(gi):
+    rng = np.random.default_rng(7)
+    for t in range(60):
+        n = int(rng.integers(1, 300))
+        m = int(rng.integers(0, 2000))
+        edges = [(int(rng.integers(0, n)), int(rng.integers(0, n)), int(rng.integers(0, 50))) for _ in range(m)]
+        g = gen.from_edges(n, edges)
+        G = gi.Graph.from_csr(g)
+        s = int(rng.integers(0, n))
+        ref, _ = oracle.dijkstra(g, s)
+        for delta in (1, 7, 10**6):
+            d, _ = run(gi, G, s, delta, fusion=bool(t % 2), max_ctas=int(rng.integers(1, 40)))
+            assert np.array_equal(d, ref), (t, delta)
+
+
+def test_config1_delta_sweep(gi, config_graph):
+    g = config_graph(1)
+    G = gi.Graph.from_csr(g)
+    ref, _ = oracle.dijkstra(g, 0)
+    for delta in (250, 500, 1000, 2000, 4000, 1, 10**9):
+        for o in OPTS:
+            d, st = run(gi, G, 0, delta, **o)
+            assert np.array_equal(d, ref), (delta, o)
+            assert st["buckets"] == oracle.bucket_count(ref, delta), (delta, o, st)
+
+
+def test_host_output_buffer(gi, config_graph):
+    g = config_graph(1)
+    G = gi.Graph.from_csr(g)
+    out = np.zeros(g.n, np.uint32)
+    gi.gi_sssp_delta(G, 0, 1000, out)
+    assert np.array_equal(out, oracle.dijkstra(g, 0)[0])
+    srcs = np.array([5, 700, 65535, 5], np.int32)
+    outb = np.zeros((4, g.n), np.uint32)
+    gi.gi_sssp_batch(G, srcs, 1000, outb)
+    assert np.array_equal(outb, oracle.dijkstra_many(g, srcs)[0])
+
+
+def test_device_csr_input(gi, config_graph):
+    import torch
+    g = config_graph(1)
+    G = gi.Graph(torch.from_numpy(g.offsets).cuda(), torch.from_numpy(g.cols).cuda(),
+                 torch.from_numpy(g.w.view(np.int32)).cuda())
+    d, _ = run(gi, G, 0, 1000)
+    assert np.array_equal(d, oracle.dijkstra(g, 0)[0])
+
+
+def test_path_closed_form_rounds(gi):
+    """Path, unit weights: rounds without fusion = n; with fusion = ⌈n/Δ⌉ = buckets."""
+    for n, delta in ((1000, 100), (4096, 1024), (300, 1)):
+        g = gen.path(n)
+        G = gi.Graph.from_csr(g)
+        d, st = run(gi, G, 0, delta, fusion=False)
+        assert d.tolist() == list(range(n))
+        assert st["rounds"] == n and st["buckets"] == -(-n // delta)
+        d, st = run(gi, G, 0, delta, fusion=True)
+        assert d.tolist() == list(range(n))
+        assert st["rounds"] == -(-n // delta) == st["buckets"], st
+        assert st["spills"] == 0
+
+
+def test_delta_le_wmin_processes_each_vertex_once(gi):
+    """Δ <= w_min: every reached vertex is processed exactly once."""
+    g = gen.grid(64, 64, 3, 4, 0)
+    G = gi.Graph.from_csr(g)
+    s = 32 * 64 + 32
+    for delta in (1, 3):
+        for fusion in (True, False):
+            d, st = run(gi, G, s, delta, fusion=fusion)
+            assert np.array_equal(d, oracle.dijkstra(g, s)[0])
+            assert st["vertices_processed"] == g.n and st["edges_relaxed"] == g.m
+
+
+def test_errors(gi):
+    g = gen.path(5)
+    G = gi.Graph.from_csr(g)
+    with pytest.raises(gi.GiError) as e:
+        run(gi, G, 5, 1)
+    assert e.value.status == 2
+    with pytest.raises(gi.GiError) as e:
+        run(gi, G, -1, 1)
+    assert e.value.status == 2
+    with pytest.raises(gi.GiError) as e:
+        run(gi, G, 0, 0)
+    assert e.value.status == 1
+    bad_off = np.array([0, 2, 1, 3], np.int64)
+    with pytest.raises(gi.GiError) as e:
+        gi.Graph(bad_off, np.zeros(3, np.int32), np.ones(3, np.uint32))
+    assert e.value.status == 3
+    with pytest.raises(gi.GiError) as e:
+        gi.Graph(np.array([0, 1], np.int64), np.array([1], np.int32), np.ones(1, np.uint32))
+    assert e.value.status == 3
+    with pytest.raises(gi.GiError) as e:
+        gi.Graph(np.array([0, 1, 3], np.int64), np.zeros(2, np.int32), np.ones(2, np.uint32))
+    assert e.value.status == 3
+    # nsrc = 0 is a no-op
+    import torch
+    out = torch.empty((0, 5), dtype=torch.int32, device="cuda")
+    gi.gi_sssp_batch(G, np.zeros(0, np.int32), 1, out)
+
+
+@pytest.mark.slow
+def test_config2_full(gi, config_graph):
+    g = config_graph(2)
+    G = gi.Graph.from_csr(g)
+    src = gen.config_source(2, g)
+    ref, _ = oracle.dijkstra(g, src)
+    for delta, fusion in ((1 << 13, True), (1 << 16, True), (1 << 10, False)):
+        d, st = run(gi, G, src, delta, fusion=fusion)
+        assert np.array_equal(d, ref), (delta, fusion)
+        assert st["buckets"] == oracle.bucket_count(ref, delta)
+    assert oracle.certificate(g, src, d, symmetric=True)[0] == 0
+
+
+@pytest.mark.slow
+def test_config3_full(gi, config_graph):
+    g = config_graph(3)
+    G = gi.Graph.from_csr(g)
+    ref, _ = oracle.dijkstra(g, 0)
+    for delta in (1, 2, 4, 8):
+        for fusion in (True, False):
+            d, st = run(gi, G, 0, delta, fusion=fusion)
+            assert np.array_equal(d, ref), (delta, fusion)
+            assert st["buckets"] == oracle.bucket_count(ref, delta)
+    d, st = run(gi, G, 0, 1)
+    assert st["edges_relaxed"] == int(np.diff(g.offsets)[ref != INF].sum())  # Δ=1 <= w_min
+
+
+@pytest.mark.slow
+def test_config5_batch(gi, config_graph):
+    g = config_graph(5)
+    G = gi.Graph.from_csr(g)
+    srcs = gen.config_sources(5, g)
+    out, st = gi.sssp_batch(G, srcs, 1 << 13)
+    got = gi.as_uint32(out)
+    # batch symmetry on a symmetric graph: δ(si,sj) == δ(sj,si) for all 64x64 pairs
+    M = got[:, srcs.astype(np.int64)]
+    assert np.array_equal(M, M.T)
+    # element-wise parity on a subset of rows (oracle ~5 s per source)
+    idx = [0, 21, 63]
+    refs, _, _ = oracle.dijkstra_many(g, srcs[idx])
+    assert np.array_equal(got[idx], refs)
+    for i in range(64):
+        assert st[i]["buckets"] > 0
