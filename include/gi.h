@@ -98,6 +98,8 @@ typedef struct {
   uint32_t deg_warp_min;     /* out-degree >= this -> one warp per vertex (0 = default 32) */
   uint32_t deg_cta_min;      /* out-degree >= this -> whole CTA per vertex (0 = default) */
   int32_t group_ctas;        /* batch only: CTAs per concurrent query group (0 = auto) */
+  int32_t pre_read;          /* read dist[v] before atomicMin: 0 = auto (on when max out-degree > 32),
+                                1 = on, 2 = off */
   void* cuda_stream;         /* cudaStream_t to run on (NULL = library stream); calls still
                                 synchronise that stream before returning */
 } gi_options;

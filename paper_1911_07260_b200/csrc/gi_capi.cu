@@ -86,6 +86,8 @@ struct gi_graph {
   int64_t n = 0, m = 0;
   int64_t* d_off = nullptr;
   uint2* d_edges = nullptr;
+  uint4* d_slots = nullptr;  // ELL adjacency slots, 64 B per vertex
+  uint32_t max_deg = 0;
   int sm_count = 0;
   int bps_fused = 0, bps_plain = 0;  // co-resident CTAs per SM
   std::mutex mu;
@@ -291,7 +293,7 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   if ((e = cudaMemsetAsync(w->d_qstats, 0, sizeof(QStats) * nsrc, st))) return bail(e, "memset qstats");
 
   KArgs a;
-  a.off = g->d_off;
+  a.slots = g->d_slots;
   a.edges = g->d_edges;
   a.n = g->n;
   a.nwords = (uint32_t)((g->n + 31) / 32);
@@ -307,6 +309,11 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   if (a.T > (uint32_t)kBinCap) a.T = kBinCap;
   a.deg_warp_min = opt.deg_warp_min ? opt.deg_warp_min : kDefaultWarpMin;
   a.deg_cta_min = opt.deg_cta_min ? opt.deg_cta_min : kDefaultCtaMin;
+  if (a.deg_warp_min < 1) a.deg_warp_min = 1;
+  if (a.deg_cta_min < 1) a.deg_cta_min = 1;
+  // pre-read dist[v] before the atomic: pays off when hubs attract many redundant
+  // relaxations (skewed degrees), costs one L2 round trip per level otherwise
+  a.pre_read = opt.pre_read == 1 ? 1u : opt.pre_read == 2 ? 0u : (g->max_deg > 32 ? 1u : 0u);
 
   if ((e = cudaEventRecord(w->ev0, st))) return bail(e, "event");
   if ((e = launch_sssp(a, fused, G * ngroups, st))) return bail(e, "launch sssp_persistent");
@@ -436,6 +443,15 @@ gi_status gi_graph_create(int64_t n, int64_t m, const int64_t* row_offsets, cons
   uint32_t bad = 0;
   GI_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st), "copy flag");
   GI_CUDA(cudaStreamSynchronize(st), "graph validation");
+  if (!bad) {
+    GI_CUDA(cudaMalloc(&g->d_slots, sizeof(uint4) * 4 * (size_t)n), "alloc slots");
+    GI_CUDA(launch_build_slots(g->d_off, g->d_edges, g->d_slots, n, st), "build slots");
+    uint32_t* d_maxdeg = d_bad;  // reuse the flag word
+    GI_CUDA(cudaMemsetAsync(d_maxdeg, 0, 4, st), "memset");
+    GI_CUDA(launch_max_degree(g->d_off, n, d_maxdeg, st), "max degree");
+    GI_CUDA(cudaMemcpyAsync(&g->max_deg, d_maxdeg, 4, cudaMemcpyDeviceToHost, st), "copy max degree");
+    GI_CUDA(cudaStreamSynchronize(st), "graph build");
+  }
   if (bad) {
     cudaFree(g->d_off);
     cudaFree(g->d_edges);
@@ -453,6 +469,7 @@ void gi_graph_destroy(gi_graph* g) {
     g->pool.clear();
     cudaFree(g->d_off);
     cudaFree(g->d_edges);
+    cudaFree(g->d_slots);
   }
   delete g;
 }

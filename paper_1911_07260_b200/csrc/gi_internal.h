@@ -11,6 +11,10 @@ constexpr int kBinCap = 2048;        // entries per CTA-local bin (uint2 {v, d})
 constexpr uint32_t kDefaultT = 1024; // fusion threshold default (vertices per CTA bin)
 constexpr uint32_t kDefaultWarpMin = 32;
 constexpr uint32_t kDefaultCtaMin = 2048;
+constexpr int kSlotEdges = 8;        // ELL slot: up to 8 {col, w} edges inline (64 B per vertex)
+constexpr uint32_t kColEmpty = 0xFFFFFFFFu;  // unused slot entry
+constexpr uint32_t kColBig = 0xFFFFFFFEu;    // slot header of a vertex with deg > 8: {kColBig, deg, beg_lo, beg_hi}
+constexpr int kFarStage = 2048;      // CTA-local staging of far-pile pushes (flushed at phase end)
 
 // Division by the invariant Δ (Granlund & Montgomery 1994, round-up method):
 // q = (t + ((x - t) >> s1)) >> s2 with t = umulhi(mul, x).
@@ -63,8 +67,8 @@ struct GroupWs {
 };
 
 struct KArgs {
-  const int64_t* off;   // [n+1]
-  const uint2* edges;   // [m] {col, w} interleaved
+  const uint4* slots;   // [n][4] ELL adjacency slots (64 B per vertex)
+  const uint2* edges;   // [m] {col, w} interleaved CSR edges (vertices with deg > 8)
   int64_t n;
   uint32_t nwords;
   const int32_t* srcs;  // [nsrc] device
@@ -77,6 +81,7 @@ struct KArgs {
   FastDiv div;
   uint32_t T;           // fusion threshold (<= kBinCap)
   uint32_t deg_warp_min, deg_cta_min;
+  uint32_t pre_read;    // read dist[v] before atomicMin (filters atomics on skewed graphs)
 };
 
 // Host-side launchers (gi_kernels.cu).
@@ -84,6 +89,9 @@ cudaError_t launch_sssp(const KArgs& a, bool fused, int grid, cudaStream_t st);
 cudaError_t query_occupancy(bool fused, int* blocks_per_sm);
 cudaError_t launch_interleave(const int32_t* cols, const uint32_t* w, uint2* edges, int64_t count,
                               int64_t n, uint32_t* bad_flag, cudaStream_t st);
+cudaError_t launch_build_slots(const int64_t* off, const uint2* edges, uint4* slots, int64_t n,
+                               cudaStream_t st);
+cudaError_t launch_max_degree(const int64_t* off, int64_t n, uint32_t* max_deg, cudaStream_t st);
 cudaError_t launch_validate_offsets(const int64_t* off, int64_t n, int64_t m, uint32_t* bad_flag,
                                     cudaStream_t st);
 int smem_bytes();

@@ -45,7 +45,7 @@ class gi_options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("fusion", ctypes.c_int32),
                 ("fusion_threshold", ctypes.c_uint32), ("max_ctas", ctypes.c_int32),
                 ("deg_warp_min", ctypes.c_uint32), ("deg_cta_min", ctypes.c_uint32),
-                ("group_ctas", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p)]
+                ("group_ctas", ctypes.c_int32), ("pre_read", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p)]
 
 
 class gi_stats(ctypes.Structure):
@@ -112,7 +112,7 @@ def _ptr(x):
 
 
 def make_options(fusion=True, threshold=0, max_ctas=0, deg_warp_min=0, deg_cta_min=0, group_ctas=0,
-                 stream=None) -> gi_options:
+                 pre_read=0, stream=None) -> gi_options:
     o = gi_options()
     _lib.gi_options_default(ctypes.byref(o))
     o.fusion = 1 if fusion else 0
@@ -121,6 +121,7 @@ def make_options(fusion=True, threshold=0, max_ctas=0, deg_warp_min=0, deg_cta_m
     o.deg_warp_min = deg_warp_min
     o.deg_cta_min = deg_cta_min
     o.group_ctas = group_ctas
+    o.pre_read = pre_read
     if stream is not None:
         o.cuda_stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     return o
