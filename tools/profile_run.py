@@ -1,0 +1,21 @@
+"""Run a few queries of one config (for ncu / compute-sanitizer captures).
+usage: python tools/profile_run.py --config 2 --delta 65536 --reps 2 [--no-fusion]"""
+import argparse, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import gen
+from paper_1911_07260_b200 import gi
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--delta", type=int, default=1 << 16)
+ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--no-fusion", action="store_true")
+ap.add_argument("--threshold", type=int, default=0)
+ap.add_argument("--max-ctas", type=int, default=0)
+a = ap.parse_args()
+g = gen.config_graph(a.config)
+G = gi.Graph.from_csr(g)
+src = gen.config_source(a.config, g)
+for i in range(a.reps):
+    d, st = gi.sssp(G, src, a.delta, fusion=not a.no_fusion, threshold=a.threshold, max_ctas=a.max_ctas)
+    print(i, {k: st[k] for k in ("gpu_ms", "buckets", "rounds", "grid_syncs", "fused_subrounds", "spills", "ctas")})
