@@ -86,7 +86,7 @@ struct gi_graph {
   int64_t n = 0, m = 0;
   int64_t* d_off = nullptr;
   uint2* d_edges = nullptr;
-  uint4* d_slots = nullptr;  // ELL adjacency slots, 64 B per vertex
+  uint2* d_slots = nullptr;  // ELL adjacency slots, 64 B per vertex
   uint32_t max_deg = 0;
   int sm_count = 0;
   int bps_fused = 0, bps_plain = 0;  // co-resident CTAs per SM
@@ -444,7 +444,7 @@ gi_status gi_graph_create(int64_t n, int64_t m, const int64_t* row_offsets, cons
   GI_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st), "copy flag");
   GI_CUDA(cudaStreamSynchronize(st), "graph validation");
   if (!bad) {
-    GI_CUDA(cudaMalloc(&g->d_slots, sizeof(uint4) * 4 * (size_t)n), "alloc slots");
+    GI_CUDA(cudaMalloc(&g->d_slots, sizeof(uint2) * 8 * (size_t)n), "alloc slots");
     GI_CUDA(launch_build_slots(g->d_off, g->d_edges, g->d_slots, n, st), "build slots");
     uint32_t* d_maxdeg = d_bad;  // reuse the flag word
     GI_CUDA(cudaMemsetAsync(d_maxdeg, 0, 4, st), "memset");

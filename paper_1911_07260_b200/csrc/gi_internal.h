@@ -7,13 +7,14 @@ namespace gi {
 
 constexpr uint32_t kInf = 0xFFFFFFFFu;
 constexpr int kBlock = 512;          // threads per persistent CTA
-constexpr int kBinCap = 2048;        // entries per CTA-local bin (uint2 {v, d}); two bins per CTA
+constexpr int kBinCap = 2048;        // CTA-local current-bucket bin of uint2 {v, d}; two (ping-pong) per CTA
+constexpr int kBigCap = 64;          // CTA-local ring of high-degree vertices (<= one per octet per wave)
 constexpr uint32_t kDefaultT = 1024; // fusion threshold default (vertices per CTA bin)
 constexpr uint32_t kDefaultWarpMin = 32;
 constexpr uint32_t kDefaultCtaMin = 2048;
 constexpr int kSlotEdges = 8;        // ELL slot: up to 8 {col, w} edges inline (64 B per vertex)
 constexpr uint32_t kColEmpty = 0xFFFFFFFFu;  // unused slot entry
-constexpr uint32_t kColBig = 0xFFFFFFFEu;    // slot header of a vertex with deg > 8: {kColBig, deg, beg_lo, beg_hi}
+constexpr uint32_t kColBig = 0xFFFFFFFEu;    // deg > 8: all 8 entries {kColBig, payload}; payloads deg, beg_lo, beg_hi
 constexpr int kFarStage = 2048;      // CTA-local staging of far-pile pushes (flushed at phase end)
 
 // Division by the invariant Δ (Granlund & Montgomery 1994, round-up method):
@@ -42,10 +43,8 @@ struct alignas(128) Ctl {
   uint32_t xlive[3];    // live vertices extracted, by extraction mod 3
   uint32_t ovf_cand;    // some candidate distance >= UINT32_MAX was produced
   uint32_t pad0[19];
-  uint32_t bar_count;   // group barrier arrival counter (own 128 B line)
+  uint32_t bar;         // group barrier: arrivals (low 16 bits) | generation (high 16), own 128 B line
   uint32_t pad1[31];
-  uint32_t bar_gen;     // group barrier generation (own 128 B line)
-  uint32_t pad2[31];
 };
 
 // Per-source result record (device, copied back to gi_stats).
@@ -67,7 +66,7 @@ struct GroupWs {
 };
 
 struct KArgs {
-  const uint4* slots;   // [n][4] ELL adjacency slots (64 B per vertex)
+  const uint2* slots;   // [n][8] ELL adjacency slots (64 B per vertex)
   const uint2* edges;   // [m] {col, w} interleaved CSR edges (vertices with deg > 8)
   int64_t n;
   uint32_t nwords;
@@ -89,7 +88,7 @@ cudaError_t launch_sssp(const KArgs& a, bool fused, int grid, cudaStream_t st);
 cudaError_t query_occupancy(bool fused, int* blocks_per_sm);
 cudaError_t launch_interleave(const int32_t* cols, const uint32_t* w, uint2* edges, int64_t count,
                               int64_t n, uint32_t* bad_flag, cudaStream_t st);
-cudaError_t launch_build_slots(const int64_t* off, const uint2* edges, uint4* slots, int64_t n,
+cudaError_t launch_build_slots(const int64_t* off, const uint2* edges, uint2* slots, int64_t n,
                                cudaStream_t st);
 cudaError_t launch_max_degree(const int64_t* off, int64_t n, uint32_t* max_deg, cudaStream_t st);
 cudaError_t launch_validate_offsets(const int64_t* off, int64_t n, int64_t m, uint32_t* bad_flag,

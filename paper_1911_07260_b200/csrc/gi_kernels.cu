@@ -18,17 +18,20 @@
 //
 // and every phase then drains its CTA-local current-bucket bin in shared memory
 // while the bin stays below the threshold T — bucket fusion (kernel (c),
-// Fig. alg:eager_delta_stepping_merge). Edge relaxation
-// (kernel (b)) is degree-binned: CTA per vertex (deg >= deg_cta_min), warp per
-// vertex (deg >= deg_warp_min), thread per vertex otherwise; Dist[dst] =
-// min(Dist[dst], Dist[src]+w) is an atomicMin on uint32, issued
-// for all of a thread's edges before any result is consumed.
+// Fig. alg:eager_delta_stepping_merge).
+//
+// Edge relaxation (kernel (b)), Dist[dst] = min(Dist[dst], Dist[src]+w)
+// (PAPER.md:422), is an atomicMin on uint32 and is degree-binned:
+//   * deg <= 8: one OCTET (8 lanes) per vertex, lane k relaxes entry k of the
+//     vertex's 64-byte ELL slot (one coalesced 64 B load, one atomic per lane);
+//   * 8 < deg < deg_cta_min: one warp per vertex over the CSR edges;
+//   * deg >= deg_cta_min: the whole CTA per vertex.
 // Lowerings into a FUTURE bucket are appended once per vertex to the far pile
 // (dedup bit = reduceBucketUpdates; "a single bucket update
 // per vertex"), staged in shared memory and flushed at the phase
 // end, off the bucket's critical chain; lowerings into the CURRENT bucket go to
-// the CTA bin as (vertex, distance) pairs (eager) and the
-// vertex's adjacency slot is prefetched into L2 for the next sub-round.
+// the CTA ring as (vertex, distance) pairs (eager) and the
+// vertex's slot is prefetched into L2 for the next sub-round.
 #include "gi_internal.h"
 
 #include <cooperative_groups.h>
@@ -40,11 +43,44 @@ namespace {
 
 enum : uint32_t { MODE_ROUND = 0, MODE_EXTRACT = 1, MODE_DONE = 2, MODE_NONE = 3 };
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+#ifdef GI_TRACE
+// Debug builds only: cycles between trace points, accumulated by CTA 0 / thread 0 in
+// shared memory (so that tracing adds ~no latency) and flushed at kernel exit.
+__device__ unsigned long long g_trace[32];
+__shared__ unsigned long long s_trace[32];
+__shared__ long long s_trace_last;
+#define TRACE(k)                                                   \
+  do {                                                             \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                     \
+      long long t_ = clock64();                                    \
+      s_trace[k] += (unsigned long long)(t_ - s_trace_last);       \
+      s_trace[16 + (k)] += 1;                                      \
+      s_trace_last = t_;                                           \
+    }                                                              \
+  } while (0)
+#define TRACE_INIT()                                                          \
+  do {                                                                        \
+    if (threadIdx.x < 32) s_trace[threadIdx.x] = 0;                           \
+    if (threadIdx.x == 0) s_trace_last = clock64();                           \
+    __syncthreads();                                                          \
+  } while (0)
+#define TRACE_FLUSH()                                                         \
+  do {                                                                        \
+    if (blockIdx.x == 0 && threadIdx.x < 32) atomicAdd(&g_trace[threadIdx.x], s_trace[threadIdx.x]); \
+  } while (0)
+#else
+#define TRACE(k) do {} while (0)
+#define TRACE_INIT() do {} while (0)
+#define TRACE_FLUSH() do {} while (0)
+#endif
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // dist[] is written by atomics inside this kernel: read it coherently from L2,
 // never through the non-coherent/L1 path (SURVEY §7 hard part 1).
@@ -59,22 +95,22 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
   return (t + ((x - t) >> f.s1)) >> f.s2;
 }
 
-// Barrier over the CTAs of one group (all co-resident: cooperative launch).
-__device__ __forceinline__ void group_barrier(Ctl* ctl, uint32_t nblocks) {
+// Barrier over the G CTAs of one group (all co-resident: cooperative launch).
+// One word: arrivals in the low 16 bits, generation in the high 16; the last
+// arriver resets the count and bumps the generation with a single atomic.
+__device__ __forceinline__ void group_barrier(Ctl* ctl, uint32_t G) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t gen = ld_acquire(&ctl->bar_gen);
-    __threadfence();
-    const uint32_t arrived = atomicAdd(&ctl->bar_count, 1u);
-    if (arrived == nblocks - 1) {
-      atomicExch(&ctl->bar_count, 0u);
-      __threadfence();
-      atomicAdd(&ctl->bar_gen, 1u);
+    fence_acq_rel();  // publish this CTA's writes (cumulative over the bar.sync above)
+    const uint32_t old = atomicAdd(&ctl->bar, 1u);
+    if ((old & 0xFFFFu) == G - 1) {
+      atomicAdd(&ctl->bar, 0x10000u - G);
     } else {
-      while (ld_acquire(&ctl->bar_gen) == gen) {
+      const uint32_t gen = old >> 16;
+      while ((ld_relaxed(&ctl->bar) >> 16) == gen) {
       }
     }
-    __threadfence();
+    fence_acq_rel();
   }
   __syncthreads();
 }
@@ -86,13 +122,17 @@ __device__ __forceinline__ T warp_sum(T x) {
   return x;
 }
 
+struct BigEnt {
+  int64_t beg;
+  uint32_t deg;
+  uint32_t du;
+};
+
 struct Shared {
-  uint32_t outcnt;         // fill of the current-bucket bin
-  uint32_t farcnt;         // fill of the far staging buffer
+  uint32_t cnt3[3];         // current-bucket bin fills, rotating by sub-round
+  uint32_t bigtail;         // high-degree ring: monotonic fill counter
+  uint32_t farcnt;          // fill of the far staging buffer
   uint32_t mode, b, cnt;
-  int32_t claim;
-  uint32_t cdu;
-  int64_t cbeg, cend;
   uint32_t fmin;
   unsigned long long red[kBlock / 32];
   int32_t farstage[kFarStage];
@@ -101,7 +141,7 @@ struct Shared {
 // Everything a relaxation needs, held in registers for one phase.
 struct Ctx {
   uint32_t* dist;
-  const uint4* slots;
+  const uint2* slots;
   const uint2* edges;
   FastDiv div;
   uint32_t b;              // current bucket
@@ -113,8 +153,11 @@ struct Ctx {
   uint32_t* fcount_live;
   uint32_t* ovfbits;
   uint32_t* ovf_cand;
-  uint2* out;              // CTA-local current-bucket bin (shared memory)
+  uint2* out;              // CTA-local current-bucket bin receiving pushes (shared memory)
+  uint32_t* outcnt;        // its fill counter (shared memory)
+  BigEnt* big;             // CTA-local high-degree ring (shared memory)
   Shared* s;
+  uint32_t bighead;
   uint32_t my_fmin;        // thread-local min far bucket (reduced at phase end)
   bool pre_read;
 };
@@ -124,7 +167,7 @@ __device__ __forceinline__ void push_global(Ctx& c, int32_t v) {
   const uint32_t bit = 1u << (v & 31);
   const uint32_t old = atomicOr(&c.qbits_next[v >> 5], bit);
   if (!(old & bit)) {
-    prefetch_l2(c.slots + 4 * (size_t)v);
+    prefetch_l2(c.slots + 8 * (size_t)v);
     cg::coalesced_group g = cg::coalesced_threads();
     uint32_t base = 0;
     if (g.thread_rank() == 0) base = atomicAdd(c.qcount_next, g.size());
@@ -133,18 +176,18 @@ __device__ __forceinline__ void push_global(Ctx& c, int32_t v) {
   }
 }
 
-// Current-bucket push: CTA-local bin (fusion) or the global frontier.
+// Current-bucket push: CTA-local ring (fusion) or the global frontier.
 template <bool FUSED>
 __device__ __forceinline__ void push_cur(Ctx& c, int32_t v, uint32_t d) {
   if constexpr (FUSED) {
-    prefetch_l2(c.slots + 4 * (size_t)v);
+    prefetch_l2(c.slots + 8 * (size_t)v);
     cg::coalesced_group g = cg::coalesced_threads();
     uint32_t base = 0;
-    if (g.thread_rank() == 0) base = atomicAdd(&c.s->outcnt, g.size());
+    if (g.thread_rank() == 0) base = atomicAdd(c.outcnt, g.size());
     base = g.shfl(base, 0);
     const uint32_t pos = base + g.thread_rank();
     if (pos < (uint32_t)kBinCap) c.out[pos] = make_uint2((uint32_t)v, d);
-    else push_global(c, v);
+    else push_global(c, v);  // bin full: the vertex goes to the next group-wide round
   } else {
     push_global(c, v);
   }
@@ -176,125 +219,132 @@ __device__ __forceinline__ void push_far(Ctx& c, int32_t v, uint32_t bk) {
   else push_far_global(c, v);
 }
 
-__device__ __noinline__ void mark_overflow(Ctx& c, uint32_t v) {
-  atomicOr(&c.ovfbits[v >> 5], 1u << (v & 31));
-  atomicOr(c.ovf_cand, 1u);
+__device__ __noinline__ void mark_overflow(uint32_t* ovfbits, uint32_t* ovf_cand, uint32_t v) {
+  atomicOr(&ovfbits[v >> 5], 1u << (v & 31));
+  atomicOr(ovf_cand, 1u);
 }
 
-// Relax up to K edges (u -> e[k].x, weight e[k].y) from tentative distance du
-// (PAPER.md:422). All loads / atomics are issued before any result is consumed.
-template <bool FUSED, int K>
-__device__ __forceinline__ void relax_k(Ctx& c, uint32_t du, const uint2 (&e)[K], uint32_t valid) {
-  uint32_t nd[K];
-  uint32_t ok = 0;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    nd[k] = 0;
-    if (valid & (1u << k)) {
-      const uint64_t s = (uint64_t)du + (uint64_t)e[k].y;
-      if (s >= (uint64_t)kInf) mark_overflow(c, e[k].x);  // not representable
-      else { nd[k] = (uint32_t)s; ok |= 1u << k; }
-    }
-  }
-  if (c.pre_read) {
-    uint32_t cur[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) cur[k] = (ok & (1u << k)) ? ld_dist(c.dist + e[k].x) : 0u;
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-      if ((ok & (1u << k)) && !(nd[k] < cur[k])) ok &= ~(1u << k);
-  }
-  uint32_t old[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) old[k] = (ok & (1u << k)) ? atomicMin(c.dist + e[k].x, nd[k]) : 0u;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    if ((ok & (1u << k)) && nd[k] < old[k]) {
-      const uint32_t bk = fdiv(nd[k], c.div);
-      if (bk == c.b) push_cur<FUSED>(c, (int32_t)e[k].x, nd[k]);
-      else push_far(c, (int32_t)e[k].x, bk);  // bk > b: nd >= du >= bΔ
-    }
-  }
-}
-
-// Relax edges [beg, end) of the CSR with stride `stride` starting at beg+lane,
-// 4 per iteration per thread.
+// Relax up to 4 CSR edges per thread per iteration ([beg, end), stride `stride`
+// starting at beg+lane); all loads and atomics of an iteration are issued before
+// any result is consumed.
 template <bool FUSED>
 __device__ __forceinline__ void relax_range(Ctx& c, uint32_t du, int64_t beg, int64_t end, int lane,
                                             int stride) {
   for (int64_t e0 = beg + lane; e0 < end; e0 += 4 * (int64_t)stride) {
     uint2 e[4];
-    uint32_t valid = 0;
+    uint32_t nd[4], old[4];
+    uint32_t ok = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int64_t i = e0 + (int64_t)k * stride;
-      if (i < end) { e[k] = __ldg(c.edges + i); valid |= 1u << k; }
-      else e[k] = make_uint2(0, 0);
+      e[k] = i < end ? __ldg(c.edges + i) : make_uint2(0, 0);
+      nd[k] = du + e[k].y;
+      if (i < end) {
+        if (nd[k] < du || nd[k] == kInf) mark_overflow(c.ovfbits, c.ovf_cand, e[k].x);
+        else ok |= 1u << k;
+      }
     }
-    relax_k<FUSED, 4>(c, du, e, valid);
+    if (c.pre_read) {
+      uint32_t cur[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cur[k] = (ok & (1u << k)) ? ld_dist(c.dist + e[k].x) : 0u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (!(nd[k] < cur[k])) ok &= ~(1u << k);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) old[k] = (ok & (1u << k)) ? atomicMin(c.dist + e[k].x, nd[k]) : 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if ((ok & (1u << k)) && nd[k] < old[k]) {
+        const uint32_t bk = fdiv(nd[k], c.div);
+        if (bk == c.b) push_cur<FUSED>(c, (int32_t)e[k].x, nd[k]);
+        else push_far(c, (int32_t)e[k].x, bk);
+      }
+    }
   }
 }
 
-// One wave: every thread of the CTA holds at most one frontier entry (v, du).
-// Degree-binned relaxation (thread / warp / CTA per vertex).
+// One octet wave: the 8 lanes of an octet share one frontier entry (v, du); lane
+// k relaxes entry k of v's ELL slot. High-degree vertices (deg > 8) are queued in
+// the CTA's big ring. Returns whether this thread queued a big vertex.
 template <bool FUSED>
-__device__ __forceinline__ void relax_wave(Ctx& c, Shared& s, bool have, int32_t v, uint32_t du,
-                                           bool check_stale, uint32_t warp_min, uint32_t cta_min,
-                                           unsigned long long& nv, unsigned long long& ne) {
-  uint4 s0 = make_uint4(kColEmpty, kColEmpty, kColEmpty, kColEmpty), s1 = s0, s2 = s0, s3 = s0;
+__device__ __forceinline__ bool octet_wave(Ctx& c, bool have, int32_t v, uint32_t du, bool check_stale,
+                                           uint32_t& nv, uint32_t& ne) {
+  const uint32_t sub = threadIdx.x & 7;
+  uint2 e = make_uint2(kColEmpty, 0);
+  bool stale = false;
   if (have) {
-    const uint4* sp = c.slots + 4 * (size_t)v;
-    s0 = __ldg(sp); s1 = __ldg(sp + 1); s2 = __ldg(sp + 2); s3 = __ldg(sp + 3);
-    if (check_stale && ld_dist(c.dist + v) < du) have = false;  // a newer entry exists
+    e = __ldg(c.slots + 8 * (size_t)v + sub);
+    if (check_stale) stale = ld_dist(c.dist + v) < du;  // a newer entry exists
   }
-  const bool big = have && s0.x == kColBig;
-  int64_t deg = 0, beg = 0, end = 0;
-  uint2 e[8];
-  uint32_t valid = 0;
-  if (big) {
-    deg = s0.y;
-    beg = (int64_t)(((uint64_t)s0.w << 32) | s0.z);
-    end = beg + deg;
-  } else if (have) {
-    e[0] = make_uint2(s0.x, s0.y); e[1] = make_uint2(s0.z, s0.w);
-    e[2] = make_uint2(s1.x, s1.y); e[3] = make_uint2(s1.z, s1.w);
-    e[4] = make_uint2(s2.x, s2.y); e[5] = make_uint2(s2.z, s2.w);
-    e[6] = make_uint2(s3.x, s3.y); e[7] = make_uint2(s3.z, s3.w);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) valid |= (e[k].x != kColEmpty) ? (1u << k) : 0u;
-    deg = __popc(valid);
+  if (check_stale) {  // octet-uniform decision (lanes may observe different dist values)
+    const uint32_t sb = __ballot_sync(0xffffffffu, stale);
+    if ((sb >> (threadIdx.x & 24)) & 0xFFu) have = false;
   }
-  nv += have ? 1 : 0;
-  ne += (unsigned long long)deg;
-
-  // small vertex, adjacency inline in its slot: one thread
-  if (valid) relax_k<FUSED, 8>(c, du, e, valid);
-  if (!big) deg = 0;
-
-  // CTA per vertex
-  while (__syncthreads_or(deg >= (int64_t)cta_min)) {
-    if (deg >= (int64_t)cta_min) s.claim = (int32_t)threadIdx.x;
-    __syncthreads();
-    if (s.claim == (int32_t)threadIdx.x) {
-      s.cdu = du; s.cbeg = beg; s.cend = end;
-      deg = 0;
+  TRACE(2);
+  bool queued = false;
+  if (have && e.x == kColBig) {
+    const uint32_t om = 0xFFu << (threadIdx.x & 24);
+    const uint32_t lo = __shfl_sync(om, e.y, 1, 8);
+    const uint32_t hi = __shfl_sync(om, e.y, 2, 8);
+    if (sub == 0) {
+      const uint32_t pos = atomicAdd(&c.s->bigtail, 1u);
+      if (pos - c.bighead < (uint32_t)kBigCap) {
+        BigEnt be;
+        be.beg = (int64_t)(((uint64_t)hi << 32) | lo);
+        be.deg = e.y;
+        be.du = du;
+        c.big[pos & (kBigCap - 1)] = be;
+        queued = true;
+      } else {
+        push_global(c, v);  // big ring full: next group-wide round
+      }
+      ++nv;
     }
-    __syncthreads();
-    relax_range<FUSED>(c, s.cdu, s.cbeg, s.cend, threadIdx.x, kBlock);
   }
-  // warp per vertex
-  const int lane = threadIdx.x & 31;
-  uint32_t wm;
-  while ((wm = __ballot_sync(0xffffffffu, deg >= (int64_t)warp_min)) != 0) {
-    const int leader = __ffs(wm) - 1;
-    const uint32_t ldu = __shfl_sync(0xffffffffu, du, leader);
-    const int64_t lb = __shfl_sync(0xffffffffu, beg, leader);
-    const int64_t le = __shfl_sync(0xffffffffu, end, leader);
-    if (lane == leader) deg = 0;
-    relax_range<FUSED>(c, ldu, lb, le, lane, 32);
+  // small vertex: lane `sub` relaxes slot entry `sub`
+  if (have && e.x != kColBig) {
+    nv += sub == 0;
+    if (e.x != kColEmpty) {
+      ++ne;
+      const uint32_t nd = du + e.y;
+      if (nd < du || nd == kInf) {  // not representable; resolved at the end
+        mark_overflow(c.ovfbits, c.ovf_cand, e.x);
+      } else if (!c.pre_read || nd < ld_dist(c.dist + e.x)) {
+        const uint32_t old = atomicMin(c.dist + e.x, nd);
+        if (nd < old) {
+          const uint32_t bk = fdiv(nd, c.div);
+          if (bk == c.b) push_cur<FUSED>(c, (int32_t)e.x, nd);
+          else push_far(c, (int32_t)e.x, bk);  // bk > b: nd >= du >= bΔ
+        }
+      }
+    }
   }
-  // thread per vertex (deg > 8 but below the warp threshold)
-  if (deg > 0) relax_range<FUSED>(c, du, beg, end, 0, 1);
+  TRACE(3);
+  return queued;
+}
+
+// Relax the queued high-degree vertices [bighead, bighead + nb): CTA per vertex
+// for deg >= cta_min, warp per vertex otherwise.
+template <bool FUSED>
+__device__ __forceinline__ void big_relax(Ctx& c, uint32_t nb, uint32_t cta_min, uint32_t& ne) {
+  for (uint32_t i = 0; i < nb; ++i) {
+    const BigEnt be = c.big[(c.bighead + i) & (kBigCap - 1)];
+    if (be.deg >= cta_min) {
+      relax_range<FUSED>(c, be.du, be.beg, be.beg + be.deg, threadIdx.x, kBlock);
+      if (threadIdx.x == 0) ne += be.deg;
+    }
+  }
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t i = warp; i < nb; i += kBlock / 32) {
+    const BigEnt be = c.big[(c.bighead + i) & (kBigCap - 1)];
+    if (be.deg < cta_min) {
+      relax_range<FUSED>(c, be.du, be.beg, be.beg + be.deg, lane, 32);
+      if (lane == 0) ne += be.deg;
+    }
+  }
+  c.bighead += nb;
 }
 
 template <typename T>
@@ -313,7 +363,7 @@ __device__ __forceinline__ T block_sum(T x, Shared& s) {
 
 template <bool FUSED>
 __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
-  extern __shared__ uint2 s_bins[];  // [2 * kBinCap]
+  extern __shared__ uint2 s_dyn[];  // bins [2][kBinCap] uint2, then big ring [kBigCap] BigEnt
   __shared__ Shared s;
   const uint32_t G = (uint32_t)a.group_size;
   const uint32_t gid = blockIdx.x / G;
@@ -324,6 +374,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
   Ctl* ctl = ws.ctl;
   const int64_t n = a.n;
   const uint32_t T = a.T;
+  TRACE_INIT();
 
   for (int32_t si = (int32_t)gid; si < a.nsrc; si += a.ngroups) {
     uint32_t* dist = a.dist + (size_t)si * (size_t)n;
@@ -362,10 +413,12 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     Ctx c;
     c.dist = dist; c.slots = a.slots; c.edges = a.edges; c.div = a.div;
     c.farbits = ws.farbits; c.ovfbits = ws.ovfbits; c.ovf_cand = &ctl->ovf_cand;
+    c.big = reinterpret_cast<BigEnt*>(s_dyn + 2 * kBinCap);
     c.s = &s;
     c.pre_read = a.pre_read != 0;
 
-    unsigned long long nv = 0, ne = 0;            // per thread
+    uint32_t nv = 0, ne = 0;                       // per thread (flushed per phase)
+    unsigned long long tnv = 0, tne = 0;           // per thread, 64-bit totals
     unsigned long long subrounds = 0, spills = 0, scanned = 0;  // per CTA (thread 0)
     unsigned long long phases = 0, rounds = 0, buckets = 0, empty = 0;  // rank 0, thread 0
     uint32_t p = 0, j = 0, b = 0, prev = MODE_NONE;
@@ -373,25 +426,27 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     for (;;) {
       // ---- decide (identically in every CTA, from counters final at the barrier) ----
       if (tid == 0) {
+        // L2-coherent loads, all four in flight at once (ordered after the barrier's fence)
+        const uint32_t xl = __ldcg(&ctl->xlive[j % 3]);
+        const uint32_t qn = __ldcg(&ctl->qcount[p % 3]);
+        const uint32_t fc = __ldcg(&ctl->fcount[j % 3]);
+        const uint32_t fm = __ldcg(&ctl->fmin[j % 3]);
         if (prev == MODE_EXTRACT) {
-          const uint32_t xl = ld_acquire(&ctl->xlive[j % 3]);
           if (xl) { ++buckets; if (FUSED) ++rounds; } else { ++empty; }
         }
-        const uint32_t qn = ld_acquire(&ctl->qcount[p % 3]);
         uint32_t mode;
-        if (qn > 0) {
-          mode = MODE_ROUND; s.cnt = qn;
-        } else {
-          const uint32_t fc = ld_acquire(&ctl->fcount[j % 3]);
-          if (fc > 0) { mode = MODE_EXTRACT; s.cnt = fc; s.b = ld_acquire(&ctl->fmin[j % 3]); }
-          else mode = MODE_DONE;
-        }
+        if (qn > 0) { mode = MODE_ROUND; s.cnt = qn; }
+        else if (fc > 0) { mode = MODE_EXTRACT; s.cnt = fc; s.b = fm; }
+        else mode = MODE_DONE;
         s.mode = mode;
-        s.outcnt = 0;
+        s.cnt3[0] = 0;
+        s.cnt3[1] = 0;
+        s.bigtail = 0;
         s.farcnt = 0;
         s.fmin = kInf;
       }
       __syncthreads();
+      TRACE(5);
       const uint32_t mode = s.mode;
       if (mode == MODE_DONE) break;
       const uint32_t cnt = s.cnt;
@@ -404,12 +459,14 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
         if (mode == MODE_ROUND) ++rounds;
       }
       c.b = b;
-      c.qbits_next = ws.qbits[(p + 1) & 1];
-      c.q_next = ws.q[(p + 1) & 1];
+      c.qbits_next = (p & 1) ? ws.qbits[0] : ws.qbits[1];
+      c.q_next = (p & 1) ? ws.q[0] : ws.q[1];
       c.qcount_next = &ctl->qcount[(p + 1) % 3];
-      c.far_live = ws.far[j & 1];
+      c.far_live = (j & 1) ? ws.far[1] : ws.far[0];
       c.fcount_live = &ctl->fcount[j % 3];
-      c.out = s_bins;
+      c.out = s_dyn;  // the first stage fills bin 0 (counter cnt3[0])
+      c.outcnt = &s.cnt3[0];
+      c.bighead = 0;
       c.my_fmin = kInf;
 
       const uint32_t lo = (uint32_t)(((uint64_t)cnt * rank) / G);
@@ -417,7 +474,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
 
       if (mode == MODE_EXTRACT) {
         // (d)+(a): partition the far pile by recomputed bucket
-        const int32_t* far_src = ws.far[(j - 1) & 1];
+        const int32_t* far_src = (j & 1) ? ws.far[0] : ws.far[1];
         uint32_t nlive = 0;
         for (uint32_t i = lo + tid; i < hi; i += kBlock) {
           const int32_t v = far_src[i];
@@ -435,53 +492,72 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
             c.far_live[base + g.thread_rank()] = v;
           }
         }
-        const uint32_t tl = block_sum(nlive, s);
+        TRACE(6);
+        const uint32_t tl = block_sum(nlive, s);  // ends with a barrier: ring fill is final
         if (tid == 0) {
           if (tl) atomicAdd(&ctl->xlive[j % 3], tl);
           scanned += hi - lo;
         }
       } else {
-        // ROUND: relax the group's global frontier, one slice per CTA
-        const int32_t* q_in = ws.q[p & 1];
-        uint32_t* qbits_in = ws.qbits[p & 1];
-        for (uint32_t base = lo; base < hi; base += kBlock) {
-          const uint32_t i = base + tid;
+        // ROUND: relax the group's global frontier, one slice per CTA, 64 entries
+        // (one per octet) per wave
+        const int32_t* q_in = (p & 1) ? ws.q[1] : ws.q[0];
+        uint32_t* qbits_in = (p & 1) ? ws.qbits[1] : ws.qbits[0];
+        const uint32_t oct = tid >> 3;
+        for (uint32_t base = lo; base < hi; base += kBlock / 8) {
+          const uint32_t i = base + oct;
           const bool have = i < hi;
           int32_t v = 0;
           uint32_t du = 0;
           if (have) {
             v = q_in[i];
-            atomicAnd(&qbits_in[v >> 5], ~(1u << (v & 31)));
+            if ((tid & 7) == 0) atomicAnd(&qbits_in[v >> 5], ~(1u << (v & 31)));
             du = ld_dist(dist + v);
           }
-          relax_wave<FUSED>(c, s, have, v, du, false, a.deg_warp_min, a.deg_cta_min, nv, ne);
+          const bool q = octet_wave<FUSED>(c, have, v, du, false, nv, ne);
+          const uint32_t nbw = __syncthreads_count(q);
+          if (nbw) {
+            big_relax<FUSED>(c, nbw, a.deg_cta_min, ne);
+            __syncthreads();
+          }
         }
+        __syncthreads();
       }
 
       if constexpr (FUSED) {
         // (c) bucket fusion: drain the CTA-local bin while it stays below T
         // (PAPER.md:537-550); a bin of size >= T goes to the global frontier
-        // ("copied over to the global bucket").
-        uint2* in = s_bins + kBinCap;
-        for (;;) {
-          __syncthreads();
-          const uint32_t nout = min(s.outcnt, (uint32_t)kBinCap);
-          if (nout == 0) break;
-          if (nout >= T) {
-            for (uint32_t i = tid; i < nout; i += kBlock) push_global(c, (int32_t)c.out[i].x);
+        // ("copied over to the global bucket"). Sub-round k reads
+        // bin (k-1)%2 (fill cnt3[(k-1)%3]) and pushes into bin k%2 (fill cnt3[k%3]);
+        // cnt3[(k+1)%3] was last read at the top of sub-round k-1 and is reset here,
+        // so one barrier per sub-round suffices.
+        for (uint32_t k = 1;; ++k) {
+          // a barrier has completed: pushes of the previous sub-round are visible
+          TRACE(0);
+          const uint2* in = s_dyn + ((k - 1) & 1) * kBinCap;
+          const uint32_t nin = min(s.cnt3[(k - 1) % 3], (uint32_t)kBinCap);
+          if (nin == 0) break;
+          if (nin >= T) {
+            for (uint32_t i = tid; i < nin; i += kBlock) push_global(c, (int32_t)in[i].x);
             if (tid == 0) ++spills;
             break;
           }
-          uint2* t = in; in = c.out; c.out = t;
-          __syncthreads();
-          if (tid == 0) { s.outcnt = 0; ++subrounds; }
-          __syncthreads();
-          for (uint32_t base = 0; base < nout; base += kBlock) {
-            const uint32_t i = base + tid;
-            const bool have = i < nout;
-            uint2 e = make_uint2(0, 0);
-            if (have) e = in[i];
-            relax_wave<FUSED>(c, s, have, (int32_t)e.x, e.y, true, a.deg_warp_min, a.deg_cta_min, nv, ne);
+          if (tid == 0) { s.cnt3[(k + 1) % 3] = 0; ++subrounds; }
+          c.out = s_dyn + (k & 1) * kBinCap;
+          c.outcnt = &s.cnt3[k % 3];
+          const uint32_t oct = tid >> 3;
+          for (uint32_t base = 0; base < nin; base += kBlock / 8) {
+            const uint32_t i = base + oct;
+            const bool have = i < nin;
+            uint2 en = make_uint2(0, 0);
+            if (have) en = in[i];
+            const bool q = octet_wave<FUSED>(c, have, (int32_t)en.x, en.y, true, nv, ne);
+            const uint32_t nbw = __syncthreads_count(q);
+            TRACE(4);
+            if (nbw) {
+              big_relax<FUSED>(c, nbw, a.deg_cta_min, ne);
+              __syncthreads();
+            }
           }
         }
       }
@@ -489,6 +565,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
       // flush staged far-pile pushes (dedup + append), then the next-bucket lower
       // bound: warp min + one smem atomic per warp + one global atomic per CTA
       __syncthreads();
+      TRACE(7);
       {
         const uint32_t nf = min(s.farcnt, (uint32_t)kFarStage);
         for (uint32_t i = tid; i < nf; i += kBlock) push_far_global(c, s.farstage[i]);
@@ -497,7 +574,10 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
         __syncthreads();
         if (tid == 0 && s.fmin != kInf) atomicMin(&ctl->fmin[j % 3], s.fmin);
       }
+      tnv += nv; tne += ne; nv = 0; ne = 0;
+      TRACE(8);
       group_barrier(ctl, G);
+      TRACE(9);
       ++p;
       ++phases;
       prev = mode;
@@ -505,7 +585,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
 
     // ---- overflow resolution: a vertex with an overflowing candidate that never
     // received a representable distance has δ >= UINT32_MAX ----
-    if (ld_acquire(&ctl->ovf_cand)) {
+    if (ld_relaxed(&ctl->ovf_cand)) {
       uint32_t bad = 0;
       for (uint32_t wi = rank * kBlock + tid; wi < a.nwords; wi += G * kBlock) {
         uint32_t bits = ws.ovfbits[wi];
@@ -523,8 +603,8 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     }
 
     // ---- statistics ----
-    const unsigned long long tv = block_sum(nv, s);
-    const unsigned long long te = block_sum(ne, s);
+    const unsigned long long tv = block_sum(tnv, s);
+    const unsigned long long te = block_sum(tne, s);
     if (tid == 0) {
       QStats* q = &a.qstats[si];
       atomicAdd(&q->vertices, tv);
@@ -539,6 +619,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     }
     group_barrier(ctl, G);  // the next query re-initialises ctl
   }
+  TRACE_FLUSH();
 }
 
 __global__ void interleave_kernel(const int32_t* __restrict__ cols, const uint32_t* __restrict__ w,
@@ -551,10 +632,11 @@ __global__ void interleave_kernel(const int32_t* __restrict__ cols, const uint32
   }
 }
 
-// ELL slot per vertex: deg <= 8 -> edges inline (unused entries kColEmpty);
-// deg > 8 -> header {kColBig, deg, beg_lo, beg_hi} pointing into the CSR edges.
+// ELL slot per vertex (8 x {col, w}, 64 B): deg <= 8 -> edges inline, unused entries
+// kColEmpty; deg > 8 -> every entry {kColBig, payload} with payloads deg, beg_lo,
+// beg_hi in entries 0..2 (the CSR edges hold the adjacency).
 __global__ void build_slots_kernel(const int64_t* __restrict__ off, const uint2* __restrict__ edges,
-                                   uint4* __restrict__ slots, int64_t n) {
+                                   uint2* __restrict__ slots, int64_t n) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t beg = off[v], deg = off[v + 1] - beg;
@@ -564,11 +646,12 @@ __global__ void build_slots_kernel(const int64_t* __restrict__ off, const uint2*
       for (int k = 0; k < 8; ++k) e[k] = k < deg ? edges[beg + k] : make_uint2(kColEmpty, 0);
     } else {
       e[0] = make_uint2(kColBig, (uint32_t)deg);
-      e[1] = make_uint2((uint32_t)(uint64_t)beg, (uint32_t)((uint64_t)beg >> 32));
+      e[1] = make_uint2(kColBig, (uint32_t)(uint64_t)beg);
+      e[2] = make_uint2(kColBig, (uint32_t)((uint64_t)beg >> 32));
 #pragma unroll
-      for (int k = 2; k < 8; ++k) e[k] = make_uint2(kColEmpty, 0);
+      for (int k = 3; k < 8; ++k) e[k] = make_uint2(kColBig, 0);
     }
-    uint4* sp = slots + 4 * v;
+    uint4* sp = reinterpret_cast<uint4*>(slots + 8 * v);
     sp[0] = make_uint4(e[0].x, e[0].y, e[1].x, e[1].y);
     sp[1] = make_uint4(e[2].x, e[2].y, e[3].x, e[3].y);
     sp[2] = make_uint4(e[4].x, e[4].y, e[5].x, e[5].y);
@@ -598,7 +681,19 @@ __global__ void validate_offsets_kernel(const int64_t* __restrict__ off, int64_t
 
 }  // namespace
 
-int smem_bytes() { return 2 * kBinCap * (int)sizeof(uint2); }
+int smem_bytes() { return 2 * kBinCap * (int)sizeof(uint2) + kBigCap * (int)sizeof(BigEnt); }
+
+#ifdef GI_TRACE
+extern "C" int gi_debug_trace(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 32);
+  if (reset) {
+    unsigned long long z[32] = {0};
+    cudaMemcpyToSymbol(g_trace, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 static bool g_attr_set = false;
 
@@ -645,7 +740,7 @@ cudaError_t launch_interleave(const int32_t* cols, const uint32_t* w, uint2* edg
   return cudaGetLastError();
 }
 
-cudaError_t launch_build_slots(const int64_t* off, const uint2* edges, uint4* slots, int64_t n,
+cudaError_t launch_build_slots(const int64_t* off, const uint2* edges, uint2* slots, int64_t n,
                                cudaStream_t st) {
   build_slots_kernel<<<grid_for(n), 256, 0, st>>>(off, edges, slots, n);
   return cudaGetLastError();
