@@ -287,7 +287,7 @@ def main():
     s_last = stats[-1] if cfg != 5 else stats[-1][0]
     counters = {k: getattr(s_last, k) for k in ("buckets", "rounds", "grid_syncs", "kernel_launches",
                                                   "fused_subrounds", "spills", "vertices_processed",
-                                                  "edges_relaxed", "empty_extractions", "far_scanned",
+                                                  "edges_relaxed", "empty_extractions", "far_scanned", "critical_subrounds",
                                                   "ctas", "threads_per_cta", "groups")}
 
     # ---- fusion on vs off (untimed comparison run, same Δ) ----
@@ -302,7 +302,8 @@ def main():
             compare["fused" if fu else "unfused"] = {
                 "gpu_ms": statistics.median([x.gpu_ms for x in sts]), "buckets": s.buckets,
                 "rounds": s.rounds, "grid_syncs": s.grid_syncs, "kernel_launches": s.kernel_launches,
-                "fused_subrounds": s.fused_subrounds, "spills": s.spills}
+                "fused_subrounds": s.fused_subrounds, "spills": s.spills,
+                "critical_subrounds": s.critical_subrounds}
 
     # ---- e2e through the public C ABI with HOST buffers (pinned), copies inside ----
     e2e = None

@@ -116,6 +116,8 @@ typedef struct {
   uint64_t edges_relaxed;      /* out-edges scanned */
   uint64_t empty_extractions;  /* extractions whose bucket held only stale entries */
   uint64_t far_scanned;        /* far-pile (overflow bucket) entries scanned by extractions */
+  uint64_t critical_subrounds; /* sum over phases of the max fused sub-rounds run by one CTA
+                                  (the dependent chain the fused drain could not shorten) */
   float gpu_ms;                /* device time of the query (CUDA events, whole call for batch) */
   int32_t ctas;                /* persistent CTAs in the query's group */
   int32_t threads_per_cta;

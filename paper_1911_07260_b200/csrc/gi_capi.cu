@@ -199,6 +199,7 @@ void fill_stats(gi_stats* st, const QStats& q, float ms, int ctas, int groups) {
   st->edges_relaxed = q.edges;
   st->empty_extractions = q.empty_extr;
   st->far_scanned = q.far_scanned;
+  st->critical_subrounds = q.critical_subrounds;
   st->gpu_ms = ms;
   st->ctas = ctas;
   st->threads_per_cta = kBlock;

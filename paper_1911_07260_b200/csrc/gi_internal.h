@@ -42,7 +42,8 @@ struct alignas(128) Ctl {
   uint32_t fmin[3];     // lower bound of the min live far bucket, by extraction mod 3
   uint32_t xlive[3];    // live vertices extracted, by extraction mod 3
   uint32_t ovf_cand;    // some candidate distance >= UINT32_MAX was produced
-  uint32_t pad0[19];
+  uint32_t maxsub[3];   // max fused sub-rounds of any CTA, by phase mod 3 (critical-path stat)
+  uint32_t pad0[16];
   uint32_t bar;         // group barrier: arrivals (low 16 bits) | generation (high 16), own 128 B line
   uint32_t pad1[31];
 };
@@ -50,7 +51,7 @@ struct alignas(128) Ctl {
 // Per-source result record (device, copied back to gi_stats).
 struct QStats {
   unsigned long long buckets, rounds, phases, subrounds, spills, vertices, edges, empty_extr,
-      far_scanned;
+      far_scanned, critical_subrounds;
   uint32_t overflow;
   uint32_t pad;
 };

@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     }
     if (rank == 0 && tid == 0) {
       for (int k = 0; k < 3; ++k) {
-        ctl->qcount[k] = 0; ctl->fcount[k] = 0; ctl->fmin[k] = kInf; ctl->xlive[k] = 0;
+        ctl->qcount[k] = 0; ctl->fcount[k] = 0; ctl->fmin[k] = kInf; ctl->xlive[k] = 0; ctl->maxsub[k] = 0;
       }
       ctl->fcount[0] = 1; ctl->fmin[0] = 0; ctl->ovf_cand = 0;
       ws.far[0][0] = src;
@@ -420,7 +420,8 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     uint32_t nv = 0, ne = 0;                       // per thread (flushed per phase)
     unsigned long long tnv = 0, tne = 0;           // per thread, 64-bit totals
     unsigned long long subrounds = 0, spills = 0, scanned = 0;  // per CTA (thread 0)
-    unsigned long long phases = 0, rounds = 0, buckets = 0, empty = 0;  // rank 0, thread 0
+    unsigned long long phases = 0, rounds = 0, buckets = 0, empty = 0, critical = 0;  // rank 0, thread 0
+    unsigned long long sub_at_phase_start = 0;
     uint32_t p = 0, j = 0, b = 0, prev = MODE_NONE;
 
     for (;;) {
@@ -431,6 +432,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
         const uint32_t qn = __ldcg(&ctl->qcount[p % 3]);
         const uint32_t fc = __ldcg(&ctl->fcount[j % 3]);
         const uint32_t fm = __ldcg(&ctl->fmin[j % 3]);
+        if (p > 0 && rank == 0) critical += __ldcg(&ctl->maxsub[(p - 1) % 3]);
         if (prev == MODE_EXTRACT) {
           if (xl) { ++buckets; if (FUSED) ++rounds; } else { ++empty; }
         }
@@ -453,6 +455,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
       if (mode == MODE_EXTRACT) { ++j; b = s.b; }
       if (rank == 0 && tid == 0) {
         ctl->qcount[(p + 2) % 3] = 0;
+        ctl->maxsub[(p + 2) % 3] = 0;
         if (mode == MODE_EXTRACT) {
           ctl->fcount[(j + 1) % 3] = 0; ctl->fmin[(j + 1) % 3] = kInf; ctl->xlive[(j + 1) % 3] = 0;
         }
@@ -573,6 +576,10 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
         if ((tid & 31) == 0 && fm != kInf) atomicMin(&s.fmin, fm);
         __syncthreads();
         if (tid == 0 && s.fmin != kInf) atomicMin(&ctl->fmin[j % 3], s.fmin);
+        if (FUSED && tid == 0 && subrounds != sub_at_phase_start) {
+          atomicMax(&ctl->maxsub[p % 3], (uint32_t)(subrounds - sub_at_phase_start));
+          sub_at_phase_start = subrounds;
+        }
       }
       tnv += nv; tne += ne; nv = 0; ne = 0;
       TRACE(8);
@@ -615,6 +622,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
       if (rank == 0) {
         q->buckets = buckets; q->rounds = rounds; q->phases = phases + 2;  // + init and final barriers
         q->empty_extr = empty;
+        q->critical_subrounds = critical;
       }
     }
     group_barrier(ctl, G);  // the next query re-initialises ctl

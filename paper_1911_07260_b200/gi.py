@@ -53,7 +53,8 @@ class gi_stats(ctypes.Structure):
                 ("kernel_launches", ctypes.c_uint64), ("fused_subrounds", ctypes.c_uint64),
                 ("spills", ctypes.c_uint64), ("vertices_processed", ctypes.c_uint64),
                 ("edges_relaxed", ctypes.c_uint64), ("empty_extractions", ctypes.c_uint64),
-                ("far_scanned", ctypes.c_uint64), ("gpu_ms", ctypes.c_float), ("ctas", ctypes.c_int32),
+                ("far_scanned", ctypes.c_uint64), ("critical_subrounds", ctypes.c_uint64),
+                ("gpu_ms", ctypes.c_float), ("ctas", ctypes.c_int32),
                 ("threads_per_cta", ctypes.c_int32), ("groups", ctypes.c_int32)]
 
     def to_dict(self):
