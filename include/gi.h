@@ -95,8 +95,8 @@ typedef struct {
   uint32_t fusion_threshold; /* T: a CTA-local current-bucket bin of size >= T spills to the global
                                 frontier (PAPER.md:539 strict '<'); 0 = library default */
   int32_t max_ctas;          /* cap on persistent CTAs per query group (0 = all co-resident) */
-  uint32_t deg_warp_min;     /* out-degree >= this -> one warp per vertex (0 = default 32) */
-  uint32_t deg_cta_min;      /* out-degree >= this -> whole CTA per vertex (0 = default) */
+  uint32_t reserved0;        /* must be 0 */
+  uint32_t reserved1;        /* must be 0 */
   int32_t group_ctas;        /* batch only: CTAs per concurrent query group (0 = auto) */
   int32_t pre_read;          /* read dist[v] before atomicMin: 0 = auto (on when max out-degree > 32),
                                 1 = on, 2 = off */

@@ -308,10 +308,6 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   a.div = make_fastdiv(delta);
   a.T = opt.fusion_threshold ? opt.fusion_threshold : kDefaultT;
   if (a.T > (uint32_t)kBinCap) a.T = kBinCap;
-  a.deg_warp_min = opt.deg_warp_min ? opt.deg_warp_min : kDefaultWarpMin;
-  a.deg_cta_min = opt.deg_cta_min ? opt.deg_cta_min : kDefaultCtaMin;
-  if (a.deg_warp_min < 1) a.deg_warp_min = 1;
-  if (a.deg_cta_min < 1) a.deg_cta_min = 1;
   // pre-read dist[v] before the atomic: pays off when hubs attract many redundant
   // relaxations (skewed degrees), costs one L2 round trip per level otherwise
   a.pre_read = opt.pre_read == 1 ? 1u : opt.pre_read == 2 ? 0u : (g->max_deg > 32 ? 1u : 0u);

@@ -8,10 +8,8 @@ namespace gi {
 constexpr uint32_t kInf = 0xFFFFFFFFu;
 constexpr int kBlock = 512;          // threads per persistent CTA
 constexpr int kBinCap = 2048;        // CTA-local current-bucket bin of uint2 {v, d}; two (ping-pong) per CTA
-constexpr int kBigCap = 64;          // CTA-local ring of high-degree vertices (<= one per octet per wave)
+constexpr int kBigCap = 2048;        // CTA-local list of high-degree vertices (deg > 8) per bin
 constexpr uint32_t kDefaultT = 1024; // fusion threshold default (vertices per CTA bin)
-constexpr uint32_t kDefaultWarpMin = 32;
-constexpr uint32_t kDefaultCtaMin = 2048;
 constexpr int kSlotEdges = 8;        // ELL slot: up to 8 {col, w} edges inline (64 B per vertex)
 constexpr uint32_t kColEmpty = 0xFFFFFFFFu;  // unused slot entry
 constexpr uint32_t kColBig = 0xFFFFFFFEu;    // deg > 8: all 8 entries {kColBig, payload}; payloads deg, beg_lo, beg_hi
@@ -80,7 +78,6 @@ struct KArgs {
   int32_t group_size;   // CTAs per group
   FastDiv div;
   uint32_t T;           // fusion threshold (<= kBinCap)
-  uint32_t deg_warp_min, deg_cta_min;
   uint32_t pre_read;    // read dist[v] before atomicMin (filters atomics on skewed graphs)
 };
 

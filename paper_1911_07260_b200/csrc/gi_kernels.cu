@@ -23,9 +23,11 @@
 // Edge relaxation (kernel (b)), Dist[dst] = min(Dist[dst], Dist[src]+w)
 // (PAPER.md:422), is an atomicMin on uint32 and is degree-binned:
 //   * deg <= 8: one OCTET (8 lanes) per vertex, lane k relaxes entry k of the
-//     vertex's 64-byte ELL slot (one coalesced 64 B load, one atomic per lane);
-//   * 8 < deg < deg_cta_min: one warp per vertex over the CSR edges;
-//   * deg >= deg_cta_min: the whole CTA per vertex.
+//     vertex's 64-byte ELL slot (one coalesced 64 B load, one atomic per lane),
+//     several entries in flight per thread;
+//   * deg > 8: the vertex joins the CTA's high-degree list, whose concatenated
+//     edges are split evenly over all threads of the CTA (prefix sum + search),
+//     coalesced 8-byte {col, w} loads, 4 per thread per iteration.
 // Lowerings into a FUTURE bucket are appended once per vertex to the far pile
 // (dedup bit = reduceBucketUpdates; "a single bucket update
 // per vertex"), staged in shared memory and flushed at the phase
@@ -130,10 +132,11 @@ struct BigEnt {
 
 struct Shared {
   uint32_t cnt3[3];         // current-bucket bin fills, rotating by sub-round
-  uint32_t bigtail;         // high-degree ring: monotonic fill counter
+  uint32_t bigtail;         // fill of the high-degree list
   uint32_t farcnt;          // fill of the far staging buffer
   uint32_t mode, b, cnt;
   uint32_t fmin;
+  unsigned long long total; // edges of the high-degree list (exclusive-scan total)
   unsigned long long red[kBlock / 32];
   int32_t farstage[kFarStage];
 };
@@ -155,9 +158,9 @@ struct Ctx {
   uint32_t* ovf_cand;
   uint2* out;              // CTA-local current-bucket bin receiving pushes (shared memory)
   uint32_t* outcnt;        // its fill counter (shared memory)
-  BigEnt* big;             // CTA-local high-degree ring (shared memory)
+  BigEnt* big;             // CTA-local high-degree list (shared memory)
+  unsigned long long* pre; // exclusive prefix of its degrees (shared memory)
   Shared* s;
-  uint32_t bighead;
   uint32_t my_fmin;        // thread-local min far bucket (reduced at phase end)
   bool pre_read;
 };
@@ -224,127 +227,195 @@ __device__ __noinline__ void mark_overflow(uint32_t* ovfbits, uint32_t* ovf_cand
   atomicOr(ovf_cand, 1u);
 }
 
-// Relax up to 4 CSR edges per thread per iteration ([beg, end), stride `stride`
-// starting at beg+lane); all loads and atomics of an iteration are issued before
-// any result is consumed.
-template <bool FUSED>
-__device__ __forceinline__ void relax_range(Ctx& c, uint32_t du, int64_t beg, int64_t end, int lane,
-                                            int stride) {
-  for (int64_t e0 = beg + lane; e0 < end; e0 += 4 * (int64_t)stride) {
-    uint2 e[4];
-    uint32_t nd[4], old[4];
-    uint32_t ok = 0;
+// Relax K edges per thread (u -> e[k].x, weight e[k].y, from du[k]); lanes with
+// bit k of `valid` clear do nothing. Every load and atomic of the batch is issued
+// before any result is consumed (memory-level parallelism on the critical chain).
+template <bool FUSED, int K>
+__device__ __forceinline__ void relax_batch(Ctx& c, const uint2 (&e)[K], const uint32_t (&du)[K],
+                                            uint32_t valid) {
+  uint32_t nd[K], old[K];
+  uint32_t ok = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int64_t i = e0 + (int64_t)k * stride;
-      e[k] = i < end ? __ldg(c.edges + i) : make_uint2(0, 0);
-      nd[k] = du + e[k].y;
-      if (i < end) {
-        if (nd[k] < du || nd[k] == kInf) mark_overflow(c.ovfbits, c.ovf_cand, e[k].x);
-        else ok |= 1u << k;
-      }
+  for (int k = 0; k < K; ++k) {
+    nd[k] = du[k] + e[k].y;
+    if (valid & (1u << k)) {
+      if (nd[k] < du[k] || nd[k] == kInf) mark_overflow(c.ovfbits, c.ovf_cand, e[k].x);
+      else ok |= 1u << k;
     }
-    if (c.pre_read) {
-      uint32_t cur[4];
+  }
+  if (c.pre_read) {
+    uint32_t cur[K];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) cur[k] = (ok & (1u << k)) ? ld_dist(c.dist + e[k].x) : 0u;
+    for (int k = 0; k < K; ++k) cur[k] = (ok & (1u << k)) ? ld_dist(c.dist + e[k].x) : 0u;
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (!(nd[k] < cur[k])) ok &= ~(1u << k);
-    }
+    for (int k = 0; k < K; ++k)
+      if (!(nd[k] < cur[k])) ok &= ~(1u << k);
+  }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) old[k] = (ok & (1u << k)) ? atomicMin(c.dist + e[k].x, nd[k]) : 0u;
+  for (int k = 0; k < K; ++k) old[k] = (ok & (1u << k)) ? atomicMin(c.dist + e[k].x, nd[k]) : 0u;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if ((ok & (1u << k)) && nd[k] < old[k]) {
-        const uint32_t bk = fdiv(nd[k], c.div);
-        if (bk == c.b) push_cur<FUSED>(c, (int32_t)e[k].x, nd[k]);
-        else push_far(c, (int32_t)e[k].x, bk);
-      }
+  for (int k = 0; k < K; ++k) {
+    if ((ok & (1u << k)) && nd[k] < old[k]) {
+      const uint32_t bk = fdiv(nd[k], c.div);
+      if (bk == c.b) push_cur<FUSED>(c, (int32_t)e[k].x, nd[k]);
+      else push_far(c, (int32_t)e[k].x, bk);  // bk > b: nd >= du >= bΔ
     }
   }
 }
 
-// One octet wave: the 8 lanes of an octet share one frontier entry (v, du); lane
-// k relaxes entry k of v's ELL slot. High-degree vertices (deg > 8) are queued in
-// the CTA's big ring. Returns whether this thread queued a big vertex.
-template <bool FUSED>
-__device__ __forceinline__ bool octet_wave(Ctx& c, bool have, int32_t v, uint32_t du, bool check_stale,
-                                           uint32_t& nv, uint32_t& ne) {
+// Stage A — vertices with deg <= 8: ITEMS (entry, slot index), 8 per frontier entry;
+// the 8 lanes of an octet share one entry and lane k relaxes entry k of its 64-byte
+// ELL slot (one coalesced 64 B load per octet). Each thread holds U items in flight.
+// Vertices with deg > 8 are appended to the CTA's high-degree list for stage B.
+template <bool FUSED, int U>
+__device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t nin, bool check_stale,
+                                            uint32_t& nv, uint32_t& ne) {
+  const uint32_t nitems = nin * 8;
   const uint32_t sub = threadIdx.x & 7;
-  uint2 e = make_uint2(kColEmpty, 0);
-  bool stale = false;
-  if (have) {
-    e = __ldg(c.slots + 8 * (size_t)v + sub);
-    if (check_stale) stale = ld_dist(c.dist + v) < du;  // a newer entry exists
-  }
-  if (check_stale) {  // octet-uniform decision (lanes may observe different dist values)
-    const uint32_t sb = __ballot_sync(0xffffffffu, stale);
-    if ((sb >> (threadIdx.x & 24)) & 0xFFu) have = false;
-  }
-  TRACE(2);
-  bool queued = false;
-  if (have && e.x == kColBig) {
-    const uint32_t om = 0xFFu << (threadIdx.x & 24);
-    const uint32_t lo = __shfl_sync(om, e.y, 1, 8);
-    const uint32_t hi = __shfl_sync(om, e.y, 2, 8);
-    if (sub == 0) {
-      const uint32_t pos = atomicAdd(&c.s->bigtail, 1u);
-      if (pos - c.bighead < (uint32_t)kBigCap) {
-        BigEnt be;
-        be.beg = (int64_t)(((uint64_t)hi << 32) | lo);
-        be.deg = e.y;
-        be.du = du;
-        c.big[pos & (kBigCap - 1)] = be;
-        queued = true;
-      } else {
-        push_global(c, v);  // big ring full: next group-wide round
+  for (uint32_t base = 0; base < nitems; base += kBlock * U) {
+    uint2 e[U];
+    uint32_t du[U], v[U];
+    uint32_t have = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t item = base + u * kBlock + threadIdx.x;
+      e[u] = make_uint2(kColEmpty, 0);
+      du[u] = 0; v[u] = 0;
+      if (item < nitems) {
+        const uint2 en = in[item >> 3];
+        v[u] = en.x; du[u] = en.y;
+        e[u] = __ldg(c.slots + 8 * (size_t)en.x + sub);
+        have |= 1u << u;
       }
-      ++nv;
     }
-  }
-  // small vertex: lane `sub` relaxes slot entry `sub`
-  if (have && e.x != kColBig) {
-    nv += sub == 0;
-    if (e.x != kColEmpty) {
-      ++ne;
-      const uint32_t nd = du + e.y;
-      if (nd < du || nd == kInf) {  // not representable; resolved at the end
-        mark_overflow(c.ovfbits, c.ovf_cand, e.x);
-      } else if (!c.pre_read || nd < ld_dist(c.dist + e.x)) {
-        const uint32_t old = atomicMin(c.dist + e.x, nd);
-        if (nd < old) {
-          const uint32_t bk = fdiv(nd, c.div);
-          if (bk == c.b) push_cur<FUSED>(c, (int32_t)e.x, nd);
-          else push_far(c, (int32_t)e.x, bk);  // bk > b: nd >= du >= bΔ
+    if (check_stale) {  // a newer entry for v exists; octet-uniform decision
+      uint32_t cur[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[u] = (have & (1u << u)) ? ld_dist(c.dist + v[u]) : kInf;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t sb = __ballot_sync(0xffffffffu, cur[u] < du[u]);
+        if ((sb >> (threadIdx.x & 24)) & 0xFFu) have &= ~(1u << u);
+      }
+    }
+    TRACE(2);
+    uint32_t valid = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!(have & (1u << u))) continue;
+      if (e[u].x == kColBig) {  // octet-uniform: every entry of a big slot is kColBig
+        const uint32_t om = 0xFFu << (threadIdx.x & 24);
+        const uint32_t lo = __shfl_sync(om, e[u].y, 1, 8);
+        const uint32_t hi = __shfl_sync(om, e[u].y, 2, 8);
+        if (sub == 0) {
+          ++nv;
+          const uint32_t pos = atomicAdd(&c.s->bigtail, 1u);
+          if (pos < (uint32_t)kBigCap) {
+            BigEnt be;
+            be.beg = (int64_t)(((uint64_t)hi << 32) | lo);
+            be.deg = e[u].y;
+            be.du = du[u];
+            c.big[pos] = be;
+          } else {
+            push_global(c, (int32_t)v[u]);  // list full: the next group-wide round takes it
+          }
         }
+      } else {
+        nv += sub == 0;
+        if (e[u].x != kColEmpty) { valid |= 1u << u; ++ne; }
       }
     }
+    relax_batch<FUSED, U>(c, e, du, valid);
+    TRACE(3);
   }
-  TRACE(3);
-  return queued;
 }
 
-// Relax the queued high-degree vertices [bighead, bighead + nb): CTA per vertex
-// for deg >= cta_min, warp per vertex otherwise.
+// Stage B — vertices with deg > 8: their edges are concatenated (exclusive prefix of
+// the degrees) and split evenly over all threads of the CTA, 4 edges per thread per
+// iteration; an edge finds its vertex by binary search in the prefix array.
 template <bool FUSED>
-__device__ __forceinline__ void big_relax(Ctx& c, uint32_t nb, uint32_t cta_min, uint32_t& ne) {
-  for (uint32_t i = 0; i < nb; ++i) {
-    const BigEnt be = c.big[(c.bighead + i) & (kBigCap - 1)];
-    if (be.deg >= cta_min) {
-      relax_range<FUSED>(c, be.du, be.beg, be.beg + be.deg, threadIdx.x, kBlock);
-      if (threadIdx.x == 0) ne += be.deg;
-    }
+__device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32_t& ne) {
+  constexpr int PER = kBigCap / kBlock;
+  unsigned long long loc[PER];
+  unsigned long long sum = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const uint32_t i = threadIdx.x * PER + k;
+    loc[k] = sum;
+    sum += i < nb ? c.big[i].deg : 0u;
   }
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (uint32_t i = warp; i < nb; i += kBlock / 32) {
-    const BigEnt be = c.big[(c.bighead + i) & (kBigCap - 1)];
-    if (be.deg < cta_min) {
-      relax_range<FUSED>(c, be.du, be.beg, be.beg + be.deg, lane, 32);
-      if (lane == 0) ne += be.deg;
-    }
+  // block exclusive scan of the per-thread sums
+  unsigned long long incl = sum;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += t;
   }
-  c.bighead += nb;
+  if (lane == 31) s.red[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long w = lane < kBlock / 32 ? s.red[lane] : 0ull;
+    unsigned long long wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= (uint32_t)o) wi += t;
+    }
+    if (lane < kBlock / 32) s.red[lane] = wi - w;  // exclusive warp offsets
+    if (lane == kBlock / 32 - 1) s.total = wi;
+  }
+  __syncthreads();
+  const unsigned long long off = s.red[warp] + incl - sum;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const uint32_t i = threadIdx.x * PER + k;
+    if (i < nb) c.pre[i] = off + loc[k];
+  }
+  __syncthreads();
+  const unsigned long long total = s.total;
+  if (threadIdx.x == 0) ne += (uint32_t)total;
+  for (unsigned long long k0 = 0; k0 < total; k0 += 4ull * kBlock) {
+    uint2 e[4];
+    uint32_t du[4];
+    uint32_t valid = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const unsigned long long k = k0 + (unsigned long long)u * kBlock + threadIdx.x;
+      e[u] = make_uint2(0, 0);
+      du[u] = 0;
+      if (k < total) {
+        uint32_t lo = 0, hi = nb;  // last i with pre[i] <= k
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (c.pre[mid] <= k) lo = mid; else hi = mid;
+        }
+        const BigEnt be = c.big[lo];
+        e[u] = __ldg(c.edges + be.beg + (int64_t)(k - c.pre[lo]));
+        du[u] = be.du;
+        valid |= 1u << u;
+      }
+    }
+    relax_batch<FUSED, 4>(c, e, du, valid);
+  }
+}
+
+// Relax every entry of a CTA-local bin (stage A, then stage B when high-degree
+// vertices were found). Starts after and ends with a CTA barrier.
+template <bool FUSED>
+__device__ __forceinline__ void process_bin(Ctx& c, Shared& s, const uint2* in, uint32_t nin,
+                                            bool check_stale, uint32_t& nv, uint32_t& ne) {
+  if (nin * 8 <= (uint32_t)kBlock) stage_small<FUSED, 1>(c, in, nin, check_stale, nv, ne);
+  else stage_small<FUSED, 4>(c, in, nin, check_stale, nv, ne);
+  __syncthreads();
+  TRACE(4);
+  const uint32_t nb = min(s.bigtail, (uint32_t)kBigCap);
+  if (nb) {
+    __syncthreads();  // everyone has read bigtail
+    if (threadIdx.x == 0) s.bigtail = 0;
+    stage_big<FUSED>(c, s, nb, ne);
+    __syncthreads();
+  }
 }
 
 template <typename T>
@@ -363,7 +434,7 @@ __device__ __forceinline__ T block_sum(T x, Shared& s) {
 
 template <bool FUSED>
 __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
-  extern __shared__ uint2 s_dyn[];  // bins [2][kBinCap] uint2, then big ring [kBigCap] BigEnt
+  extern __shared__ uint2 s_dyn[];  // bins [2][kBinCap] uint2, high-degree list [kBigCap], its prefix [kBigCap]
   __shared__ Shared s;
   const uint32_t G = (uint32_t)a.group_size;
   const uint32_t gid = blockIdx.x / G;
@@ -414,6 +485,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     c.dist = dist; c.slots = a.slots; c.edges = a.edges; c.div = a.div;
     c.farbits = ws.farbits; c.ovfbits = ws.ovfbits; c.ovf_cand = &ctl->ovf_cand;
     c.big = reinterpret_cast<BigEnt*>(s_dyn + 2 * kBinCap);
+    c.pre = reinterpret_cast<unsigned long long*>(c.big + kBigCap);
     c.s = &s;
     c.pre_read = a.pre_read != 0;
 
@@ -469,7 +541,6 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
       c.fcount_live = &ctl->fcount[j % 3];
       c.out = s_dyn;  // the first stage fills bin 0 (counter cnt3[0])
       c.outcnt = &s.cnt3[0];
-      c.bighead = 0;
       c.my_fmin = kInf;
 
       const uint32_t lo = (uint32_t)(((uint64_t)cnt * rank) / G);
@@ -502,27 +573,20 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
           scanned += hi - lo;
         }
       } else {
-        // ROUND: relax the group's global frontier, one slice per CTA, 64 entries
-        // (one per octet) per wave
+        // ROUND: relax the group's global frontier, one slice per CTA, staged through
+        // bin 1 in chunks (pushes go to bin 0, which the drain below consumes)
         const int32_t* q_in = (p & 1) ? ws.q[1] : ws.q[0];
         uint32_t* qbits_in = (p & 1) ? ws.qbits[1] : ws.qbits[0];
-        const uint32_t oct = tid >> 3;
-        for (uint32_t base = lo; base < hi; base += kBlock / 8) {
-          const uint32_t i = base + oct;
-          const bool have = i < hi;
-          int32_t v = 0;
-          uint32_t du = 0;
-          if (have) {
-            v = q_in[i];
-            if ((tid & 7) == 0) atomicAnd(&qbits_in[v >> 5], ~(1u << (v & 31)));
-            du = ld_dist(dist + v);
+        uint2* stage = s_dyn + kBinCap;
+        for (uint32_t base = lo; base < hi; base += kBinCap) {
+          const uint32_t chunk = min((uint32_t)kBinCap, hi - base);
+          for (uint32_t i = tid; i < chunk; i += kBlock) {
+            const int32_t v = q_in[base + i];
+            atomicAnd(&qbits_in[v >> 5], ~(1u << (v & 31)));
+            stage[i] = make_uint2((uint32_t)v, ld_dist(dist + v));
           }
-          const bool q = octet_wave<FUSED>(c, have, v, du, false, nv, ne);
-          const uint32_t nbw = __syncthreads_count(q);
-          if (nbw) {
-            big_relax<FUSED>(c, nbw, a.deg_cta_min, ne);
-            __syncthreads();
-          }
+          __syncthreads();
+          process_bin<FUSED>(c, s, stage, chunk, false, nv, ne);
         }
         __syncthreads();
       }
@@ -548,20 +612,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
           if (tid == 0) { s.cnt3[(k + 1) % 3] = 0; ++subrounds; }
           c.out = s_dyn + (k & 1) * kBinCap;
           c.outcnt = &s.cnt3[k % 3];
-          const uint32_t oct = tid >> 3;
-          for (uint32_t base = 0; base < nin; base += kBlock / 8) {
-            const uint32_t i = base + oct;
-            const bool have = i < nin;
-            uint2 en = make_uint2(0, 0);
-            if (have) en = in[i];
-            const bool q = octet_wave<FUSED>(c, have, (int32_t)en.x, en.y, true, nv, ne);
-            const uint32_t nbw = __syncthreads_count(q);
-            TRACE(4);
-            if (nbw) {
-              big_relax<FUSED>(c, nbw, a.deg_cta_min, ne);
-              __syncthreads();
-            }
-          }
+          process_bin<FUSED>(c, s, in, nin, true, nv, ne);
         }
       }
 
@@ -689,7 +740,9 @@ __global__ void validate_offsets_kernel(const int64_t* __restrict__ off, int64_t
 
 }  // namespace
 
-int smem_bytes() { return 2 * kBinCap * (int)sizeof(uint2) + kBigCap * (int)sizeof(BigEnt); }
+int smem_bytes() {
+  return 2 * kBinCap * (int)sizeof(uint2) + kBigCap * ((int)sizeof(BigEnt) + (int)sizeof(unsigned long long));
+}
 
 #ifdef GI_TRACE
 extern "C" int gi_debug_trace(unsigned long long* out, int reset) {

@@ -44,7 +44,7 @@ class OverflowDistance(GiError):
 class gi_options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("fusion", ctypes.c_int32),
                 ("fusion_threshold", ctypes.c_uint32), ("max_ctas", ctypes.c_int32),
-                ("deg_warp_min", ctypes.c_uint32), ("deg_cta_min", ctypes.c_uint32),
+                ("reserved0", ctypes.c_uint32), ("reserved1", ctypes.c_uint32),
                 ("group_ctas", ctypes.c_int32), ("pre_read", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p)]
 
 
@@ -112,15 +112,13 @@ def _ptr(x):
     raise TypeError(type(x))
 
 
-def make_options(fusion=True, threshold=0, max_ctas=0, deg_warp_min=0, deg_cta_min=0, group_ctas=0,
-                 pre_read=0, stream=None) -> gi_options:
+def make_options(fusion=True, threshold=0, max_ctas=0, group_ctas=0, pre_read=0,
+                 stream=None) -> gi_options:
     o = gi_options()
     _lib.gi_options_default(ctypes.byref(o))
     o.fusion = 1 if fusion else 0
     o.fusion_threshold = threshold
     o.max_ctas = max_ctas
-    o.deg_warp_min = deg_warp_min
-    o.deg_cta_min = deg_cta_min
     o.group_ctas = group_ctas
     o.pre_read = pre_read
     if stream is not None:

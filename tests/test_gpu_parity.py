@@ -37,7 +37,7 @@ def run(gi, G, src, delta, **opts):
 
 OPTS = [dict(fusion=True), dict(fusion=False), dict(fusion=True, threshold=2),
         dict(fusion=True, max_ctas=1), dict(fusion=False, max_ctas=3),
-        dict(fusion=True, deg_warp_min=2, deg_cta_min=3)]
+        dict(fusion=True, pre_read=1), dict(fusion=False, pre_read=2)]
 
 
 @pytest.mark.parametrize("ex", GOLDEN, ids=[e["name"] for e in GOLDEN])
@@ -211,3 +211,22 @@ def test_config5_batch(gi, config_graph):
     assert np.array_equal(got[idx], refs)
     for i in range(64):
         assert st[i]["buckets"] > 0
+
+
+def test_hubs_and_mixed_degrees(gi):
+    """High-degree vertices (deg > 8) take the CTA-wide edge-balanced path; a hub of
+    degree 120,000 and many medium vertices exercise prefix sums and the search."""
+    rng = np.random.default_rng(11)
+    n = 150_000
+    edges = [(0, int(v), int(rng.integers(1, 100))) for v in rng.choice(np.arange(1, n), 120_000, replace=False)]
+    for _ in range(300_000):
+        u, v = int(rng.integers(0, n)), int(rng.integers(0, n))
+        edges.append((u, v, int(rng.integers(0, 30))))
+    g = gen.from_edges(n, edges)
+    G = gi.Graph.from_csr(g)
+    for s in (0, 7):
+        ref, _ = oracle.dijkstra(g, s)
+        for o, delta in ((dict(fusion=True), 1), (dict(fusion=True), 64), (dict(fusion=False), 8),
+                         (dict(fusion=True, pre_read=2), 3), (dict(fusion=True, max_ctas=2), 1 << 20)):
+            d, _ = run(gi, G, s, delta, **o)
+            assert np.array_equal(d, ref), (s, o, delta)
