@@ -206,15 +206,16 @@ def main():
                 group_ctas=args.group_ctas, stream=stream)
 
     if cfg == 5:
+        from paper_1911_07260_b200.dist import padded_shard
         srcs_all = gen.config_sources(5, g, 64)
-        per = len(srcs_all) // world
-        srcs = torch.from_numpy(srcs_all[rank * per:(rank + 1) * per].copy())
-        out = torch.empty((per, g.n), dtype=torch.int32, device="cuda")
-        gathered = torch.empty((per * world, g.n), dtype=torch.int32, device="cuda") if world > 1 else out
+        mine, _ = padded_shard(srcs_all, rank, world)  # contiguous block of the 64 sources
+        srcs = torch.from_numpy(mine)
+        out = torch.empty((mine.shape[0], g.n), dtype=torch.int32, device="cuda")
+        gathered = torch.empty((mine.shape[0] * world, g.n), dtype=torch.int32, device="cuda") if world > 1 else out
 
         def step():
             st = gi.gi_sssp_batch(G, srcs, delta, out, gi.make_options(**opts))
-            if world > 1:
+            if world > 1:  # the one data-path collective: NCCL all-gather of the uint32 rows
                 dist.all_gather_into_tensor(gathered, out)
             return st
         units_per_step = len(srcs_all) * g.m  # whole job: all 64 sources
