@@ -230,6 +230,7 @@ __device__ __noinline__ void mark_overflow(uint32_t* ovfbits, uint32_t* ovf_cand
 // Relax K edges per thread (u -> e[k].x, weight e[k].y, from du[k]); lanes with
 // bit k of `valid` clear do nothing. Every load and atomic of the batch is issued
 // before any result is consumed (memory-level parallelism on the critical chain).
+// Must be called by all 32 lanes of the warp (the appends are warp-aggregated).
 template <bool FUSED, int K>
 __device__ __forceinline__ void relax_batch(Ctx& c, const uint2 (&e)[K], const uint32_t (&du)[K],
                                             uint32_t valid) {
@@ -253,12 +254,68 @@ __device__ __forceinline__ void relax_batch(Ctx& c, const uint2 (&e)[K], const u
   }
 #pragma unroll
   for (int k = 0; k < K; ++k) old[k] = (ok & (1u << k)) ? atomicMin(c.dist + e[k].x, nd[k]) : 0u;
+  // classify the successful lowerings: current bucket (bin) or a future one (far pile)
+  uint32_t curm = 0, farm = 0;
+  uint32_t bk[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
+    bk[k] = fdiv(nd[k], c.div);
     if ((ok & (1u << k)) && nd[k] < old[k]) {
-      const uint32_t bk = fdiv(nd[k], c.div);
-      if (bk == c.b) push_cur<FUSED>(c, (int32_t)e[k].x, nd[k]);
-      else push_far(c, (int32_t)e[k].x, bk);  // bk > b: nd >= du >= bΔ
+      if (bk[k] == c.b) curm |= 1u << k;
+      else farm |= 1u << k;  // bk > b: nd >= du >= bΔ
+    }
+  }
+  // warp-aggregated appends: one ballot per item slot, one shared atomic per warp
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  if constexpr (FUSED) {
+    uint32_t mk[K], pre[K], tot = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      mk[k] = __ballot_sync(0xffffffffu, (curm >> k) & 1u);
+      pre[k] = tot;
+      tot += __popc(mk[k]);
+    }
+    if (tot) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(c.outcnt, tot);
+      base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if ((curm >> k) & 1u) {
+          const uint32_t pos = base + pre[k] + __popc(mk[k] & lt);
+          prefetch_l2(c.slots + 8 * (size_t)e[k].x);
+          if (pos < (uint32_t)kBinCap) c.out[pos] = make_uint2(e[k].x, nd[k]);
+          else push_global(c, (int32_t)e[k].x);  // bin full: next group-wide round
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if ((curm >> k) & 1u) push_global(c, (int32_t)e[k].x);
+  }
+  {
+    uint32_t mk[K], pre[K], tot = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      mk[k] = __ballot_sync(0xffffffffu, (farm >> k) & 1u);
+      pre[k] = tot;
+      tot += __popc(mk[k]);
+    }
+    if (tot) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&c.s->farcnt, tot);
+      base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if ((farm >> k) & 1u) {
+          c.my_fmin = min(c.my_fmin, bk[k]);
+          const uint32_t pos = base + pre[k] + __popc(mk[k] & lt);
+          if (pos < (uint32_t)kFarStage) c.s->farstage[pos] = (int32_t)e[k].x;
+          else push_far_global(c, (int32_t)e[k].x);
+        }
+      }
     }
   }
 }
