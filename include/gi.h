@@ -95,7 +95,9 @@ typedef struct {
   uint32_t fusion_threshold; /* T: a CTA-local current-bucket bin of size >= T spills to the global
                                 frontier (PAPER.md:539 strict '<'); 0 = library default */
   int32_t max_ctas;          /* cap on persistent CTAs per query group (0 = all co-resident) */
-  uint32_t reserved0;        /* must be 0 */
+  uint32_t hub_min;          /* out-degree >= hub_min: the vertex's edges are split over every CTA of
+                                the group in the next phase (0 = default 4096; values < 1024 are
+                                raised to 1024) */
   uint32_t reserved1;        /* must be 0 */
   int32_t group_ctas;        /* batch only: CTAs per concurrent query group (0 = auto) */
   int32_t pre_read;          /* read dist[v] before atomicMin: 0 = auto (on when max out-degree > 32),

@@ -3,6 +3,7 @@
 #include "gi.h"
 #include "gi_internal.h"
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -55,6 +56,7 @@ bool is_device_ptr(const void* p, int device, bool* wrong_device) {
 struct Workspace {
   int64_t n = 0;
   int cap_groups = 0;
+  uint32_t hubcap = 0;
   std::vector<void*> allocs;
   std::vector<GroupWs> h_groups;
   GroupWs* d_groups = nullptr;
@@ -121,6 +123,9 @@ gi_status ws_prepare(gi_graph* g, Workspace* w, int k, int nsrc) {
   const int64_t n = g->n;
   const size_t nwords = (size_t)((n + 31) / 32);
   w->n = n;
+  // a vertex with deg >= kMinHubMin can appear at most m / kMinHubMin times ... per distinct
+  // vertex; twice that covers re-queued entries, the rest fall back to CTA-local processing
+  w->hubcap = (uint32_t)std::min<int64_t>(2 * (g->m / kMinHubMin) + 64, 0x7FFFFFFF);
   if (!w->stream) {
     GI_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     GI_CUDA(cudaEventCreate(&w->ev0), "cudaEventCreate");
@@ -139,6 +144,8 @@ gi_status ws_prepare(gi_graph* g, Workspace* w, int k, int nsrc) {
       if ((s = dmalloc(&gw.q[0], (size_t)n, &w->allocs, "alloc q"))) return s;
       if ((s = dmalloc(&gw.q[1], (size_t)n, &w->allocs, "alloc q"))) return s;
       if ((s = dmalloc(&gw.ctl, 1, &w->allocs, "alloc ctl"))) return s;
+      if ((s = dmalloc(&gw.hub[0], (size_t)w->hubcap, &w->allocs, "alloc hub list"))) return s;
+      if ((s = dmalloc(&gw.hub[1], (size_t)w->hubcap, &w->allocs, "alloc hub list"))) return s;
       // bitmaps start (and, after every completed query, end) all-zero
       GI_CUDA(cudaMemsetAsync(gw.farbits, 0, nwords * 4, w->stream), "memset");
       GI_CUDA(cudaMemsetAsync(gw.qbits[0], 0, nwords * 4, w->stream), "memset");
@@ -306,6 +313,8 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   a.ngroups = ngroups;
   a.group_size = G;
   a.div = make_fastdiv(delta);
+  a.hub_min = opt.hub_min ? std::max(opt.hub_min, kMinHubMin) : kDefaultHubMin;
+  a.hubcap = w->hubcap;
   a.T = opt.fusion_threshold ? opt.fusion_threshold : kDefaultT;
   if (a.T > (uint32_t)kBinCap) a.T = kBinCap;
   // pre-read dist[v] before the atomic: pays off when hubs attract many redundant

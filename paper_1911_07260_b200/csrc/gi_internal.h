@@ -14,6 +14,8 @@ constexpr int kSlotEdges = 8;        // ELL slot: up to 8 {col, w} edges inline 
 constexpr uint32_t kColEmpty = 0xFFFFFFFFu;  // unused slot entry
 constexpr uint32_t kColBig = 0xFFFFFFFEu;    // deg > 8: all 8 entries {kColBig, payload}; payloads deg, beg_lo, beg_hi
 constexpr int kFarStage = 2048;      // CTA-local staging of far-pile pushes (flushed at phase end)
+constexpr uint32_t kDefaultHubMin = 4096;  // default out-degree for the group-wide hub path
+constexpr uint32_t kMinHubMin = 1024;      // smallest accepted hub_min (bounds the hub-list size)
 
 // Division by the invariant Δ (Granlund & Montgomery 1994, round-up method):
 // q = (t + ((x - t) >> s1)) >> s2 with t = umulhi(mul, x).
@@ -41,7 +43,8 @@ struct alignas(128) Ctl {
   uint32_t xlive[3];    // live vertices extracted, by extraction mod 3
   uint32_t ovf_cand;    // some candidate distance >= UINT32_MAX was produced
   uint32_t maxsub[3];   // max fused sub-rounds of any CTA, by phase mod 3 (critical-path stat)
-  uint32_t pad0[16];
+  uint32_t hcount[3];   // group hub-list sizes, by phase mod 3
+  uint32_t pad0[13];
   uint32_t bar;         // group barrier: arrivals (low 16 bits) | generation (high 16), own 128 B line
   uint32_t pad1[31];
 };
@@ -61,7 +64,15 @@ struct GroupWs {
   uint32_t* ovfbits;  // [nwords] vertices that received an overflowing candidate
   int32_t* far[2];    // [n] far pile, double-buffered across extractions
   int32_t* q[2];      // [n] global frontier, double-buffered across phases
+  struct HubEnt* hub[2];  // [hubcap] group hub lists (deg >= hub_min), by phase parity
   Ctl* ctl;
+};
+
+// A high-degree vertex queued for relaxation by every CTA of the group.
+struct HubEnt {
+  int64_t beg;
+  uint32_t deg;
+  uint32_t du;
 };
 
 struct KArgs {
@@ -79,6 +90,8 @@ struct KArgs {
   FastDiv div;
   uint32_t T;           // fusion threshold (<= kBinCap)
   uint32_t pre_read;    // read dist[v] before atomicMin (filters atomics on skewed graphs)
+  uint32_t hub_min;     // out-degree >= hub_min -> the vertex's edges are split over the group
+  uint32_t hubcap;      // capacity of each hub list
 };
 
 // Host-side launchers (gi_kernels.cu).

@@ -134,7 +134,7 @@ struct Shared {
   uint32_t cnt3[3];         // current-bucket bin fills, rotating by sub-round
   uint32_t bigtail;         // fill of the high-degree list
   uint32_t farcnt;          // fill of the far staging buffer
-  uint32_t mode, b, cnt;
+  uint32_t mode, b, cnt, hn;
   uint32_t fmin;
   unsigned long long total; // edges of the high-degree list (exclusive-scan total)
   unsigned long long red[kBlock / 32];
@@ -160,6 +160,9 @@ struct Ctx {
   uint32_t* outcnt;        // its fill counter (shared memory)
   BigEnt* big;             // CTA-local high-degree list (shared memory)
   unsigned long long* pre; // exclusive prefix of its degrees (shared memory)
+  HubEnt* hub_next;        // group hub list receiving appends this phase
+  uint32_t* hcount_next;
+  uint32_t hub_min, hubcap;
   Shared* s;
   uint32_t my_fmin;        // thread-local min far bucket (reduced at phase end)
   bool pre_read;
@@ -366,8 +369,22 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
         const uint32_t hi = __shfl_sync(om, e[u].y, 2, 8);
         if (sub == 0) {
           ++nv;
-          const uint32_t pos = atomicAdd(&c.s->bigtail, 1u);
-          if (pos < (uint32_t)kBigCap) {
+          const uint32_t deg = e[u].y;
+          uint32_t hp = 0xFFFFFFFFu;
+          if (deg >= c.hub_min) {  // hub: split over the whole group in the next phase
+            hp = atomicAdd(c.hcount_next, 1u);
+            if (hp < c.hubcap) {
+              HubEnt he;
+              he.beg = (int64_t)(((uint64_t)hi << 32) | lo);
+              he.deg = deg;
+              he.du = du[u];
+              c.hub_next[hp] = he;
+            }
+          }
+          const uint32_t pos = hp < c.hubcap ? 0xFFFFFFFFu : atomicAdd(&c.s->bigtail, 1u);
+          if (hp < c.hubcap) {
+            // queued on the group hub list
+          } else if (pos < (uint32_t)kBigCap) {
             BigEnt be;
             be.beg = (int64_t)(((uint64_t)hi << 32) | lo);
             be.deg = e[u].y;
@@ -531,6 +548,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     if (rank == 0 && tid == 0) {
       for (int k = 0; k < 3; ++k) {
         ctl->qcount[k] = 0; ctl->fcount[k] = 0; ctl->fmin[k] = kInf; ctl->xlive[k] = 0; ctl->maxsub[k] = 0;
+        ctl->hcount[k] = 0;
       }
       ctl->fcount[0] = 1; ctl->fmin[0] = 0; ctl->ovf_cand = 0;
       ws.far[0][0] = src;
@@ -545,6 +563,8 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     c.pre = reinterpret_cast<unsigned long long*>(c.big + kBigCap);
     c.s = &s;
     c.pre_read = a.pre_read != 0;
+    c.hub_min = a.hub_min;
+    c.hubcap = a.hubcap;
 
     uint32_t nv = 0, ne = 0;                       // per thread (flushed per phase)
     unsigned long long tnv = 0, tne = 0;           // per thread, 64-bit totals
@@ -559,6 +579,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
         // L2-coherent loads, all four in flight at once (ordered after the barrier's fence)
         const uint32_t xl = __ldcg(&ctl->xlive[j % 3]);
         const uint32_t qn = __ldcg(&ctl->qcount[p % 3]);
+        const uint32_t hn = __ldcg(&ctl->hcount[p % 3]);
         const uint32_t fc = __ldcg(&ctl->fcount[j % 3]);
         const uint32_t fm = __ldcg(&ctl->fmin[j % 3]);
         if (p > 0 && rank == 0) critical += __ldcg(&ctl->maxsub[(p - 1) % 3]);
@@ -566,7 +587,8 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
           if (xl) { ++buckets; if (FUSED) ++rounds; } else { ++empty; }
         }
         uint32_t mode;
-        if (qn > 0) { mode = MODE_ROUND; s.cnt = qn; }
+        s.hn = min(hn, a.hubcap);
+        if (qn > 0 || hn > 0) { mode = MODE_ROUND; s.cnt = qn; }
         else if (fc > 0) { mode = MODE_EXTRACT; s.cnt = fc; s.b = fm; }
         else mode = MODE_DONE;
         s.mode = mode;
@@ -585,6 +607,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
       if (rank == 0 && tid == 0) {
         ctl->qcount[(p + 2) % 3] = 0;
         ctl->maxsub[(p + 2) % 3] = 0;
+        ctl->hcount[(p + 2) % 3] = 0;
         if (mode == MODE_EXTRACT) {
           ctl->fcount[(j + 1) % 3] = 0; ctl->fmin[(j + 1) % 3] = kInf; ctl->xlive[(j + 1) % 3] = 0;
         }
@@ -594,6 +617,8 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
       c.qbits_next = (p & 1) ? ws.qbits[0] : ws.qbits[1];
       c.q_next = (p & 1) ? ws.q[0] : ws.q[1];
       c.qcount_next = &ctl->qcount[(p + 1) % 3];
+      c.hub_next = (p & 1) ? ws.hub[0] : ws.hub[1];
+      c.hcount_next = &ctl->hcount[(p + 1) % 3];
       c.far_live = (j & 1) ? ws.far[1] : ws.far[0];
       c.fcount_live = &ctl->fcount[j % 3];
       c.out = s_dyn;  // the first stage fills bin 0 (counter cnt3[0])
@@ -630,6 +655,25 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
           scanned += hi - lo;
         }
       } else {
+        // hubs queued in the previous phase: every CTA relaxes its 1/G slice of every
+        // hub's edges (stage B over the slices), so a hub costs ~deg/G per CTA
+        const uint32_t hn = s.hn;
+        const HubEnt* hub_in = (p & 1) ? ws.hub[1] : ws.hub[0];
+        for (uint32_t h0 = 0; h0 < hn; h0 += kBigCap) {
+          const uint32_t nh = min((uint32_t)kBigCap, hn - h0);
+          for (uint32_t i = tid; i < nh; i += kBlock) {
+            const HubEnt he = hub_in[h0 + i];
+            const uint64_t lo_e = (uint64_t)he.deg * rank / G, hi_e = (uint64_t)he.deg * (rank + 1) / G;
+            BigEnt be;
+            be.beg = he.beg + (int64_t)lo_e;
+            be.deg = (uint32_t)(hi_e - lo_e);
+            be.du = he.du;
+            c.big[i] = be;
+          }
+          __syncthreads();
+          stage_big<FUSED>(c, s, nh, ne);
+          __syncthreads();
+        }
         // ROUND: relax the group's global frontier, one slice per CTA, staged through
         // bin 1 in chunks (pushes go to bin 0, which the drain below consumes)
         const int32_t* q_in = (p & 1) ? ws.q[1] : ws.q[0];

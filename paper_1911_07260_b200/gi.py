@@ -44,7 +44,7 @@ class OverflowDistance(GiError):
 class gi_options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("fusion", ctypes.c_int32),
                 ("fusion_threshold", ctypes.c_uint32), ("max_ctas", ctypes.c_int32),
-                ("reserved0", ctypes.c_uint32), ("reserved1", ctypes.c_uint32),
+                ("hub_min", ctypes.c_uint32), ("reserved1", ctypes.c_uint32),
                 ("group_ctas", ctypes.c_int32), ("pre_read", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p)]
 
 
@@ -112,7 +112,7 @@ def _ptr(x):
     raise TypeError(type(x))
 
 
-def make_options(fusion=True, threshold=0, max_ctas=0, group_ctas=0, pre_read=0,
+def make_options(fusion=True, threshold=0, max_ctas=0, group_ctas=0, pre_read=0, hub_min=0,
                  stream=None) -> gi_options:
     o = gi_options()
     _lib.gi_options_default(ctypes.byref(o))
@@ -121,6 +121,7 @@ def make_options(fusion=True, threshold=0, max_ctas=0, group_ctas=0, pre_read=0,
     o.max_ctas = max_ctas
     o.group_ctas = group_ctas
     o.pre_read = pre_read
+    o.hub_min = hub_min
     if stream is not None:
         o.cuda_stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     return o

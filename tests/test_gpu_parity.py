@@ -227,6 +227,24 @@ def test_hubs_and_mixed_degrees(gi):
     for s in (0, 7):
         ref, _ = oracle.dijkstra(g, s)
         for o, delta in ((dict(fusion=True), 1), (dict(fusion=True), 64), (dict(fusion=False), 8),
-                         (dict(fusion=True, pre_read=2), 3), (dict(fusion=True, max_ctas=2), 1 << 20)):
+                         (dict(fusion=True, pre_read=2), 3), (dict(fusion=True, max_ctas=2), 1 << 20),
+                         (dict(fusion=True, hub_min=1024), 2), (dict(fusion=False, hub_min=1 << 30), 5),
+                         (dict(fusion=True, max_ctas=7, hub_min=1024), 1)):
             d, _ = run(gi, G, s, delta, **o)
             assert np.array_equal(d, ref), (s, o, delta)
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(os.environ.get("GI_SKIP_CFG4") == "1",
+                    reason="config 4 (RMAT-26, 2.1 B edges): ~2 min and ~25 GB of host RAM (GI_SKIP_CFG4=1)")
+def test_config4_full(gi):
+    """RMAT-26 at Δ=2: the certificate over every edge (exact for w >= 1),
+    the bucket closed form, and the full Dijkstra oracle element by element."""
+    g = gen.config_graph(4)
+    G = gi.Graph.from_csr(g)
+    src = gen.config_source(4, g)
+    d, st = run(gi, G, src, 2)
+    assert oracle.certificate(g, src, d, symmetric=True)[0] == 0
+    assert st["buckets"] == oracle.bucket_count(d, 2)
+    ref, rc = oracle.dijkstra(g, src)
+    assert rc == 0 and np.array_equal(d, ref)

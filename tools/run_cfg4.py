@@ -1,0 +1,65 @@
+"""Config 4 (RMAT-26, ~2.1 B directed edges) end to end on one B200:
+generate (host, gen/), upload, Δ-stepping at Δ=2 (fused and unfused), then parity:
+the C certificate over every edge (C0∧C1∧C2 <=> exact for w >= 1) and the
+full CPU Dijkstra oracle compared element by element. Prints one JSON line.
+usage: python tools/run_cfg4.py [--no-oracle] [--reps 3]"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import gen  # noqa: E402
+import oracle  # noqa: E402
+from paper_1911_07260_b200 import gi  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--no-oracle", action="store_true")
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--delta", type=int, default=2)
+a = ap.parse_args()
+res = {"config": 4}
+t = time.time()
+g = gen.config_graph(4)
+res["gen_s"] = round(time.time() - t, 1)
+res.update(n=g.n, m=g.m, sum_w=int(g.w.astype(np.uint64).sum()))
+src = gen.config_source(4, g)
+res["src"] = src
+t = time.time()
+G = gi.Graph.from_csr(g)
+res["upload_s"] = round(time.time() - t, 2)
+import torch  # noqa: E402
+
+out = torch.empty(g.n, dtype=torch.int32, device="cuda")
+runs = {}
+for fusion in (True, False):
+    best = None
+    for _ in range(a.reps):
+        st = gi.gi_sssp_delta(G, src, a.delta, out, gi.make_options(fusion=fusion))
+        best = st if best is None or st.gpu_ms < best.gpu_ms else best
+    runs["fused" if fusion else "unfused"] = {k: getattr(best, k) for k in (
+        "gpu_ms", "buckets", "rounds", "grid_syncs", "fused_subrounds", "critical_subrounds", "spills",
+        "vertices_processed", "edges_relaxed")}
+res["runs"] = runs
+res["gteps_fused"] = g.m / (runs["fused"]["gpu_ms"] * 1e-3) / 1e9
+d = gi.as_uint32(out)
+reached = d != 0xFFFFFFFF
+res["n_reached"] = int(reached.sum())
+res["m_reached"] = int(np.diff(g.offsets)[reached].sum())
+res["max_dist"] = int(d[reached].max())
+t = time.time()
+code, bad = oracle.certificate(g, src, d, symmetric=True)
+res["certificate"] = {"code": code, "bad": bad, "s": round(time.time() - t, 1)}
+res["buckets_closed_form"] = oracle.bucket_count(d, a.delta)
+if not a.no_oracle:
+    t = time.time()
+    ref, rc = oracle.dijkstra(g, src)
+    res["oracle_s"] = round(time.time() - t, 1)
+    res["oracle_rc"] = rc
+    res["bit_exact"] = bool(np.array_equal(ref, d))
+    res["mismatches"] = int((ref != d).sum())
+    res["checksum"] = oracle.checksum(ref)
+print(json.dumps(res), flush=True)
