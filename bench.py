@@ -180,6 +180,8 @@ def main():
     ap.add_argument("--no-fusion", action="store_true")
     ap.add_argument("--max-ctas", type=int, default=0)
     ap.add_argument("--group-ctas", type=int, default=0)
+    ap.add_argument("--hub-min", type=int, default=0)
+    ap.add_argument("--pre-read", type=int, default=0, help="0 auto, 1 on, 2 off")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compare", action="store_true", help="skip the fusion on/off counter comparison")
     args = ap.parse_args()
@@ -203,7 +205,7 @@ def main():
     t_upload = time.perf_counter() - t0
     stream = torch.cuda.current_stream()
     opts = dict(fusion=not args.no_fusion, threshold=args.threshold, max_ctas=args.max_ctas,
-                group_ctas=args.group_ctas, stream=stream)
+                group_ctas=args.group_ctas, hub_min=args.hub_min, pre_read=args.pre_read, stream=stream)
 
     if cfg == 5:
         from paper_1911_07260_b200.dist import padded_shard

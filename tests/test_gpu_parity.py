@@ -205,10 +205,9 @@ def test_config5_batch(gi, config_graph):
     # batch symmetry on a symmetric graph: δ(si,sj) == δ(sj,si) for all 64x64 pairs
     M = got[:, srcs.astype(np.int64)]
     assert np.array_equal(M, M.T)
-    # element-wise parity on a subset of rows (oracle ~5 s per source)
-    idx = [0, 21, 63]
-    refs, _, _ = oracle.dijkstra_many(g, srcs[idx])
-    assert np.array_equal(got[idx], refs)
+    # element-wise parity on every row (oracle ~5 s per source, threaded over host cores)
+    refs, _, _ = oracle.dijkstra_many(g, srcs)
+    assert np.array_equal(got, refs)
     for i in range(64):
         assert st[i]["buckets"] > 0
 
