@@ -182,6 +182,8 @@ def main():
     ap.add_argument("--group-ctas", type=int, default=0)
     ap.add_argument("--hub-min", type=int, default=0)
     ap.add_argument("--pre-read", type=int, default=0, help="0 auto, 1 on, 2 off")
+    ap.add_argument("--drain", default="auto", choices=["auto", "bsp", "async"],
+                    help="fused drain: per-sub-round CTA barriers (default) or the barrier-free async ring")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compare", action="store_true", help="skip the fusion on/off counter comparison")
     args = ap.parse_args()
@@ -205,7 +207,8 @@ def main():
     t_upload = time.perf_counter() - t0
     stream = torch.cuda.current_stream()
     opts = dict(fusion=not args.no_fusion, threshold=args.threshold, max_ctas=args.max_ctas,
-                group_ctas=args.group_ctas, hub_min=args.hub_min, pre_read=args.pre_read, stream=stream)
+                group_ctas=args.group_ctas, hub_min=args.hub_min, pre_read=args.pre_read, drain=args.drain,
+                stream=stream)
 
     if cfg == 5:
         from paper_1911_07260_b200.dist import padded_shard
@@ -291,22 +294,26 @@ def main():
     counters = {k: getattr(s_last, k) for k in ("buckets", "rounds", "grid_syncs", "kernel_launches",
                                                   "fused_subrounds", "spills", "vertices_processed",
                                                   "edges_relaxed", "empty_extractions", "far_scanned", "critical_subrounds",
-                                                  "ctas", "threads_per_cta", "groups")}
+                                                  "ctas", "threads_per_cta", "groups", "kernel_kind")}
 
     # ---- fusion on vs off (untimed comparison run, same Δ) ----
     compare = None
     if not args.no_compare and cfg != 5:
         compare = {}
-        for fu in (True, False):
+        variants = [("fused", dict(fusion=True)), ("unfused", dict(fusion=False))]
+        if int(np.diff(g.offsets).max(initial=0)) <= 8:  # both drains run on low-degree graphs
+            variants = [("fused", dict(fusion=True, drain="bsp")), ("fused_async_drain", dict(fusion=True, drain="async")),
+                        ("unfused", dict(fusion=False))]
+        for name, ov in variants:
             o2 = dict(opts)
-            o2["fusion"] = fu
+            o2.update(ov)
             sts = [gi.gi_sssp_delta(G, src, delta, out, gi.make_options(**o2)) for _ in range(3)]
             s = sts[-1]
-            compare["fused" if fu else "unfused"] = {
+            compare[name] = {
                 "gpu_ms": statistics.median([x.gpu_ms for x in sts]), "buckets": s.buckets,
                 "rounds": s.rounds, "grid_syncs": s.grid_syncs, "kernel_launches": s.kernel_launches,
                 "fused_subrounds": s.fused_subrounds, "spills": s.spills,
-                "critical_subrounds": s.critical_subrounds}
+                "critical_subrounds": s.critical_subrounds, "kernel_kind": s.kernel_kind}
 
     # ---- e2e through the public C ABI with HOST buffers (pinned), copies inside ----
     e2e = None

@@ -98,7 +98,9 @@ typedef struct {
   uint32_t hub_min;          /* out-degree >= hub_min: the vertex's edges are split over every CTA of
                                 the group in the next phase (0 = default 4096; values < 1024 are
                                 raised to 1024) */
-  uint32_t reserved1;        /* must be 0 */
+  uint32_t drain;            /* fused drain of the CTA-local bucket: 0 = default (bsp), 1 = bsp (one
+                                CTA barrier per sub-round), 2 = async (barrier-free work ring;
+                                GI_ERR_UNSUPPORTED if some out-degree > 8); ignored without fusion */
   int32_t group_ctas;        /* batch only: CTAs per concurrent query group (0 = auto) */
   int32_t pre_read;          /* read dist[v] before atomicMin: 0 = auto (on when max out-degree > 32),
                                 1 = on, 2 = off */
@@ -124,6 +126,8 @@ typedef struct {
   int32_t ctas;                /* persistent CTAs in the query's group */
   int32_t threads_per_cta;
   int32_t groups;              /* concurrent query groups (1 for single source) */
+  int32_t kernel_kind;         /* persistent kernel that ran: 0 unfused, 1 fused + bsp drain,
+                                  2 fused + async drain */
 } gi_stats;
 
 /* Fill *opt with defaults (fusion on, library-default threshold, all CTAs). */

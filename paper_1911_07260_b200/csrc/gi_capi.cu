@@ -91,7 +91,7 @@ struct gi_graph {
   uint2* d_slots = nullptr;  // ELL adjacency slots, 64 B per vertex
   uint32_t max_deg = 0;
   int sm_count = 0;
-  int bps_fused = 0, bps_plain = 0;  // co-resident CTAs per SM
+  int bps[3] = {0, 0, 0};  // co-resident CTAs per SM, by KernelKind
   std::mutex mu;
   std::vector<std::unique_ptr<Workspace>> pool;
 };
@@ -195,7 +195,7 @@ void ws_release(gi_graph* g, Workspace* w, bool healthy) {
   g->pool.emplace_back(w);
 }
 
-void fill_stats(gi_stats* st, const QStats& q, float ms, int ctas, int groups) {
+void fill_stats(gi_stats* st, const QStats& q, float ms, int ctas, int groups, int kind) {
   st->buckets = q.buckets;
   st->rounds = q.rounds;
   st->grid_syncs = q.phases;
@@ -211,6 +211,7 @@ void fill_stats(gi_stats* st, const QStats& q, float ms, int ctas, int groups) {
   st->ctas = ctas;
   st->threads_per_cta = kBlock;
   st->groups = groups;
+  st->kernel_kind = kind;
 }
 
 gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, uint32_t delta,
@@ -247,7 +248,15 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   if (wrongdev) return fail(GI_ERR_INVALID_ARGUMENT, "dist_out on another device");
 
   const bool fused = opt.fusion != 0;
-  const int bps = fused ? g->bps_fused : g->bps_plain;
+  if (opt.drain > 2) return fail(GI_ERR_INVALID_ARGUMENT, "drain must be 0 (auto), 1 (bsp) or 2 (async)");
+  if (fused && opt.drain == 2 && g->max_deg > kAsyncMaxDeg)
+    return fail(GI_ERR_UNSUPPORTED, "async drain needs max out-degree <= %u (graph has %u)", kAsyncMaxDeg,
+                g->max_deg);
+  // default: the CTA-barrier (BSP) drain with the degree-binned stages; the barrier-free
+  // async drain (every adjacency inline in its ELL slot) is opt-in — measured slower on
+  // configs 1-2, kept as the comparison point
+  const int kind = !fused ? KIND_UNFUSED : opt.drain == 2 ? KIND_FUSED_ASYNC : KIND_FUSED_BSP;
+  const int bps = g->bps[kind];
   int total = g->sm_count * bps;
   // group sizing: single source -> one group of every CTA (capped by max_ctas);
   // batch -> several groups in flight, each of group_ctas CTAs
@@ -317,12 +326,13 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   a.hubcap = w->hubcap;
   a.T = opt.fusion_threshold ? opt.fusion_threshold : kDefaultT;
   if (a.T > (uint32_t)kBinCap) a.T = kBinCap;
+  if (kind == KIND_FUSED_ASYNC && a.T > kRingSafe) a.T = kRingSafe;
   // pre-read dist[v] before the atomic: pays off when hubs attract many redundant
   // relaxations (skewed degrees), costs one L2 round trip per level otherwise
   a.pre_read = opt.pre_read == 1 ? 1u : opt.pre_read == 2 ? 0u : (g->max_deg > 32 ? 1u : 0u);
 
   if ((e = cudaEventRecord(w->ev0, st))) return bail(e, "event");
-  if ((e = launch_sssp(a, fused, G * ngroups, st))) return bail(e, "launch sssp_persistent");
+  if ((e = launch_sssp(a, kind, G * ngroups, st))) return bail(e, "launch sssp_persistent");
   if ((e = cudaEventRecord(w->ev1, st))) return bail(e, "event");
   std::vector<QStats> hq(nsrc);
   if ((e = cudaMemcpyAsync(hq.data(), w->d_qstats, sizeof(QStats) * nsrc, cudaMemcpyDeviceToHost, st)))
@@ -339,7 +349,7 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   bool ovf = false;
   for (int i = 0; i < nsrc; ++i) {
     if (hq[i].overflow) ovf = true;
-    if (stats) fill_stats(&stats[i], hq[i], ms, G, ngroups);
+    if (stats) fill_stats(&stats[i], hq[i], ms, G, ngroups, kind);
   }
   if (ovf) return fail(GI_ERR_OVERFLOW, "a reachable vertex has distance >= UINT32_MAX");
   return GI_OK;
@@ -397,9 +407,10 @@ gi_status gi_graph_create(int64_t n, int64_t m, const int64_t* row_offsets, cons
   g->n = n;
   g->m = m;
   g->sm_count = prop.multiProcessorCount;
-  GI_CUDA(query_occupancy(true, &g->bps_fused), "occupancy");
-  GI_CUDA(query_occupancy(false, &g->bps_plain), "occupancy");
-  if (g->bps_fused < 1 || g->bps_plain < 1) return fail(GI_ERR_CUDA, "persistent kernel cannot be resident");
+  for (int k = 0; k < 3; ++k) {
+    GI_CUDA(query_occupancy(k, &g->bps[k]), "occupancy");
+    if (g->bps[k] < 1) return fail(GI_ERR_CUDA, "persistent kernel variant %d cannot be resident", k);
+  }
 
   cudaStream_t st;
   GI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");

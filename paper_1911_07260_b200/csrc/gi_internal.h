@@ -16,6 +16,13 @@ constexpr uint32_t kColBig = 0xFFFFFFFEu;    // deg > 8: all 8 entries {kColBig,
 constexpr int kFarStage = 2048;      // CTA-local staging of far-pile pushes (flushed at phase end)
 constexpr uint32_t kDefaultHubMin = 4096;  // default out-degree for the group-wide hub path
 constexpr uint32_t kMinHubMin = 1024;      // smallest accepted hub_min (bounds the hub-list size)
+constexpr int kRingLog = 11;
+constexpr int kRing = 1 << kRingLog;       // async drain: CTA-local work ring (entries of 16 B header + 64 B slot)
+constexpr uint32_t kRingSafe = kRing - 16 * 32 - 64;  // admission limit (see the ring protocol)
+constexpr uint32_t kAsyncMaxDeg = kSlotEdges;  // async drain needs every adjacency inline in its ELL slot
+
+// Persistent-kernel variants.
+enum KernelKind : int { KIND_UNFUSED = 0, KIND_FUSED_BSP = 1, KIND_FUSED_ASYNC = 2 };
 
 // Division by the invariant Δ (Granlund & Montgomery 1994, round-up method):
 // q = (t + ((x - t) >> s1)) >> s2 with t = umulhi(mul, x).
@@ -44,7 +51,8 @@ struct alignas(128) Ctl {
   uint32_t ovf_cand;    // some candidate distance >= UINT32_MAX was produced
   uint32_t maxsub[3];   // max fused sub-rounds of any CTA, by phase mod 3 (critical-path stat)
   uint32_t hcount[3];   // group hub-list sizes, by phase mod 3
-  uint32_t pad0[13];
+  uint32_t qclaim[3];   // ROUND phases: next unclaimed global-frontier position, by phase mod 3
+  uint32_t pad0[10];
   uint32_t bar;         // group barrier: arrivals (low 16 bits) | generation (high 16), own 128 B line
   uint32_t pad1[31];
 };
@@ -95,8 +103,8 @@ struct KArgs {
 };
 
 // Host-side launchers (gi_kernels.cu).
-cudaError_t launch_sssp(const KArgs& a, bool fused, int grid, cudaStream_t st);
-cudaError_t query_occupancy(bool fused, int* blocks_per_sm);
+cudaError_t launch_sssp(const KArgs& a, int kind, int grid, cudaStream_t st);
+cudaError_t query_occupancy(int kind, int* blocks_per_sm);
 cudaError_t launch_interleave(const int32_t* cols, const uint32_t* w, uint2* edges, int64_t count,
                               int64_t n, uint32_t* bad_flag, cudaStream_t st);
 cudaError_t launch_build_slots(const int64_t* off, const uint2* edges, uint2* slots, int64_t n,
@@ -104,6 +112,6 @@ cudaError_t launch_build_slots(const int64_t* off, const uint2* edges, uint2* sl
 cudaError_t launch_max_degree(const int64_t* off, int64_t n, uint32_t* max_deg, cudaStream_t st);
 cudaError_t launch_validate_offsets(const int64_t* off, int64_t n, int64_t m, uint32_t* bad_flag,
                                     cudaStream_t st);
-int smem_bytes();
+int smem_bytes(int kind);
 
 }  // namespace gi

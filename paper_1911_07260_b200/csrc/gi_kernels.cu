@@ -70,7 +70,24 @@ __shared__ long long s_trace_last;
   do {                                                                        \
     if (blockIdx.x == 0 && threadIdx.x < 32) atomicAdd(&g_trace[threadIdx.x], s_trace[threadIdx.x]); \
   } while (0)
+// async drain: per phase max over CTAs of feed+drain cycles / max depth; per item
+// (all CTAs, lane 0 of each warp) claim->atomics-returned, ->push-done, idle spins
+constexpr int kTracePhases = 16384;
+__device__ unsigned long long g_phase[4][kTracePhases];  // max drain (async), max depth, max busy, sum busy
+__device__ unsigned long long g_item[16];
+#define ITRACE_T(var) long long var = clock64()
+#define ITRACE_DECL() unsigned long long it_acc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}
+#define ITRACE_ADD(k, v) (it_acc[k] += (unsigned long long)(v))
+#define ITRACE_FLUSH()                                                                    \
+  do {                                                                                    \
+    for (int k_ = 0; k_ < 16; ++k_)                                                       \
+      if (it_acc[k_] && ((threadIdx.x & 31) == 0 || k_ >= 10)) atomicAdd(&g_item[k_], it_acc[k_]); \
+  } while (0)
 #else
+#define ITRACE_T(var) do {} while (0)
+#define ITRACE_DECL() do {} while (0)
+#define ITRACE_ADD(k, v) do {} while (0)
+#define ITRACE_FLUSH() do {} while (0)
 #define TRACE(k) do {} while (0)
 #define TRACE_INIT() do {} while (0)
 #define TRACE_FLUSH() do {} while (0)
@@ -90,6 +107,15 @@ __device__ __forceinline__ uint32_t ld_dist(const uint32_t* p) { return __ldcg(p
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+// The slot of a vertex pushed into this CTA's own bin is read by this SM in the next
+// sub-round: pull it into L1 so that the read does not cost an L2 round trip.
+__device__ __forceinline__ void prefetch_own(const void* p) {
+#ifdef GI_PF_L2
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+#else
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+#endif
 }
 
 __device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
@@ -135,10 +161,17 @@ struct Shared {
   uint32_t bigtail;         // fill of the high-degree list
   uint32_t farcnt;          // fill of the far staging buffer
   uint32_t mode, b, cnt, hn;
+  uint32_t claim;           // ROUND: base of the chunk this CTA claimed
   uint32_t fmin;
   unsigned long long total; // edges of the high-degree list (exclusive-scan total)
   unsigned long long red[kBlock / 32];
   int32_t farstage[kFarStage];
+  // async drain (KIND_FUSED_ASYNC): CTA-local work ring counters
+  uint32_t head;            // next ring position to claim
+  uint32_t tail;            // ring positions reserved by producers
+  uint32_t done;            // processed entries + finished feeding warps - warps (termination)
+  uint32_t maxdep;          // max depth (sub-round equivalent) processed this phase
+  uint32_t spilled;         // some push overflowed the ring threshold this phase
 };
 
 // Everything a relaxation needs, held in registers for one phase.
@@ -163,6 +196,7 @@ struct Ctx {
   HubEnt* hub_next;        // group hub list receiving appends this phase
   uint32_t* hcount_next;
   uint32_t hub_min, hubcap;
+  uint32_t T;              // fusion threshold (async drain: ring occupancy limit)
   Shared* s;
   uint32_t my_fmin;        // thread-local min far bucket (reduced at phase end)
   bool pre_read;
@@ -186,7 +220,7 @@ __device__ __forceinline__ void push_global(Ctx& c, int32_t v) {
 template <bool FUSED>
 __device__ __forceinline__ void push_cur(Ctx& c, int32_t v, uint32_t d) {
   if constexpr (FUSED) {
-    prefetch_l2(c.slots + 8 * (size_t)v);
+    prefetch_own(c.slots + 8 * (size_t)v);
     cg::coalesced_group g = cg::coalesced_threads();
     uint32_t base = 0;
     if (g.thread_rank() == 0) base = atomicAdd(c.outcnt, g.size());
@@ -212,19 +246,6 @@ __device__ __forceinline__ void push_far_global(Ctx& c, int32_t v) {
   }
 }
 
-// Future-bucket push: lazy (bucket recomputed from dist at extraction), staged in
-// shared memory; the dedup + append happens at the phase end.
-__device__ __forceinline__ void push_far(Ctx& c, int32_t v, uint32_t bk) {
-  c.my_fmin = min(c.my_fmin, bk);
-  cg::coalesced_group g = cg::coalesced_threads();
-  uint32_t base = 0;
-  if (g.thread_rank() == 0) base = atomicAdd(&c.s->farcnt, g.size());
-  base = g.shfl(base, 0);
-  const uint32_t pos = base + g.thread_rank();
-  if (pos < (uint32_t)kFarStage) c.s->farstage[pos] = v;
-  else push_far_global(c, v);
-}
-
 __device__ __noinline__ void mark_overflow(uint32_t* ovfbits, uint32_t* ovf_cand, uint32_t v) {
   atomicOr(&ovfbits[v >> 5], 1u << (v & 31));
   atomicOr(ovf_cand, 1u);
@@ -235,8 +256,8 @@ __device__ __noinline__ void mark_overflow(uint32_t* ovfbits, uint32_t* ovf_cand
 // before any result is consumed (memory-level parallelism on the critical chain).
 // Must be called by all 32 lanes of the warp (the appends are warp-aggregated).
 template <bool FUSED, int K>
-__device__ __forceinline__ void relax_batch(Ctx& c, const uint2 (&e)[K], const uint32_t (&du)[K],
-                                            uint32_t valid) {
+__device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], const uint32_t (&du)[K],
+                                                uint32_t valid, const uint32_t* cur = nullptr) {
   uint32_t nd[K], old[K];
   uint32_t ok = 0;
 #pragma unroll
@@ -257,6 +278,16 @@ __device__ __forceinline__ void relax_batch(Ctx& c, const uint2 (&e)[K], const u
   }
 #pragma unroll
   for (int k = 0; k < K; ++k) old[k] = (ok & (1u << k)) ? atomicMin(c.dist + e[k].x, nd[k]) : 0u;
+  // late staleness: the probe of the source vertex (cur, issued with the slot load) was
+  // not waited for before the atomics; an entry superseded by a newer one of the same
+  // vertex drops its pushes (that entry's relaxations supersede these)
+  uint32_t stale = 0;
+  if (cur) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (cur[k] < du[k]) stale |= 1u << k;
+    ok &= ~stale;
+  }
   // classify the successful lowerings: current bucket (bin) or a future one (far pile)
   uint32_t curm = 0, farm = 0;
   uint32_t bk[K];
@@ -287,8 +318,10 @@ __device__ __forceinline__ void relax_batch(Ctx& c, const uint2 (&e)[K], const u
       for (int k = 0; k < K; ++k) {
         if ((curm >> k) & 1u) {
           const uint32_t pos = base + pre[k] + __popc(mk[k] & lt);
-          prefetch_l2(c.slots + 8 * (size_t)e[k].x);
-          if (pos < (uint32_t)kBinCap) c.out[pos] = make_uint2(e[k].x, nd[k]);
+          if (pos < (uint32_t)kBinCap) {
+            prefetch_own(c.slots + 8 * (size_t)e[k].x);
+            c.out[pos] = make_uint2(e[k].x, nd[k]);
+          }
           else push_global(c, (int32_t)e[k].x);  // bin full: next group-wide round
         }
       }
@@ -321,6 +354,7 @@ __device__ __forceinline__ void relax_batch(Ctx& c, const uint2 (&e)[K], const u
       }
     }
   }
+  return stale;
 }
 
 // Stage A — vertices with deg <= 8: ITEMS (entry, slot index), 8 per frontier entry;
@@ -348,18 +382,13 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
         have |= 1u << u;
       }
     }
-    if (check_stale) {  // a newer entry for v exists; octet-uniform decision
-      uint32_t cur[U];
+    // staleness probe of the source vertices: issued now, consumed after the atomics
+    // (relax_batch) except for high-degree vertices, which are queued only if fresh
+    uint32_t cur[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) cur[u] = (have & (1u << u)) ? ld_dist(c.dist + v[u]) : kInf;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t sb = __ballot_sync(0xffffffffu, cur[u] < du[u]);
-        if ((sb >> (threadIdx.x & 24)) & 0xFFu) have &= ~(1u << u);
-      }
-    }
+    for (int u = 0; u < U; ++u) cur[u] = (check_stale && (have & (1u << u))) ? ld_dist(c.dist + v[u]) : kInf;
     TRACE(2);
-    uint32_t valid = 0;
+    uint32_t valid = 0, heads = 0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (!(have & (1u << u))) continue;
@@ -367,7 +396,7 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
         const uint32_t om = 0xFFu << (threadIdx.x & 24);
         const uint32_t lo = __shfl_sync(om, e[u].y, 1, 8);
         const uint32_t hi = __shfl_sync(om, e[u].y, 2, 8);
-        if (sub == 0) {
+        if (sub == 0 && !(cur[u] < du[u])) {
           ++nv;
           const uint32_t deg = e[u].y;
           uint32_t hp = 0xFFFFFFFFu;
@@ -395,11 +424,15 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
           }
         }
       } else {
-        nv += sub == 0;
-        if (e[u].x != kColEmpty) { valid |= 1u << u; ++ne; }
+        if (sub == 0) heads |= 1u << u;
+        if (e[u].x != kColEmpty) valid |= 1u << u;
       }
     }
-    relax_batch<FUSED, U>(c, e, du, valid);
+    const uint32_t stale = relax_batch<FUSED, U>(c, e, du, valid, check_stale ? cur : nullptr);
+    // counters: non-stale entries and their edges (stale is per lane; each lane saw
+    // its own probe of the same word)
+    nv += __popc(heads & ~stale);
+    ne += __popc(valid & ~stale);
     TRACE(3);
   }
 }
@@ -449,26 +482,43 @@ __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32
   __syncthreads();
   const unsigned long long total = s.total;
   if (threadIdx.x == 0) ne += (uint32_t)total;
+  // each thread relaxes 4 CONSECUTIVE edges per iteration: one binary search for the
+  // first, then a forward walk (entries have deg >= 1 except empty hub slices, which the
+  // walk skips); a warp still covers 1 KB of contiguous edges per iteration
   for (unsigned long long k0 = 0; k0 < total; k0 += 4ull * kBlock) {
     uint2 e[4];
     uint32_t du[4];
     uint32_t valid = 0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const unsigned long long k = k0 + (unsigned long long)u * kBlock + threadIdx.x;
-      e[u] = make_uint2(0, 0);
-      du[u] = 0;
-      if (k < total) {
-        uint32_t lo = 0, hi = nb;  // last i with pre[i] <= k
-        while (hi - lo > 1) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (c.pre[mid] <= k) lo = mid; else hi = mid;
-        }
-        const BigEnt be = c.big[lo];
-        e[u] = __ldg(c.edges + be.beg + (int64_t)(k - c.pre[lo]));
-        du[u] = be.du;
-        valid |= 1u << u;
+    const unsigned long long kt = k0 + 4ull * threadIdx.x;
+    if (kt < total) {
+      uint32_t lo = 0, hi = nb;  // last i with pre[i] <= kt
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (c.pre[mid] <= kt) lo = mid; else hi = mid;
       }
+      unsigned long long nxt = lo + 1 < nb ? c.pre[lo + 1] : total;
+      BigEnt be = c.big[lo];
+      int64_t rel = be.beg - (int64_t)c.pre[lo];  // edge index = rel + k within entry lo
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned long long k = kt + u;
+        e[u] = make_uint2(0, 0);
+        du[u] = 0;
+        if (k < total) {
+          while (k >= nxt) {  // next entry (skipping empty ones)
+            ++lo;
+            be = c.big[lo];
+            rel = be.beg - (int64_t)nxt;
+            nxt = lo + 1 < nb ? c.pre[lo + 1] : total;
+          }
+          e[u] = __ldg(c.edges + rel + (int64_t)k);
+          du[u] = be.du;
+          valid |= 1u << u;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { e[u] = make_uint2(0, 0); du[u] = 0; }
     }
     relax_batch<FUSED, 4>(c, e, du, valid);
   }
@@ -506,8 +556,344 @@ __device__ __forceinline__ T block_sum(T x, Shared& s) {
   return t;  // valid in thread 0
 }
 
-template <bool FUSED>
+// ---------------------------------------------------------------------------------
+// Async drain (KIND_FUSED_ASYNC; graphs whose every adjacency fits its ELL slot).
+//
+// The bucket-fusion drain without sub-round barriers: each CTA keeps a work ring in
+// shared memory; warps claim up to 4 entries (one per octet), relax them and push the
+// lowered current-bucket vertices straight back, so a vertex is relaxed as soon as it
+// is lowered instead of at the next CTA barrier. Every ring entry carries the 64-byte
+// ELL slot of its vertex, loaded by the producer IN PARALLEL with the atomicMin that
+// lowered it; the next hop then starts from shared memory and a level of the
+// dependent chain costs one L2 round trip (the atomic), not two (slot load, then
+// atomic). Producers also prefetch into L2 the slots of the pushed vertex's
+// neighbours (the hop after next).
+//
+// Ring protocol (positions are per phase, entry i = pos mod kRing, lap = pos/kRing+1):
+//   state word hdr[i].w: 2*lap-1 = free for lap, 2*lap = written for lap,
+//   2*lap+1 = consumed. A producer reserves positions (one shared atomic on `tail`),
+//   waits for "free", writes the slot and {v, d, depth}, then release-stores
+//   "written". A consumer claims positions below `tail` by CAS on `head`, waits for
+//   "written" (acquire), reads, and marks the entries consumed once its loads that
+//   use them have issued.
+//   Admission: a push is accepted only while reserved-but-unclaimed entries
+//   (tail - head) stay <= its limit, checked before reserving; concurrent pushers can
+//   overshoot by < 16 warps x 32 lanes, and claimed-but-unread entries are < 64, so
+//   limits <= kRingSafe keep every unread entry inside the ring (a producer never
+//   waits on an entry nobody will read).
+//   Termination: `done` starts at -(warps) and gains 1 per processed entry (after its
+//   children are reserved) and 1 per warp that finished feeding; a warp that finds
+//   nothing to claim and reads done == tail (done first) knows that no entry is in
+//   flight and no push can follow.
+// Threshold: a drain push that would make the local bucket (tail - head) reach T
+// spills to the global frontier ("copied over to the global bucket",
+// PAPER.md:595-596), processed in the next group-wide round: the paper's
+// `size() < threshold` test on the CTA's local bucket.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t lds_volatile(const uint32_t* p) {
+  return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+__device__ __forceinline__ void sts_volatile(uint32_t* p, uint32_t v) {
+  *reinterpret_cast<volatile uint32_t*>(p) = v;
+}
+__device__ __forceinline__ uint32_t lds_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_release(uint32_t* p, uint32_t v) {
+#ifdef GI_NO_FENCE
+  *reinterpret_cast<volatile uint32_t*>(p) = v; return;
+#endif
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+
+#ifndef GI_MIN_BACKOFF
+#define GI_MIN_BACKOFF 32
+#endif
+#ifndef GI_MAX_BACKOFF
+#define GI_MAX_BACKOFF 256
+#endif
+constexpr uint32_t kMinBackoffNs = GI_MIN_BACKOFF, kMaxBackoffNs = GI_MAX_BACKOFF;
+
+struct Ring {
+  uint4* hdr;   // [kRing] {v, d, depth, state}
+  uint4* slot;  // [kRing][4] the vertex's 64 B ELL slot
+  uint4* wq;    // [warps][4][5] per-warp continuation queue: {v, d, depth, -} + slot
+};
+
+__device__ __forceinline__ void load_slot(const uint2* slots, uint32_t v, uint4 (&sl)[4]) {
+  const uint4* p = reinterpret_cast<const uint4*>(slots + 8 * (size_t)v);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) sl[j] = __ldg(p + j);
+}
+
+// Warp-aggregated push of (x, nd, dep, slot) for the lanes with `want`; called by all
+// 32 lanes. FEED pushes may fill the ring; drain pushes respect the threshold T.
+template <bool FEED>
+__device__ __forceinline__ void ring_push(Ctx& c, Shared& s, const Ring& r, bool want, uint32_t x,
+                                          uint32_t nd, uint32_t dep, const uint4 (&sl)[4],
+                                          unsigned long long* tr = nullptr) {
+  const uint32_t mask = __ballot_sync(0xffffffffu, want);
+  if (!mask) return;
+#ifdef GI_TRACE
+  long long t0 = clock64();
+#endif
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t cnt = __popc(mask);
+  uint32_t acc = 0, base = 0;
+  if (lane == 0) {
+    const uint32_t lim = FEED ? (uint32_t)kRingSafe : c.T;
+    const uint32_t h = lds_volatile(&s.head), t = lds_volatile(&s.tail);
+    const uint32_t size = t - h;  // local bucket: reserved, not yet claimed
+    acc = size + cnt < lim ? cnt : (size + 1 < lim ? lim - 1 - size : 0u);  // keep size < T
+    if (acc) base = atomicAdd(&s.tail, acc);
+  }
+  acc = __shfl_sync(0xffffffffu, acc, 0);
+  base = __shfl_sync(0xffffffffu, base, 0);
+#ifdef GI_TRACE
+  long long t1 = clock64();
+  long long t2 = t1, t3 = t1;
+#endif
+  if (want) {
+    const uint32_t rk = __popc(mask & ((1u << lane) - 1u));
+    if (rk < acc) {
+      const uint32_t pos = base + rk, i = pos & (kRing - 1), lap = (pos >> kRingLog) + 1;
+      while (lds_volatile(&r.hdr[i].w) != 2 * lap - 1) {
+      }
+#ifdef GI_TRACE
+      t2 = clock64();
+#endif
+#pragma unroll
+      for (int j = 0; j < 4; ++j) r.slot[4 * i + j] = sl[j];
+      r.hdr[i].x = x;
+      r.hdr[i].y = nd;
+      r.hdr[i].z = dep;
+#ifdef GI_TRACE
+      t3 = clock64();
+#endif
+      sts_release(&r.hdr[i].w, 2 * lap);  // slot + header visible before the state
+#ifdef GI_TRACE
+      if (tr) {
+        const long long t4 = clock64();
+        tr[0] += t1 - t0; tr[1] += t2 - t1; tr[2] += t3 - t2; tr[3] += t4 - t3; tr[4] += 1;
+      }
+#endif
+    } else {
+      if (!FEED) s.spilled = 1;
+      push_global(c, (int32_t)x);  // over threshold: the next group-wide round takes it
+    }
+  }
+}
+
+// Drain the CTA's ring until it is empty and no warp is feeding or processing.
+// Called by every warp (warp-uniform control flow).
+//
+// Continuation: of the current-bucket vertices a warp lowers, the first (up to) four
+// stay with the warp — written with their slots into its private 4-entry queue `wq`
+// and relaxed in its next iteration — and only the rest go to the shared ring for
+// other warps. A dependent chain thus stays in one warp and a hop costs the atomic's
+// round trip plus a warp-local hand-off, with no claim/publish between warps. A warp
+// reports the ring entries it claimed as done only when the chains it grew from them
+// have ended, so done == tail still means "nothing in flight anywhere".
+// Continuation entries skip the staleness probe: the warp itself lowered them a hop
+// ago; a duplicate entry of a vertex lowered again since is relaxed once more, which
+// costs work but never correctness.
+__device__ __forceinline__ void async_drain(Ctx& c, Shared& s, const Ring& r, uint4* wq, uint32_t& nv,
+                                            uint32_t& ne) {
+  const uint32_t lane = threadIdx.x & 31, oct = lane >> 3, sub = lane & 7;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t mydep = 0;
+  uint32_t nloc = 0;  // continuation entries in wq (octets [0, nloc))
+  uint32_t owed = 0;  // ring entries claimed whose chains have not ended yet
+  uint32_t backoff = kMinBackoffNs;
+  ITRACE_DECL();
+  for (;;) {
+    // top up the free octets from the shared ring (blocking only when idle)
+    uint32_t h = 0, got = 0;
+    if (lane == 0) {
+      for (;;) {
+        const uint32_t dn = lds_volatile(&s.done);  // before tail (see the protocol)
+        const uint32_t t = lds_volatile(&s.tail);
+        h = lds_volatile(&s.head);
+        if ((int32_t)(t - h) <= 0) {
+          got = (nloc == 0 && owed == 0 && dn == t) ? 0xFFFFFFFFu : 0u;  // all done / nothing claimable
+          break;
+        }
+        const uint32_t k = min(4u - nloc, t - h);
+        if (k == 0) break;
+        if (atomicCAS(&s.head, h, h + k) == h) {
+          got = k;
+          break;
+        }
+        if (nloc) break;  // busy warp: do not fight over the ring
+      }
+    }
+    got = __shfl_sync(0xffffffffu, got, 0);
+    if (got == 0xFFFFFFFFu) break;
+    if (nloc == 0 && got == 0) {
+      if (owed) {  // this warp's chains have ended
+        if (lane == 0) atomicAdd(&s.done, owed);
+        owed = 0;
+      }
+      ITRACE_ADD(7, 1);
+      // idle: back off so that polling does not steal shared-memory issue slots from
+      // the warps on the chain
+      __nanosleep(backoff);
+      backoff = min(backoff * 2, (uint32_t)kMaxBackoffNs);
+      continue;
+    }
+    backoff = kMinBackoffNs;
+    h = __shfl_sync(0xffffffffu, h, 0);
+    owed += got;
+    ITRACE_ADD(8, 1);
+    ITRACE_ADD(9, nloc + got);
+    ITRACE_ADD(10, nloc);
+
+    const bool local = oct < nloc;
+    const bool ring_e = !local && oct < nloc + got;
+    const bool mine = local || ring_e;
+    const uint32_t pos = h + oct - nloc, i = pos & (kRing - 1), lap = (pos >> kRingLog) + 1;
+    uint32_t v = 0, du = 0, dep = 0;
+    uint2 e = make_uint2(kColEmpty, 0);
+    if (local) {
+      const uint4 hd = wq[5 * oct];
+      v = hd.x; du = hd.y; dep = hd.z;
+      e = reinterpret_cast<const uint2*>(wq + 5 * oct + 1)[sub];
+    } else if (ring_e) {
+      while (lds_acquire(&r.hdr[i].w) != 2 * lap) {
+      }
+      const uint4 hd = r.hdr[i];
+      v = hd.x; du = hd.y; dep = hd.z;
+      e = reinterpret_cast<const uint2*>(r.slot + 4 * i)[sub];
+    }
+
+    // relax edge `sub` of the vertex; the atomic, the neighbour's slot and (for ring
+    // entries) the staleness probe of the vertex itself are all in flight together
+    bool valid = mine && e.x != kColEmpty;
+    const uint32_t nd = du + e.y;
+    if (valid && (nd < du || nd == kInf)) {
+      mark_overflow(c.ovfbits, c.ovf_cand, e.x);
+      valid = false;
+    }
+    uint32_t old = 0, cu = kInf;
+    uint4 sl[4];
+    if (valid) old = atomicMin(c.dist + e.x, nd);
+    if (valid) {
+      load_slot(c.slots, e.x, sl);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sl[j] = make_uint4(kColEmpty, 0, kColEmpty, 0);
+    }
+    if (mine && sub == 0 && dep > 0) cu = ld_dist(c.dist + v);
+    // every lane's ring / wq reads have completed (their values fed the loads above):
+    // release the ring entries for the next lap without a fence; wq may be rewritten
+    __syncwarp();
+    if (ring_e && sub == 0) sts_volatile(&r.hdr[i].w, 2 * lap + 1);
+    cu = __shfl_sync(0xffffffffu, cu, lane & 24);
+    const bool stale = cu < du;  // a newer entry of v exists: its relaxations supersede these
+    if (mine && !stale) {
+      nv += sub == 0;
+      ne += valid;
+    }
+    const bool imp = valid && !stale && nd < old;
+    const uint32_t bk = fdiv(nd, c.div);
+    const bool curp = imp && bk == c.b;
+    const bool farp = imp && bk != c.b;  // bk > b: nd >= du >= bΔ
+
+    // continuation: the first four lowered current-bucket vertices stay in this warp
+    const uint32_t cm = __ballot_sync(0xffffffffu, curp);
+    const uint32_t rk = __popc(cm & lt);
+    const uint32_t keep = min(__popc(cm), 4u);
+    if (curp && rk < keep) {
+      uint4* q = wq + 5 * rk;
+      q[0] = make_uint4(e.x, nd, dep + 1, 0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) q[1 + j] = sl[j];
+    }
+    ring_push<false>(c, s, r, curp && rk >= keep, e.x, nd, dep + 1, sl);
+    if (curp) {  // the hop after next: neighbours' slots into L2
+      mydep = max(mydep, dep + 1);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (sl[j].x < kColBig) prefetch_l2(c.slots + 8 * (size_t)sl[j].x);
+        if (sl[j].z < kColBig) prefetch_l2(c.slots + 8 * (size_t)sl[j].z);
+      }
+    }
+    {
+      const uint32_t mk = __ballot_sync(0xffffffffu, farp);
+      if (mk) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&s.farcnt, __popc(mk));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (farp) {
+          c.my_fmin = min(c.my_fmin, bk);
+          const uint32_t p2 = base + __popc(mk & lt);
+          if (p2 < (uint32_t)kFarStage) s.farstage[p2] = (int32_t)e.x;
+          else push_far_global(c, (int32_t)e.x);
+        }
+      }
+    }
+    nloc = keep;
+    __syncwarp();  // wq writes visible to the warp's next iteration
+  }
+  // max depth processed by this warp (an entry of depth k is what the BSP drain relaxes
+  // in sub-round k)
+  ITRACE_FLUSH();
+  mydep = __reduce_max_sync(0xffffffffu, mydep);
+  if (lane == 0 && mydep) atomicMax(&s.maxdep, mydep);
+}
+
+// Feed one phase's initial work into the ring: the extracted bucket (EXTRACT) or this
+// CTA's slice of the global frontier (ROUND). Warp-uniform; ends by releasing the
+// warp's `live` token, after which the warp joins the drain.
+__device__ __forceinline__ void async_feed(Ctx& c, Shared& s, const Ring& r, bool extract,
+                                           const int32_t* src_list, uint32_t* qbits_in, uint32_t lo,
+                                           uint32_t hi, uint32_t& nlive) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t b = c.b;
+  for (uint32_t i0 = lo + warp * 32; i0 < hi; i0 += kBlock) {
+    const uint32_t i = i0 + lane;
+    const bool in = i < hi;
+    const int32_t v = in ? src_list[i] : 0;
+    if (in && !extract) atomicAnd(&qbits_in[v >> 5], ~(1u << (v & 31)));
+    const uint32_t d = in ? ld_dist(c.dist + v) : kInf;
+    bool take;
+    if (extract) {  // (d)+(a): partition the far pile by recomputed bucket
+      const uint32_t bk = fdiv(d, c.div);
+      if (in && bk <= b) atomicAnd(&c.farbits[v >> 5], ~(1u << (v & 31)));
+      take = in && bk == b;  // bk < b: stale (already settled)
+      if (in && bk > b) {
+        c.my_fmin = min(c.my_fmin, bk);
+        cg::coalesced_group g = cg::coalesced_threads();
+        uint32_t base = 0;
+        if (g.thread_rank() == 0) base = atomicAdd(c.fcount_live, g.size());
+        base = g.shfl(base, 0);
+        c.far_live[base + g.thread_rank()] = v;
+      }
+      nlive += take;
+    } else {
+      take = in;
+    }
+    uint4 sl[4];
+    if (take) {
+      load_slot(c.slots, (uint32_t)v, sl);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sl[j] = make_uint4(0, 0, 0, 0);
+    }
+    // EXTRACT entries are relaxed in "sub-round 1" of the BSP drain, ROUND entries in
+    // the round itself (depth 0)
+    ring_push<true>(c, s, r, take, (uint32_t)v, d, extract ? 1u : 0u, sl);
+  }
+  __syncwarp();
+  if (lane == 0) atomicAdd(&s.done, 1u);  // this warp has finished feeding
+}
+
+template <int KIND>
 __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
+  constexpr bool FUSED = KIND != KIND_UNFUSED;
+  constexpr bool ASYNC = KIND == KIND_FUSED_ASYNC;
   extern __shared__ uint2 s_dyn[];  // bins [2][kBinCap] uint2, high-degree list [kBigCap], its prefix [kBigCap]
   __shared__ Shared s;
   const uint32_t G = (uint32_t)a.group_size;
@@ -548,7 +934,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     if (rank == 0 && tid == 0) {
       for (int k = 0; k < 3; ++k) {
         ctl->qcount[k] = 0; ctl->fcount[k] = 0; ctl->fmin[k] = kInf; ctl->xlive[k] = 0; ctl->maxsub[k] = 0;
-        ctl->hcount[k] = 0;
+        ctl->hcount[k] = 0; ctl->qclaim[k] = 0;
       }
       ctl->fcount[0] = 1; ctl->fmin[0] = 0; ctl->ovf_cand = 0;
       ws.far[0][0] = src;
@@ -565,8 +951,13 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     c.pre_read = a.pre_read != 0;
     c.hub_min = a.hub_min;
     c.hubcap = a.hubcap;
+    c.T = T;
+    Ring ring;
+    ring.hdr = reinterpret_cast<uint4*>(s_dyn);
+    ring.slot = ring.hdr + kRing;
+    ring.wq = ring.slot + 4 * kRing;
 
-    uint32_t nv = 0, ne = 0;                       // per thread (flushed per phase)
+    uint32_t nv = 0, ne = 0;                      // per thread (flushed per phase)
     unsigned long long tnv = 0, tne = 0;           // per thread, 64-bit totals
     unsigned long long subrounds = 0, spills = 0, scanned = 0;  // per CTA (thread 0)
     unsigned long long phases = 0, rounds = 0, buckets = 0, empty = 0, critical = 0;  // rank 0, thread 0
@@ -597,9 +988,18 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
         s.bigtail = 0;
         s.farcnt = 0;
         s.fmin = kInf;
+        if constexpr (ASYNC) {
+          s.head = 0; s.tail = 0; s.done = 0u - (uint32_t)(kBlock / 32); s.maxdep = 0; s.spilled = 0;
+        }
+      }
+      if constexpr (ASYNC) {  // every ring entry "free for lap 1"
+        for (uint32_t i = tid; i < (uint32_t)kRing; i += kBlock) ring.hdr[i].w = 1;
       }
       __syncthreads();
       TRACE(5);
+#ifdef GI_TRACE
+      const long long t_busy0 = clock64();
+#endif
       const uint32_t mode = s.mode;
       if (mode == MODE_DONE) break;
       const uint32_t cnt = s.cnt;
@@ -608,6 +1008,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
         ctl->qcount[(p + 2) % 3] = 0;
         ctl->maxsub[(p + 2) % 3] = 0;
         ctl->hcount[(p + 2) % 3] = 0;
+        ctl->qclaim[(p + 1) % 3] = 0;  // last used in phase p-2, which every CTA has left
         if (mode == MODE_EXTRACT) {
           ctl->fcount[(j + 1) % 3] = 0; ctl->fmin[(j + 1) % 3] = kInf; ctl->xlive[(j + 1) % 3] = 0;
         }
@@ -628,7 +1029,33 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
       const uint32_t lo = (uint32_t)(((uint64_t)cnt * rank) / G);
       const uint32_t hi = (uint32_t)(((uint64_t)cnt * (rank + 1)) / G);
 
-      if (mode == MODE_EXTRACT) {
+      if constexpr (ASYNC) {
+        // feed the extracted bucket / the global-frontier slice into the ring, then
+        // drain it without sub-round barriers (bucket fusion)
+        const bool ex = mode == MODE_EXTRACT;
+        const int32_t* list = ex ? ((j & 1) ? ws.far[0] : ws.far[1]) : ((p & 1) ? ws.q[1] : ws.q[0]);
+        uint32_t* qbits_in = (p & 1) ? ws.qbits[1] : ws.qbits[0];
+        uint32_t nlive = 0;
+        ITRACE_T(t_ph0);
+        async_feed(c, s, ring, ex, list, qbits_in, lo, hi, nlive);
+        TRACE(6);
+        async_drain(c, s, ring, ring.wq + (tid >> 5) * 20, nv, ne);
+#ifdef GI_TRACE
+        __syncthreads();
+        TRACE(11);
+        if (tid == 0 && p < (uint32_t)kTracePhases) {
+          atomicMax(&g_phase[0][p], (unsigned long long)(clock64() - t_ph0));
+          atomicMax(&g_phase[1][p], (unsigned long long)s.maxdep);
+        }
+#endif
+        if (ex) {
+          const uint32_t tl = block_sum(nlive, s);
+          if (tid == 0) {
+            if (tl) atomicAdd(&ctl->xlive[j % 3], tl);
+            scanned += hi - lo;
+          }
+        }
+      } else if (mode == MODE_EXTRACT) {
         // (d)+(a): partition the far pile by recomputed bucket
         const int32_t* far_src = (j & 1) ? ws.far[0] : ws.far[1];
         uint32_t nlive = 0;
@@ -678,21 +1105,35 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
         // bin 1 in chunks (pushes go to bin 0, which the drain below consumes)
         const int32_t* q_in = (p & 1) ? ws.q[1] : ws.q[0];
         uint32_t* qbits_in = (p & 1) ? ws.qbits[1] : ws.qbits[0];
+        // Chunks are CLAIMED dynamically (one atomic per chunk, the next claim in flight
+        // while the current chunk is relaxed): skewed degrees make equal vertex slices
+        // unequal work, and a CTA that drew heavy vertices simply claims fewer chunks.
         uint2* stage = s_dyn + kBinCap;
-        for (uint32_t base = lo; base < hi; base += kBinCap) {
-          const uint32_t chunk = min((uint32_t)kBinCap, hi - base);
+        const uint32_t claim = max(32u, min((uint32_t)kBinCap, cnt / (4 * G)));
+        uint32_t* qclaim = &ctl->qclaim[p % 3];
+        uint32_t next = 0;
+        if (tid == 0) next = atomicAdd(qclaim, claim);
+        for (;;) {
+          if (tid == 0) {
+            s.claim = next;
+            if (next < cnt) next = atomicAdd(qclaim, claim);  // in flight during this chunk
+          }
+          __syncthreads();
+          const uint32_t base = s.claim;
+          if (base >= cnt) break;
+          const uint32_t chunk = min(claim, cnt - base);
           for (uint32_t i = tid; i < chunk; i += kBlock) {
             const int32_t v = q_in[base + i];
             atomicAnd(&qbits_in[v >> 5], ~(1u << (v & 31)));
             stage[i] = make_uint2((uint32_t)v, ld_dist(dist + v));
           }
           __syncthreads();
-          process_bin<FUSED>(c, s, stage, chunk, false, nv, ne);
+          process_bin<FUSED>(c, s, stage, chunk, false, nv, ne);  // ends with a barrier
         }
         __syncthreads();
       }
 
-      if constexpr (FUSED) {
+      if constexpr (FUSED && !ASYNC) {
         // (c) bucket fusion: drain the CTA-local bin while it stays below T
         // (PAPER.md:537-550); a bin of size >= T goes to the global frontier
         // ("copied over to the global bucket"). Sub-round k reads
@@ -728,6 +1169,10 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
         if ((tid & 31) == 0 && fm != kInf) atomicMin(&s.fmin, fm);
         __syncthreads();
         if (tid == 0 && s.fmin != kInf) atomicMin(&ctl->fmin[j % 3], s.fmin);
+        if (ASYNC && tid == 0) {
+          subrounds += s.maxdep;
+          spills += s.spilled;
+        }
         if (FUSED && tid == 0 && subrounds != sub_at_phase_start) {
           atomicMax(&ctl->maxsub[p % 3], (uint32_t)(subrounds - sub_at_phase_start));
           sub_at_phase_start = subrounds;
@@ -735,6 +1180,13 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
       }
       tnv += nv; tne += ne; nv = 0; ne = 0;
       TRACE(8);
+#ifdef GI_TRACE
+      if (tid == 0 && p < (uint32_t)kTracePhases) {
+        const unsigned long long busy = (unsigned long long)(clock64() - t_busy0);
+        atomicMax(&g_phase[2][p], busy);
+        atomicAdd(&g_phase[3][p], busy);
+      }
+#endif
       group_barrier(ctl, G);
       TRACE(9);
       ++p;
@@ -841,11 +1293,24 @@ __global__ void validate_offsets_kernel(const int64_t* __restrict__ off, int64_t
 
 }  // namespace
 
-int smem_bytes() {
+int smem_bytes(int kind) {
+  if (kind == KIND_FUSED_ASYNC) return (kRing + (kBlock / 32) * 4) * (int)(sizeof(uint4) * 5);
   return 2 * kBinCap * (int)sizeof(uint2) + kBigCap * ((int)sizeof(BigEnt) + (int)sizeof(unsigned long long));
 }
 
 #ifdef GI_TRACE
+extern "C" int gi_debug_trace2(unsigned long long* phase, unsigned long long* item, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(phase, g_phase, sizeof(unsigned long long) * 4 * kTracePhases);
+  cudaMemcpyFromSymbol(item, g_item, sizeof(unsigned long long) * 16);
+  if (reset) {
+    static unsigned long long z[4 * kTracePhases];
+    cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+    cudaMemcpyToSymbol(g_item, z, sizeof(unsigned long long) * 16);
+  }
+  return 0;
+}
+
 extern "C" int gi_debug_trace(unsigned long long* out, int reset) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 32);
@@ -857,35 +1322,36 @@ extern "C" int gi_debug_trace(unsigned long long* out, int reset) {
 }
 #endif
 
-static bool g_attr_set = false;
+static const void* kernel_fn(int kind) {
+  switch (kind) {
+    case KIND_UNFUSED: return (const void*)sssp_persistent<KIND_UNFUSED>;
+    case KIND_FUSED_BSP: return (const void*)sssp_persistent<KIND_FUSED_BSP>;
+    default: return (const void*)sssp_persistent<KIND_FUSED_ASYNC>;
+  }
+}
 
-static cudaError_t set_attrs() {
-  if (g_attr_set) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(sssp_persistent<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       smem_bytes());
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(sssp_persistent<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           smem_bytes());
-  if (e == cudaSuccess) g_attr_set = true;
+static bool g_attr_set[3] = {false, false, false};
+
+static cudaError_t set_attrs(int kind) {
+  if (g_attr_set[kind]) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel_fn(kind), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem_bytes(kind));
+  if (e == cudaSuccess) g_attr_set[kind] = true;
   return e;
 }
 
-cudaError_t query_occupancy(bool fused, int* blocks_per_sm) {
-  cudaError_t e = set_attrs();
+cudaError_t query_occupancy(int kind, int* blocks_per_sm) {
+  cudaError_t e = set_attrs(kind);
   if (e != cudaSuccess) return e;
-  return fused ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sssp_persistent<true>,
-                                                               kBlock, smem_bytes())
-               : cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sssp_persistent<false>,
-                                                               kBlock, smem_bytes());
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, kernel_fn(kind), kBlock, smem_bytes(kind));
 }
 
-cudaError_t launch_sssp(const KArgs& a, bool fused, int grid, cudaStream_t st) {
-  cudaError_t e = set_attrs();
+cudaError_t launch_sssp(const KArgs& a, int kind, int grid, cudaStream_t st) {
+  cudaError_t e = set_attrs(kind);
   if (e != cudaSuccess) return e;
   KArgs args = a;
   void* params[] = {&args};
-  const void* fn = fused ? (const void*)sssp_persistent<true> : (const void*)sssp_persistent<false>;
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), params, smem_bytes(), st);
+  return cudaLaunchCooperativeKernel(kernel_fn(kind), dim3(grid), dim3(kBlock), params, smem_bytes(kind), st);
 }
 
 static unsigned grid_for(int64_t count) {

@@ -44,7 +44,7 @@ class OverflowDistance(GiError):
 class gi_options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("fusion", ctypes.c_int32),
                 ("fusion_threshold", ctypes.c_uint32), ("max_ctas", ctypes.c_int32),
-                ("hub_min", ctypes.c_uint32), ("reserved1", ctypes.c_uint32),
+                ("hub_min", ctypes.c_uint32), ("drain", ctypes.c_uint32),
                 ("group_ctas", ctypes.c_int32), ("pre_read", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p)]
 
 
@@ -55,7 +55,8 @@ class gi_stats(ctypes.Structure):
                 ("edges_relaxed", ctypes.c_uint64), ("empty_extractions", ctypes.c_uint64),
                 ("far_scanned", ctypes.c_uint64), ("critical_subrounds", ctypes.c_uint64),
                 ("gpu_ms", ctypes.c_float), ("ctas", ctypes.c_int32),
-                ("threads_per_cta", ctypes.c_int32), ("groups", ctypes.c_int32)]
+                ("threads_per_cta", ctypes.c_int32), ("groups", ctypes.c_int32),
+                ("kernel_kind", ctypes.c_int32)]
 
     def to_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -113,7 +114,7 @@ def _ptr(x):
 
 
 def make_options(fusion=True, threshold=0, max_ctas=0, group_ctas=0, pre_read=0, hub_min=0,
-                 stream=None) -> gi_options:
+                 drain=0, stream=None) -> gi_options:
     o = gi_options()
     _lib.gi_options_default(ctypes.byref(o))
     o.fusion = 1 if fusion else 0
@@ -122,6 +123,7 @@ def make_options(fusion=True, threshold=0, max_ctas=0, group_ctas=0, pre_read=0,
     o.group_ctas = group_ctas
     o.pre_read = pre_read
     o.hub_min = hub_min
+    o.drain = {"auto": 0, "bsp": 1, "async": 2}.get(drain, drain)
     if stream is not None:
         o.cuda_stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     return o

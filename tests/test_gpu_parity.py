@@ -35,8 +35,11 @@ def run(gi, G, src, delta, **opts):
     return gi.as_uint32(d), st
 
 
+# drain: default bsp (CTA barrier per sub-round); "async" = barrier-free ring (out-degree <= 8)
 OPTS = [dict(fusion=True), dict(fusion=False), dict(fusion=True, threshold=2),
-        dict(fusion=True, max_ctas=1), dict(fusion=False, max_ctas=3),
+        dict(fusion=True, drain="async"), dict(fusion=True, drain="async", threshold=2),
+        dict(fusion=True, max_ctas=1), dict(fusion=True, max_ctas=1, drain="async"),
+        dict(fusion=False, max_ctas=3), dict(fusion=True, threshold=1, max_ctas=5),
         dict(fusion=True, pre_read=1), dict(fusion=False, pre_read=2)]
 
 
@@ -174,9 +177,10 @@ def test_config2_full(gi, config_graph):
     G = gi.Graph.from_csr(g)
     src = gen.config_source(2, g)
     ref, _ = oracle.dijkstra(g, src)
-    for delta, fusion in ((1 << 13, True), (1 << 16, True), (1 << 10, False)):
-        d, st = run(gi, G, src, delta, fusion=fusion)
-        assert np.array_equal(d, ref), (delta, fusion)
+    for delta, o in ((1 << 13, dict()), (1 << 16, dict()), (1 << 10, dict(fusion=False)),
+                     (1 << 15, dict(drain="async")), (1 << 15, dict(threshold=64)), (1 << 20, dict())):
+        d, st = run(gi, G, src, delta, **o)
+        assert np.array_equal(d, ref), (delta, o)
         assert st["buckets"] == oracle.bucket_count(ref, delta)
     assert oracle.certificate(g, src, d, symmetric=True)[0] == 0
 
@@ -210,6 +214,42 @@ def test_config5_batch(gi, config_graph):
     assert np.array_equal(got, refs)
     for i in range(64):
         assert st[i]["buckets"] > 0
+
+
+def test_async_drain_low_degree_random(gi):
+    """Random directed graphs with out-degree <= 8 (the async drain's domain): zero weights,
+    self-loops, parallel edges, unreachable parts; every drain / threshold / CTA count."""
+    rng = np.random.default_rng(23)
+    for t in range(40):
+        n = int(rng.integers(1, 3000))
+        deg = rng.integers(0, 9, size=n)
+        wmax = int(rng.choice([1, 3, 50, 10000]))
+        edges = [(u, int(rng.integers(0, n)), int(rng.integers(0, wmax))) for u in range(n) for _ in range(deg[u])]
+        g = gen.from_edges(n, edges)
+        G = gi.Graph.from_csr(g)
+        s = int(rng.integers(0, n))
+        ref, _ = oracle.dijkstra(g, s)
+        for delta in (1, 5, 64, 10**6, 2**31):
+            for o in (dict(drain="async"), dict(drain="async", threshold=1), dict(drain="async", threshold=3, max_ctas=2),
+                      dict(drain="async", max_ctas=1), dict(drain="bsp")):
+                d, st = run(gi, G, s, delta, **o)
+                assert np.array_equal(d, ref), (t, delta, o)
+                assert st["kernel_kind"] == (2 if o["drain"] == "async" else 1)
+                assert st["buckets"] == oracle.bucket_count(ref, delta), (t, delta, o, st)
+
+
+def test_drain_selection_and_unsupported(gi):
+    g = gen.grid(16, 16, 1, 10, 0)
+    G = gi.Graph.from_csr(g)
+    assert run(gi, G, 0, 8)[1]["kernel_kind"] == 1
+    assert run(gi, G, 0, 8, drain="async")[1]["kernel_kind"] == 2
+    assert run(gi, G, 0, 8, fusion=False)[1]["kernel_kind"] == 0
+    star = gen.from_edges(20, [(0, v, 1) for v in range(1, 20)])
+    S = gi.Graph.from_csr(star)
+    assert run(gi, S, 0, 1)[1]["kernel_kind"] == 1
+    with pytest.raises(gi.GiError) as e:
+        run(gi, S, 0, 1, drain="async")
+    assert e.value.status == 7
 
 
 def test_hubs_and_mixed_degrees(gi):

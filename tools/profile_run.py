@@ -13,10 +13,12 @@ ap.add_argument("--no-fusion", action="store_true")
 ap.add_argument("--threshold", type=int, default=0)
 ap.add_argument("--max-ctas", type=int, default=0)
 ap.add_argument("--pre-read", type=int, default=0)
+ap.add_argument("--drain", default="auto")
 a = ap.parse_args()
 g = gen.config_graph(a.config)
 G = gi.Graph.from_csr(g)
 src = gen.config_source(a.config, g)
 for i in range(a.reps):
-    d, st = gi.sssp(G, src, a.delta, fusion=not a.no_fusion, threshold=a.threshold, max_ctas=a.max_ctas, pre_read=a.pre_read)
+    d, st = gi.sssp(G, src, a.delta, fusion=not a.no_fusion, threshold=a.threshold, max_ctas=a.max_ctas, pre_read=a.pre_read,
+                     drain=a.drain)
     print(i, {k: st[k] for k in ("gpu_ms", "buckets", "rounds", "grid_syncs", "fused_subrounds", "critical_subrounds", "spills", "ctas", "edges_relaxed")})

@@ -1,0 +1,94 @@
+"""GI_TRACE build of libgi.so: where the async drain's time goes (per phase and per item).
+usage: python tools/trace_async.py cfg1|cfg2|path [delta] [drain: async|bsp] [max_ctas]"""
+import ctypes
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+
+import gen  # noqa: E402
+
+so = "/tmp/libgi_trace.so"
+src = [os.path.join(ROOT, "paper_1911_07260_b200/csrc", f) for f in ("gi_kernels.cu", "gi_capi.cu")]
+if not os.path.exists(so) or os.environ.get("REBUILD"):
+    subprocess.check_call(["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-DGI_TRACE",
+                           "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"), "-o", so] + src)
+lib = ctypes.CDLL(so)
+vp, i64, i32, u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32
+lib.gi_debug_trace.argtypes = [vp, ctypes.c_int]
+lib.gi_debug_trace2.argtypes = [vp, vp, ctypes.c_int]
+lib.gi_graph_create.argtypes = [i64, i64, vp, vp, vp, ctypes.c_int, ctypes.POINTER(vp)]
+from paper_1911_07260_b200.gi import gi_options, gi_stats  # noqa: E402  (struct layouts only)
+lib.gi_sssp_delta_ex.argtypes = [vp, i32, u32, ctypes.POINTER(gi_options), vp, ctypes.POINTER(gi_stats)]
+lib.gi_options_default.argtypes = [ctypes.POINTER(gi_options)]
+
+what = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+delta = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+drain = sys.argv[3] if len(sys.argv) > 3 else "async"
+max_ctas = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+if what == "path":
+    g = gen.path(20000); src_v = 0; delta = delta or 10**9
+elif what == "cfg3":
+    g = gen.config_graph(3); src_v = gen.config_source(3, g); delta = delta or 1
+elif what == "cfg1":
+    g = gen.config_graph(1); src_v = 0; delta = delta or 1000
+else:
+    g = gen.config_graph(2); src_v = gen.config_source(2, g); delta = delta or 32768
+h = vp()
+assert lib.gi_graph_create(g.n, g.m, g.offsets.ctypes.data, g.cols.ctypes.data, g.w.ctypes.data, 0,
+                           ctypes.byref(h)) == 0
+import torch  # noqa: E402
+
+out = torch.empty(g.n, dtype=torch.int32, device="cuda")
+opt = gi_options()
+lib.gi_options_default(ctypes.byref(opt))
+opt.max_ctas = max_ctas
+opt.drain = {"async": 2, "bsp": 1, "unfused": 1}[drain]
+opt.fusion = 0 if drain == "unfused" else 1
+st = gi_stats()
+buf = np.zeros(32, np.uint64)
+ph = np.zeros((4, 16384), np.uint64)
+it = np.zeros(16, np.uint64)
+for rep in range(2):
+    lib.gi_debug_trace(buf.ctypes.data, 1)
+    lib.gi_debug_trace2(ph.ctypes.data, it.ctypes.data, 1)
+    rc = lib.gi_sssp_delta_ex(h, src_v, delta, ctypes.byref(opt), out.data_ptr(), ctypes.byref(st))
+    assert rc == 0, rc
+    lib.gi_debug_trace(buf.ctypes.data, 0)
+    lib.gi_debug_trace2(ph.ctypes.data, it.ctypes.data, 0)
+print(what, "delta", delta, "drain", drain, "max_ctas", max_ctas, "gpu_ms %.3f" % st.gpu_ms, "subrounds",
+      st.fused_subrounds, "critical", st.critical_subrounds, "buckets", st.buckets, "kind", st.kernel_kind)
+clk = 1.965e3  # cycles per µs at the max SM clock
+names = {0: "bsp drain loop top", 2: "slot load", 3: "relax", 4: "rest", 5: "decision", 6: "feed (async) / extract",
+         7: "phase work end", 8: "far flush + fmin", 9: "group barrier", 11: "drain (async, CTA 0)"}
+tot = 0
+for k in range(16):
+    c = int(buf[16 + k])
+    if c:
+        tot += int(buf[k])
+        print(f"CTA0 {k:2d} {names.get(k, '?'):28s} calls={c:8d} cyc/call={int(buf[k]) / c:9.1f} "
+              f"total={int(buf[k]) / clk / 1e3:8.3f} ms")
+print(f"CTA0 traced total {tot / clk / 1e3:.3f} ms")
+dr, dep = ph[0].astype(np.float64), ph[1].astype(np.float64)
+m = dr > 0
+if m.any():
+    print(f"phases traced {int(m.sum())}; sum over phases of max-CTA feed+drain = {dr[m].sum() / clk / 1e3:.3f} ms; "
+          f"sum max depth = {int(dep[m].sum())}; cycles per depth level = {dr[m].sum() / max(dep[m].sum(), 1):.0f}")
+    q = np.percentile(dr[m] / np.maximum(dep[m], 1), [10, 50, 90])
+    print("per-phase cycles/level p10/p50/p90:", q.round(0))
+if it[8]:
+    nb = it[8]
+    print(f"items: warp-iterations={int(nb)} entries={int(it[9])} (avg {it[9] / nb:.2f}/iter, "
+          f"continuation {it[10] / max(it[9], 1):.1%}); idle polls={int(it[7])}")
+mx, sm = ph[2].astype(np.float64), ph[3].astype(np.float64)
+m2 = mx > 0
+if m2.any():
+    G = st.ctas
+    print(f"phases {int(m2.sum())}: sum of max-CTA busy {mx[m2].sum() / clk / 1e3:.3f} ms, sum of mean-CTA busy "
+          f"{sm[m2].sum() / G / clk / 1e3:.3f} ms (imbalance {mx[m2].sum() / max(sm[m2].sum() / G, 1):.2f}x); "
+          f"gpu_ms {st.gpu_ms:.3f}")
+    top = np.argsort(-mx)[:8]
+    print("  heaviest phases (us max / mean):", [(int(i), round(mx[i] / clk, 1), round(sm[i] / G / clk, 1)) for i in top])
