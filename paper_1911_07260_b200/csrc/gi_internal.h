@@ -13,7 +13,7 @@ constexpr uint32_t kDefaultT = 1024; // fusion threshold default (vertices per C
 constexpr int kSlotEdges = 8;        // ELL slot: up to 8 {col, w} edges inline (64 B per vertex)
 constexpr uint32_t kColEmpty = 0xFFFFFFFFu;  // unused slot entry
 constexpr uint32_t kColBig = 0xFFFFFFFEu;    // deg > 8: all 8 entries {kColBig, payload}; payloads deg, beg_lo, beg_hi
-constexpr int kFarStage = 2048;      // CTA-local staging of far-pile pushes (flushed at phase end)
+constexpr int kFarStage = 8192;      // CTA-local staging of far-pile pushes (flushed at phase end)
 constexpr uint32_t kDefaultHubMin = 4096;  // default out-degree for the group-wide hub path
 constexpr uint32_t kMinHubMin = 1024;      // smallest accepted hub_min (bounds the hub-list size)
 constexpr int kRingLog = 11;

@@ -44,6 +44,11 @@ namespace gi {
 namespace {
 
 enum : uint32_t { MODE_ROUND = 0, MODE_EXTRACT = 1, MODE_DONE = 2, MODE_NONE = 3 };
+constexpr int kXtr = 4;  // far-pile entries per thread per extraction chunk
+#ifndef GI_BIGK
+#define GI_BIGK 8
+#endif
+constexpr int kBigK = GI_BIGK;  // stage B: consecutive edges per thread per iteration
 
 #ifdef GI_TRACE
 // Debug builds only: cycles between trace points, accumulated by CTA 0 / thread 0 in
@@ -162,10 +167,11 @@ struct Shared {
   uint32_t farcnt;          // fill of the far staging buffer
   uint32_t mode, b, cnt, hn;
   uint32_t claim;           // ROUND: base of the chunk this CTA claimed
+  uint32_t redw[kBlock / 32];  // EXTRACT: per-warp exclusive offsets of kept far entries
+  uint32_t xbase;           // EXTRACT: this chunk's base in the receiving far buffer
   uint32_t fmin;
   unsigned long long total; // edges of the high-degree list (exclusive-scan total)
   unsigned long long red[kBlock / 32];
-  int32_t farstage[kFarStage];
   // async drain (KIND_FUSED_ASYNC): CTA-local work ring counters
   uint32_t head;            // next ring position to claim
   uint32_t tail;            // ring positions reserved by producers
@@ -197,6 +203,7 @@ struct Ctx {
   uint32_t* hcount_next;
   uint32_t hub_min, hubcap;
   uint32_t T;              // fusion threshold (async drain: ring occupancy limit)
+  int32_t* farstage;       // CTA-local staging of far-pile pushes (shared memory, kFarStage)
   Shared* s;
   uint32_t my_fmin;        // thread-local min far bucket (reduced at phase end)
   bool pre_read;
@@ -249,6 +256,60 @@ __device__ __forceinline__ void push_far_global(Ctx& c, int32_t v) {
 __device__ __noinline__ void mark_overflow(uint32_t* ovfbits, uint32_t* ovf_cand, uint32_t v) {
   atomicOr(&ovfbits[v >> 5], 1u << (v & 31));
   atomicOr(ovf_cand, 1u);
+}
+
+// Block-wide dedup-append of n staged vertices to a global list: the bit test-and-set
+// (atomicOr) of 4 entries per thread is in flight at once and the list positions come
+// from one global atomic per CTA per chunk (block scan), so that a flush of thousands
+// of entries costs a few round trips, not one chain per entry. All threads call it.
+template <typename Get>
+__device__ __forceinline__ void bulk_append(Shared& s, uint32_t n, Get get, uint32_t* bits, int32_t* list,
+                                            uint32_t* count, const uint2* slots_pf) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t base = 0; base < n; base += 4 * kBlock) {
+    int32_t v[4];
+    uint32_t old[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const uint32_t i = base + x * kBlock + threadIdx.x;
+      v[x] = i < n ? get(i) : -1;
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x) old[x] = v[x] >= 0 ? atomicOr(&bits[v[x] >> 5], 1u << (v[x] & 31)) : ~0u;
+    uint32_t newm = 0;
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      if (v[x] >= 0 && !(old[x] & (1u << (v[x] & 31)))) newm |= 1u << x;
+    const uint32_t nk = __popc(newm);
+    uint32_t incl = nk;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += t;
+    }
+    if (lane == 31) s.redw[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t w = lane < kBlock / 32 ? s.redw[lane] : 0u;
+      uint32_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= (uint32_t)o) wi += t;
+      }
+      if (lane < kBlock / 32) s.redw[lane] = wi - w;
+      const uint32_t tot = __shfl_sync(0xffffffffu, wi, kBlock / 32 - 1);
+      if (lane == 0) s.xbase = tot ? atomicAdd(count, tot) : 0u;
+    }
+    __syncthreads();
+    uint32_t off = s.xbase + s.redw[warp] + incl - nk;
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      if (newm & (1u << x)) {
+        if (slots_pf) prefetch_l2(slots_pf + 8 * (size_t)v[x]);
+        list[off++] = v[x];
+      }
+  }
 }
 
 // Relax K edges per thread (u -> e[k].x, weight e[k].y, from du[k]); lanes with
@@ -348,7 +409,7 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
         if ((farm >> k) & 1u) {
           c.my_fmin = min(c.my_fmin, bk[k]);
           const uint32_t pos = base + pre[k] + __popc(mk[k] & lt);
-          if (pos < (uint32_t)kFarStage) c.s->farstage[pos] = (int32_t)e[k].x;
+          if (pos < (uint32_t)kFarStage) c.farstage[pos] = (int32_t)e[k].x;
           else push_far_global(c, (int32_t)e[k].x);
         }
       }
@@ -482,14 +543,16 @@ __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32
   __syncthreads();
   const unsigned long long total = s.total;
   if (threadIdx.x == 0) ne += (uint32_t)total;
-  // each thread relaxes 4 CONSECUTIVE edges per iteration: one binary search for the
-  // first, then a forward walk (entries have deg >= 1 except empty hub slices, which the
-  // walk skips); a warp still covers 1 KB of contiguous edges per iteration
-  for (unsigned long long k0 = 0; k0 < total; k0 += 4ull * kBlock) {
-    uint2 e[4];
-    uint32_t du[4];
+  // each thread relaxes kBigK CONSECUTIVE edges per iteration: one binary search for
+  // the first, then a forward walk (entries have deg >= 1 except empty hub slices, which
+  // the walk skips); a warp covers kBigK*256 B of contiguous edges per iteration
+  for (unsigned long long k0 = 0; k0 < total; k0 += (unsigned long long)kBigK * kBlock) {
+    uint2 e[kBigK];
+    uint32_t du[kBigK];
     uint32_t valid = 0;
-    const unsigned long long kt = k0 + 4ull * threadIdx.x;
+    const unsigned long long kt = k0 + (unsigned long long)kBigK * threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < kBigK; ++u) { e[u] = make_uint2(0, 0); du[u] = 0; }
     if (kt < total) {
       uint32_t lo = 0, hi = nb;  // last i with pre[i] <= kt
       while (hi - lo > 1) {
@@ -500,10 +563,8 @@ __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32
       BigEnt be = c.big[lo];
       int64_t rel = be.beg - (int64_t)c.pre[lo];  // edge index = rel + k within entry lo
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kBigK; ++u) {
         const unsigned long long k = kt + u;
-        e[u] = make_uint2(0, 0);
-        du[u] = 0;
         if (k < total) {
           while (k >= nxt) {  // next entry (skipping empty ones)
             ++lo;
@@ -516,11 +577,8 @@ __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32
           valid |= 1u << u;
         }
       }
-    } else {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) { e[u] = make_uint2(0, 0); du[u] = 0; }
     }
-    relax_batch<FUSED, 4>(c, e, du, valid);
+    relax_batch<FUSED, kBigK>(c, e, du, valid);
   }
 }
 
@@ -829,7 +887,7 @@ __device__ __forceinline__ void async_drain(Ctx& c, Shared& s, const Ring& r, ui
         if (farp) {
           c.my_fmin = min(c.my_fmin, bk);
           const uint32_t p2 = base + __popc(mk & lt);
-          if (p2 < (uint32_t)kFarStage) s.farstage[p2] = (int32_t)e.x;
+          if (p2 < (uint32_t)kFarStage) c.farstage[p2] = (int32_t)e.x;
           else push_far_global(c, (int32_t)e.x);
         }
       }
@@ -894,7 +952,9 @@ template <int KIND>
 __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
   constexpr bool FUSED = KIND != KIND_UNFUSED;
   constexpr bool ASYNC = KIND == KIND_FUSED_ASYNC;
-  extern __shared__ uint2 s_dyn[];  // bins [2][kBinCap] uint2, high-degree list [kBigCap], its prefix [kBigCap]
+  // bsp: bins [2][kBinCap] uint2, high-degree list [kBigCap], its prefix [kBigCap], far staging
+  // [kFarStage]; async: ring [kRing] (+ per-warp queues), far staging
+  extern __shared__ uint2 s_dyn[];
   __shared__ Shared s;
   const uint32_t G = (uint32_t)a.group_size;
   const uint32_t gid = blockIdx.x / G;
@@ -952,6 +1012,8 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     c.hub_min = a.hub_min;
     c.hubcap = a.hubcap;
     c.T = T;
+    c.farstage = ASYNC ? reinterpret_cast<int32_t*>(s_dyn + (kRing + (kBlock / 32) * 4) * 10)
+                       : reinterpret_cast<int32_t*>(c.pre + kBigCap);
     Ring ring;
     ring.hdr = reinterpret_cast<uint4*>(s_dyn);
     ring.slot = ring.hdr + kRing;
@@ -1056,24 +1118,62 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
           }
         }
       } else if (mode == MODE_EXTRACT) {
-        // (d)+(a): partition the far pile by recomputed bucket
+        // (d)+(a): partition the far pile by recomputed bucket.
+        // kXtr entries per thread per chunk with every load in flight together; the
+        // entries kept for later buckets are compacted with one global atomic per CTA
+        // per chunk (block scan), not one per warp per entry.
         const int32_t* far_src = (j & 1) ? ws.far[0] : ws.far[1];
         uint32_t nlive = 0;
-        for (uint32_t i = lo + tid; i < hi; i += kBlock) {
-          const int32_t v = far_src[i];
-          const uint32_t d = ld_dist(dist + v);
-          const uint32_t bk = fdiv(d, c.div);
-          if (bk <= b) {
-            atomicAnd(&ws.farbits[v >> 5], ~(1u << (v & 31)));
-            if (bk == b) { ++nlive; push_cur<FUSED>(c, v, d); }  // else: stale (already settled)
-          } else {
-            c.my_fmin = min(c.my_fmin, bk);
-            cg::coalesced_group g = cg::coalesced_threads();
-            uint32_t base = 0;
-            if (g.thread_rank() == 0) base = atomicAdd(c.fcount_live, g.size());
-            base = g.shfl(base, 0);
-            c.far_live[base + g.thread_rank()] = v;
+        const uint32_t lane = tid & 31, warp = tid >> 5;
+        for (uint32_t base = lo; base < hi; base += kXtr * kBlock) {
+          int32_t v[kXtr];
+          uint32_t d[kXtr];
+#pragma unroll
+          for (int x = 0; x < kXtr; ++x) {
+            const uint32_t i = base + x * kBlock + tid;
+            v[x] = i < hi ? far_src[i] : -1;
           }
+#pragma unroll
+          for (int x = 0; x < kXtr; ++x) d[x] = v[x] >= 0 ? ld_dist(dist + v[x]) : kInf;
+          uint32_t keepm = 0;
+#pragma unroll
+          for (int x = 0; x < kXtr; ++x) {
+            if (v[x] < 0) continue;
+            const uint32_t bk = fdiv(d[x], c.div);
+            if (bk <= b) {
+              atomicAnd(&ws.farbits[v[x] >> 5], ~(1u << (v[x] & 31)));
+              if (bk == b) { ++nlive; push_cur<FUSED>(c, v[x], d[x]); }  // else: stale (settled)
+            } else {
+              c.my_fmin = min(c.my_fmin, bk);
+              keepm |= 1u << x;
+            }
+          }
+          const uint32_t nk = __popc(keepm);
+          uint32_t incl = nk;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += t;
+          }
+          if (lane == 31) s.redw[warp] = incl;
+          __syncthreads();
+          if (warp == 0) {
+            const uint32_t w = lane < kBlock / 32 ? s.redw[lane] : 0u;
+            uint32_t wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+              if (lane >= (uint32_t)o) wi += t;
+            }
+            if (lane < kBlock / 32) s.redw[lane] = wi - w;
+            const uint32_t tot = __shfl_sync(0xffffffffu, wi, kBlock / 32 - 1);
+            if (lane == 0) s.xbase = tot ? atomicAdd(c.fcount_live, tot) : 0u;
+          }
+          __syncthreads();
+          uint32_t off = s.xbase + s.redw[warp] + incl - nk;
+#pragma unroll
+          for (int x = 0; x < kXtr; ++x)
+            if (keepm & (1u << x)) c.far_live[off++] = v[x];
         }
         TRACE(6);
         const uint32_t tl = block_sum(nlive, s);  // ends with a barrier: ring fill is final
@@ -1122,10 +1222,22 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
           const uint32_t base = s.claim;
           if (base >= cnt) break;
           const uint32_t chunk = min(claim, cnt - base);
-          for (uint32_t i = tid; i < chunk; i += kBlock) {
-            const int32_t v = q_in[base + i];
-            atomicAnd(&qbits_in[v >> 5], ~(1u << (v & 31)));
-            stage[i] = make_uint2((uint32_t)v, ld_dist(dist + v));
+          for (uint32_t i0 = 0; i0 < chunk; i0 += 4 * kBlock) {  // one pass: chunk <= kBinCap
+            int32_t vv[4];
+            uint32_t dd[4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              const uint32_t i = i0 + x * kBlock + tid;
+              vv[x] = i < chunk ? q_in[base + i] : -1;
+            }
+#pragma unroll
+            for (int x = 0; x < 4; ++x) dd[x] = vv[x] >= 0 ? ld_dist(dist + vv[x]) : 0u;
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              if (vv[x] < 0) continue;
+              atomicAnd(&qbits_in[vv[x] >> 5], ~(1u << (vv[x] & 31)));
+              stage[i0 + x * kBlock + tid] = make_uint2((uint32_t)vv[x], dd[x]);
+            }
           }
           __syncthreads();
           process_bin<FUSED>(c, s, stage, chunk, false, nv, ne);  // ends with a barrier
@@ -1147,7 +1259,8 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
           const uint32_t nin = min(s.cnt3[(k - 1) % 3], (uint32_t)kBinCap);
           if (nin == 0) break;
           if (nin >= T) {
-            for (uint32_t i = tid; i < nin; i += kBlock) push_global(c, (int32_t)in[i].x);
+            bulk_append(s, nin, [&](uint32_t i) { return (int32_t)in[i].x; }, c.qbits_next, c.q_next,
+                        c.qcount_next, c.slots);
             if (tid == 0) ++spills;
             break;
           }
@@ -1164,7 +1277,8 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
       TRACE(7);
       {
         const uint32_t nf = min(s.farcnt, (uint32_t)kFarStage);
-        for (uint32_t i = tid; i < nf; i += kBlock) push_far_global(c, s.farstage[i]);
+        const int32_t* fs = c.farstage;
+        bulk_append(s, nf, [&](uint32_t i) { return fs[i]; }, c.farbits, c.far_live, c.fcount_live, nullptr);
         uint32_t fm = __reduce_min_sync(0xffffffffu, c.my_fmin);
         if ((tid & 31) == 0 && fm != kInf) atomicMin(&s.fmin, fm);
         __syncthreads();
@@ -1294,8 +1408,9 @@ __global__ void validate_offsets_kernel(const int64_t* __restrict__ off, int64_t
 }  // namespace
 
 int smem_bytes(int kind) {
-  if (kind == KIND_FUSED_ASYNC) return (kRing + (kBlock / 32) * 4) * (int)(sizeof(uint4) * 5);
-  return 2 * kBinCap * (int)sizeof(uint2) + kBigCap * ((int)sizeof(BigEnt) + (int)sizeof(unsigned long long));
+  const int far = kFarStage * (int)sizeof(int32_t);
+  if (kind == KIND_FUSED_ASYNC) return (kRing + (kBlock / 32) * 4) * (int)(sizeof(uint4) * 5) + far;
+  return 2 * kBinCap * (int)sizeof(uint2) + kBigCap * ((int)sizeof(BigEnt) + (int)sizeof(unsigned long long)) + far;
 }
 
 #ifdef GI_TRACE
