@@ -142,6 +142,20 @@ gi_status gi_sssp_delta_ex(const gi_graph* g, int32_t src, uint32_t delta, const
 gi_status gi_sssp_batch_ex(const gi_graph* g, const int32_t* srcs, int32_t nsrc, uint32_t delta,
                            const gi_options* opt, uint32_t* dist_out, gi_stats* per_src);
 
+/* Point-to-point shortest path: Δ-stepping from src that stops when it
+ * enters bucket i with iΔ >= the distance already found to dst — "terminates the program
+ * early when it enters iteration i where iΔ is greater than or equal to the shortest
+ * distance between s and d it has already found".
+ *   src, dst  0 <= src, dst < n, else GI_ERR_OUT_OF_RANGE;
+ *   delta     Δ >= 1 (Δ = 0 -> GI_ERR_INVALID_ARGUMENT);
+ *   dist_st   ONE uint32, host or device (on the graph's device): δ(src, dst),
+ *             UINT32_MAX if dst is unreachable. The distance array lives in a library
+ *             workspace (n uint32 on the device).
+ * GI_ERR_OVERFLOW iff δ(src, dst) >= UINT32_MAX. Synchronous like gi_sssp_delta. */
+gi_status gi_ppsp_delta(const gi_graph* g, int32_t src, int32_t dst, uint32_t delta, uint32_t* dist_st);
+gi_status gi_ppsp_delta_ex(const gi_graph* g, int32_t src, int32_t dst, uint32_t delta, const gi_options* opt,
+                           uint32_t* dist_st, gi_stats* stats);
+
 /* Thread-local description of the last non-OK status returned on this thread. */
 const char* gi_last_error(void);
 

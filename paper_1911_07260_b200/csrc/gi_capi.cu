@@ -215,7 +215,8 @@ void fill_stats(gi_stats* st, const QStats& q, float ms, int ctas, int groups, i
 }
 
 gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, uint32_t delta,
-                      const gi_options* opt_in, uint32_t* dist_out, gi_stats* stats, bool batch) {
+                      const gi_options* opt_in, uint32_t* dist_out, gi_stats* stats, bool batch,
+                      int32_t target = -1) {
   gi_graph* g = const_cast<gi_graph*>(cg_);
   if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "graph is NULL");
   if (nsrc < 0) return fail(GI_ERR_INVALID_ARGUMENT, "nsrc < 0");
@@ -244,8 +245,11 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   for (int i = 0; i < nsrc; ++i)
     if (hsrc[i] < 0 || hsrc[i] >= g->n)
       return fail(GI_ERR_OUT_OF_RANGE, "source %d not in [0, %lld)", hsrc[i], (long long)g->n);
+  if (target >= 0 && target >= g->n)
+    return fail(GI_ERR_OUT_OF_RANGE, "target %d not in [0, %lld)", target, (long long)g->n);
   const bool dev_out = is_device_ptr(dist_out, g->device, &wrongdev);
   if (wrongdev) return fail(GI_ERR_INVALID_ARGUMENT, "dist_out on another device");
+  const bool ppsp = target >= 0;  // dist_out is ONE value; the distances live in the workspace
 
   const bool fused = opt.fusion != 0;
   if (opt.drain > 2) return fail(GI_ERR_INVALID_ARGUMENT, "drain must be 0 (auto), 1 (bsp) or 2 (async)");
@@ -295,7 +299,7 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
     return cuda_fail(e, what);
   };
   cudaError_t e;
-  if (!dev_out) {
+  if (!dev_out || ppsp) {
     if (w->stagecap < total_elems) {
       if (w->d_stage) cudaFree(w->d_stage);
       w->d_stage = nullptr;
@@ -324,12 +328,13 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   a.div = make_fastdiv(delta);
   a.hub_min = opt.hub_min ? std::max(opt.hub_min, kMinHubMin) : kDefaultHubMin;
   a.hubcap = w->hubcap;
-  a.T = opt.fusion_threshold ? opt.fusion_threshold : kDefaultT;
+  a.T = opt.fusion_threshold ? opt.fusion_threshold : (g->max_deg > 32 ? kDefaultTSkewed : kDefaultT);
   if (a.T > (uint32_t)kBinCap) a.T = kBinCap;
   if (kind == KIND_FUSED_ASYNC && a.T > kRingSafe) a.T = kRingSafe;
   // pre-read dist[v] before the atomic: pays off when hubs attract many redundant
   // relaxations (skewed degrees), costs one L2 round trip per level otherwise
   a.pre_read = opt.pre_read == 1 ? 1u : opt.pre_read == 2 ? 0u : (g->max_deg > 32 ? 1u : 0u);
+  a.target = target;
 
   if ((e = cudaEventRecord(w->ev0, st))) return bail(e, "event");
   if ((e = launch_sssp(a, kind, G * ngroups, st))) return bail(e, "launch sssp_persistent");
@@ -337,7 +342,11 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   std::vector<QStats> hq(nsrc);
   if ((e = cudaMemcpyAsync(hq.data(), w->d_qstats, sizeof(QStats) * nsrc, cudaMemcpyDeviceToHost, st)))
     return bail(e, "copy stats");
-  if (!dev_out) {
+  if (ppsp) {
+    if ((e = cudaMemcpyAsync(dist_out, d_dist + target, 4, dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                             st)))
+      return bail(e, "copy dist[target]");
+  } else if (!dev_out) {
     if ((e = cudaMemcpyAsync(dist_out, d_dist, total_elems * 4, cudaMemcpyDeviceToHost, st)))
       return bail(e, "copy dist");
   }
@@ -516,6 +525,16 @@ gi_status gi_sssp_batch_ex(const gi_graph* g, const int32_t* srcs, int32_t nsrc,
 gi_status gi_sssp_batch(const gi_graph* g, const int32_t* srcs, int32_t nsrc, uint32_t delta,
                         uint32_t* dist_out) {
   return gi_sssp_batch_ex(g, srcs, nsrc, delta, nullptr, dist_out, nullptr);
+}
+
+gi_status gi_ppsp_delta_ex(const gi_graph* g, int32_t src, int32_t dst, uint32_t delta, const gi_options* opt,
+                           uint32_t* dist_st, gi_stats* stats) {
+  if (dst < 0) return fail(GI_ERR_OUT_OF_RANGE, "target %d < 0", dst);
+  return run_queries(g, &src, 1, delta, opt, dist_st, stats, false, dst);
+}
+
+gi_status gi_ppsp_delta(const gi_graph* g, int32_t src, int32_t dst, uint32_t delta, uint32_t* dist_st) {
+  return gi_ppsp_delta_ex(g, src, dst, delta, nullptr, dist_st, nullptr);
 }
 
 }  // extern "C"

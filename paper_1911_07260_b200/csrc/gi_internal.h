@@ -9,13 +9,14 @@ constexpr uint32_t kInf = 0xFFFFFFFFu;
 constexpr int kBlock = 512;          // threads per persistent CTA
 constexpr int kBinCap = 2048;        // CTA-local current-bucket bin of uint2 {v, d}; two (ping-pong) per CTA
 constexpr int kBigCap = 2048;        // CTA-local list of high-degree vertices (deg > 8) per bin
-constexpr uint32_t kDefaultT = 1024; // fusion threshold default (vertices per CTA bin)
+constexpr uint32_t kDefaultT = 1024; // fusion threshold default (vertices per CTA bin), max out-degree <= 32
+constexpr uint32_t kDefaultTSkewed = 256;  // ... and on skewed graphs (max out-degree > 32); DESIGN.md §10
 constexpr int kSlotEdges = 8;        // ELL slot: up to 8 {col, w} edges inline (64 B per vertex)
 constexpr uint32_t kColEmpty = 0xFFFFFFFFu;  // unused slot entry
 constexpr uint32_t kColBig = 0xFFFFFFFEu;    // deg > 8: all 8 entries {kColBig, payload}; payloads deg, beg_lo, beg_hi
 constexpr int kFarStage = 8192;      // CTA-local staging of far-pile pushes (flushed at phase end)
-constexpr uint32_t kDefaultHubMin = 4096;  // default out-degree for the group-wide hub path
-constexpr uint32_t kMinHubMin = 1024;      // smallest accepted hub_min (bounds the hub-list size)
+constexpr uint32_t kDefaultHubMin = 1024;  // default out-degree for the group-wide hub path
+constexpr uint32_t kMinHubMin = 256;       // smallest accepted hub_min (bounds the hub-list size)
 constexpr int kRingLog = 11;
 constexpr int kRing = 1 << kRingLog;       // async drain: CTA-local work ring (entries of 16 B header + 64 B slot)
 constexpr uint32_t kRingSafe = kRing - 16 * 32 - 64;  // admission limit (see the ring protocol)
@@ -52,7 +53,8 @@ struct alignas(128) Ctl {
   uint32_t maxsub[3];   // max fused sub-rounds of any CTA, by phase mod 3 (critical-path stat)
   uint32_t hcount[3];   // group hub-list sizes, by phase mod 3
   uint32_t qclaim[3];   // ROUND phases: next unclaimed global-frontier position, by phase mod 3
-  uint32_t pad0[10];
+  uint32_t tdist[3];    // PPSP: min over CTAs of dist[target] read at the phase end, by phase mod 3
+  uint32_t pad0[7];
   uint32_t bar;         // group barrier: arrivals (low 16 bits) | generation (high 16), own 128 B line
   uint32_t pad1[31];
 };
@@ -100,6 +102,7 @@ struct KArgs {
   uint32_t pre_read;    // read dist[v] before atomicMin (filters atomics on skewed graphs)
   uint32_t hub_min;     // out-degree >= hub_min -> the vertex's edges are split over the group
   uint32_t hubcap;      // capacity of each hub list
+  int32_t target;       // PPSP: stop once the next bucket's lower bound reaches dist[target]; -1 = SSSP
 };
 
 // Host-side launchers (gi_kernels.cu).

@@ -43,7 +43,7 @@ namespace cg = cooperative_groups;
 namespace gi {
 namespace {
 
-enum : uint32_t { MODE_ROUND = 0, MODE_EXTRACT = 1, MODE_DONE = 2, MODE_NONE = 3 };
+enum : uint32_t { MODE_ROUND = 0, MODE_EXTRACT = 1, MODE_DONE = 2, MODE_NONE = 3, MODE_STOP = 4 };
 constexpr int kXtr = 4;  // far-pile entries per thread per extraction chunk
 #ifndef GI_BIGK
 #define GI_BIGK 8
@@ -994,7 +994,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     if (rank == 0 && tid == 0) {
       for (int k = 0; k < 3; ++k) {
         ctl->qcount[k] = 0; ctl->fcount[k] = 0; ctl->fmin[k] = kInf; ctl->xlive[k] = 0; ctl->maxsub[k] = 0;
-        ctl->hcount[k] = 0; ctl->qclaim[k] = 0;
+        ctl->hcount[k] = 0; ctl->qclaim[k] = 0; ctl->tdist[k] = kInf;
       }
       ctl->fcount[0] = 1; ctl->fmin[0] = 0; ctl->ovf_cand = 0;
       ws.far[0][0] = src;
@@ -1044,6 +1044,14 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
         if (qn > 0 || hn > 0) { mode = MODE_ROUND; s.cnt = qn; }
         else if (fc > 0) { mode = MODE_EXTRACT; s.cnt = fc; s.b = fm; }
         else mode = MODE_DONE;
+        // PPSP: entering bucket i with iΔ >= the best distance found
+        // to the target ends the query — every vertex below iΔ is settled. The snapshot
+        // of dist[target] is a slot every CTA wrote before the barrier (identical
+        // decisions in all CTAs; a stale, larger snapshot only delays the stop a phase).
+        if (a.target >= 0 && mode == MODE_EXTRACT && p > 0) {
+          const uint32_t td = __ldcg(&ctl->tdist[(p - 1) % 3]);
+          if (td != kInf && (uint64_t)fm * (uint64_t)a.div.d >= (uint64_t)td) mode = MODE_STOP;
+        }
         s.mode = mode;
         s.cnt3[0] = 0;
         s.cnt3[1] = 0;
@@ -1064,6 +1072,18 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
 #endif
       const uint32_t mode = s.mode;
       if (mode == MODE_DONE) break;
+      if (mode == MODE_STOP) {
+        // PPSP early stop: the far pile still holds entries; clear their dedup bits so
+        // that the workspace ends clean (every bitmap all-zero) for the next query
+        const int32_t* pile = (j & 1) ? ws.far[1] : ws.far[0];
+        const uint32_t fc = s.cnt;
+        const uint32_t lo2 = (uint32_t)(((uint64_t)fc * rank) / G), hi2 = (uint32_t)(((uint64_t)fc * (rank + 1)) / G);
+        for (uint32_t i = lo2 + tid; i < hi2; i += kBlock) {
+          const int32_t v = pile[i];
+          atomicAnd(&ws.farbits[v >> 5], ~(1u << (v & 31)));
+        }
+        break;
+      }
       const uint32_t cnt = s.cnt;
       if (mode == MODE_EXTRACT) { ++j; b = s.b; }
       if (rank == 0 && tid == 0) {
@@ -1071,6 +1091,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
         ctl->maxsub[(p + 2) % 3] = 0;
         ctl->hcount[(p + 2) % 3] = 0;
         ctl->qclaim[(p + 1) % 3] = 0;  // last used in phase p-2, which every CTA has left
+        ctl->tdist[(p + 1) % 3] = kInf;  // written at the end of phase p+1
         if (mode == MODE_EXTRACT) {
           ctl->fcount[(j + 1) % 3] = 0; ctl->fmin[(j + 1) % 3] = kInf; ctl->xlive[(j + 1) % 3] = 0;
         }
@@ -1287,6 +1308,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
           subrounds += s.maxdep;
           spills += s.spilled;
         }
+        if (tid == 0 && a.target >= 0) atomicMin(&ctl->tdist[p % 3], ld_dist(dist + a.target));
         if (FUSED && tid == 0 && subrounds != sub_at_phase_start) {
           atomicMax(&ctl->maxsub[p % 3], (uint32_t)(subrounds - sub_at_phase_start));
           sub_at_phase_start = subrounds;
@@ -1320,7 +1342,8 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
             const int k = __ffs(bits) - 1;
             bits &= bits - 1;
             const int64_t v = (int64_t)wi * 32 + k;
-            if (v < n && ld_dist(dist + v) == kInf) bad = 1;
+            // PPSP stops early: only the target's distance is the result
+            if (v < n && (a.target < 0 || v == a.target) && ld_dist(dist + v) == kInf) bad = 1;
           }
         }
       }

@@ -27,7 +27,7 @@ STATUS = {0: "GI_OK", 1: "GI_ERR_INVALID_ARGUMENT", 2: "GI_ERR_OUT_OF_RANGE", 3:
           4: "GI_ERR_OUT_OF_MEMORY", 5: "GI_ERR_CUDA", 6: "GI_ERR_OVERFLOW", 7: "GI_ERR_UNSUPPORTED"}
 EXPORTS = ["gi_graph_create", "gi_graph_destroy", "gi_graph_info", "gi_sssp_delta", "gi_sssp_batch",
            "gi_options_default", "gi_sssp_delta_ex", "gi_sssp_batch_ex", "gi_last_error",
-           "gi_status_string", "gi_version"]
+           "gi_status_string", "gi_version", "gi_ppsp_delta", "gi_ppsp_delta_ex"]
 
 
 class GiError(RuntimeError):
@@ -73,12 +73,14 @@ _lib.gi_options_default.argtypes = [ctypes.POINTER(gi_options)]
 _lib.gi_options_default.restype = None
 _lib.gi_sssp_delta_ex.argtypes = [_vp, _i32, _u32, ctypes.POINTER(gi_options), _vp, ctypes.POINTER(gi_stats)]
 _lib.gi_sssp_batch_ex.argtypes = [_vp, _vp, _i32, _u32, ctypes.POINTER(gi_options), _vp, ctypes.POINTER(gi_stats)]
+_lib.gi_ppsp_delta.argtypes = [_vp, _i32, _i32, _u32, _vp]
+_lib.gi_ppsp_delta_ex.argtypes = [_vp, _i32, _i32, _u32, ctypes.POINTER(gi_options), _vp, ctypes.POINTER(gi_stats)]
 _lib.gi_last_error.restype = ctypes.c_char_p
 _lib.gi_status_string.argtypes = [ctypes.c_int]
 _lib.gi_status_string.restype = ctypes.c_char_p
 _lib.gi_version.restype = _i32
 for _f in ("gi_graph_create", "gi_graph_info", "gi_sssp_delta", "gi_sssp_batch", "gi_sssp_delta_ex",
-           "gi_sssp_batch_ex"):
+           "gi_sssp_batch_ex", "gi_ppsp_delta", "gi_ppsp_delta_ex"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 
@@ -207,6 +209,24 @@ def sssp_batch(g: Graph, srcs, delta: int, out=None, **opts):
         out = torch.empty((k, g.n), dtype=torch.int32, device=f"cuda:{g.device}")
     st = gi_sssp_batch(g, srcs, delta, out, make_options(**opts) if opts else None)
     return out, [st[i].to_dict() for i in range(k)]
+
+
+def gi_ppsp_delta(g: Graph, src: int, dst: int, delta: int, dist_st, options: gi_options | None = None,
+                  want_stats: bool = True):
+    """C-ABI gi_ppsp_delta_ex. dist_st: one-element uint32 (or int32) array/tensor."""
+    st = gi_stats() if want_stats else None
+    _check(_lib.gi_ppsp_delta_ex(g.handle, int(src), int(dst), int(delta),
+                                 ctypes.byref(options) if options else None, _ptr(dist_st),
+                                 ctypes.byref(st) if st is not None else None))
+    return st
+
+
+def ppsp(g: Graph, src: int, dst: int, delta: int, **opts):
+    """Point-to-point Δ-stepping with the paper's early stop. Returns (δ(src, dst) as a
+    Python int, UINT32_MAX if unreachable; stats dict)."""
+    out = np.zeros(1, np.uint32)
+    st = gi_ppsp_delta(g, src, dst, delta, out, make_options(**opts) if opts else None)
+    return int(out[0]), st.to_dict()
 
 
 def as_uint32(t) -> np.ndarray:

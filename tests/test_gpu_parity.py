@@ -287,3 +287,53 @@ def test_config4_full(gi):
     assert st["buckets"] == oracle.bucket_count(d, 2)
     ref, rc = oracle.dijkstra(g, src)
     assert rc == 0 and np.array_equal(d, ref)
+
+
+def test_ppsp_matches_oracle_and_stops_early(gi, config_graph):
+    """PPSP: δ(s,t) equals the Dijkstra oracle's
+    dist[t] on random triples; it never runs more buckets/rounds than SSSP
+    (SPEC.md:353); target == source costs one bucket; unreachable -> UINT32_MAX."""
+    rng = np.random.default_rng(31)
+    g = config_graph(1)
+    G = gi.Graph.from_csr(g)
+    for _ in range(20):
+        s, t = (int(x) for x in rng.integers(0, g.n, 2))
+        ref, _ = oracle.dijkstra(g, s)
+        for delta, o in ((1000, dict()), (250, dict(fusion=False)), (4000, dict(drain="async")), (7, dict())):
+            d, st = gi.ppsp(G, s, t, delta, **o)
+            assert d == int(ref[t]), (s, t, delta, o)
+            _, full = gi.sssp(G, s, delta, **o)
+            assert st["buckets"] <= full["buckets"] and st["rounds"] <= full["rounds"]
+    d, st = gi.ppsp(G, 77, 77, 1000)
+    assert d == 0 and st["buckets"] == 1
+    # random small graphs with unreachable targets, zero weights, parallel edges
+    for trial in range(30):
+        n = int(rng.integers(2, 400))
+        edges = [(int(rng.integers(0, n)), int(rng.integers(0, n)), int(rng.integers(0, 20)))
+                 for _ in range(int(rng.integers(0, 3 * n)))]
+        h = gen.from_edges(n, edges)
+        H = gi.Graph.from_csr(h)
+        s, t = int(rng.integers(0, n)), int(rng.integers(0, n))
+        ref, _ = oracle.dijkstra(h, s)
+        for delta in (1, 5, 1 << 20):
+            assert gi.ppsp(H, s, t, delta)[0] == int(ref[t]), (trial, s, t, delta)
+    # device scalar output and error codes
+    import torch
+    out = torch.zeros(1, dtype=torch.int32, device="cuda")
+    gi.gi_ppsp_delta(G, 0, 65535, 1000, out)
+    assert int(out.item()) == int(oracle.dijkstra(g, 0)[0][65535])
+    with pytest.raises(gi.GiError) as e:
+        gi.ppsp(G, 0, g.n, 1000)
+    assert e.value.status == 2
+    with pytest.raises(gi.GiError) as e:
+        gi.ppsp(G, 0, -1, 1000)
+    assert e.value.status == 2
+
+
+def test_ppsp_overflow_only_for_the_target(gi):
+    """Ex7-like: 0->1 (2^32-2), 1->2 (1). PPSP to 1 is fine; PPSP to 2 overflows."""
+    g = gen.from_edges(3, [(0, 1, 2**32 - 2), (1, 2, 1)])
+    G = gi.Graph.from_csr(g)
+    assert gi.ppsp(G, 0, 1, 1)[0] == 2**32 - 2
+    with pytest.raises(gi.OverflowDistance):
+        gi.ppsp(G, 0, 2, 1)
