@@ -49,6 +49,14 @@ constexpr int kXtr = 4;  // far-pile entries per thread per extraction chunk
 #define GI_BIGK 8
 #endif
 constexpr int kBigK = GI_BIGK;  // stage B: consecutive edges per thread per iteration
+#ifndef GI_SPILL_EDGES
+#define GI_SPILL_EDGES 16384
+#endif
+constexpr unsigned long long kSpillEdges = GI_SPILL_EDGES;
+#ifndef GI_CLAIMS
+#define GI_CLAIMS 4
+#endif
+constexpr uint32_t kClaimsPerCta = GI_CLAIMS;  // ROUND: ~claims per CTA per phase (chunk size)  // drain: spill a bin's big list above this
 
 #ifdef GI_TRACE
 // Debug builds only: cycles between trace points, accumulated by CTA 0 / thread 0 in
@@ -78,7 +86,7 @@ __shared__ long long s_trace_last;
 // async drain: per phase max over CTAs of feed+drain cycles / max depth; per item
 // (all CTAs, lane 0 of each warp) claim->atomics-returned, ->push-done, idle spins
 constexpr int kTracePhases = 16384;
-__device__ unsigned long long g_phase[4][kTracePhases];  // max drain (async), max depth, max busy, sum busy
+__device__ unsigned long long g_phase[7][kTracePhases];  // max drain (async), max depth, max busy, sum busy, mode, cnt, hubs
 __device__ unsigned long long g_item[16];
 #define ITRACE_T(var) long long var = clock64()
 #define ITRACE_DECL() unsigned long long it_acc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}
@@ -102,6 +110,10 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+__device__ __forceinline__ void red_min(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
@@ -159,6 +171,8 @@ struct BigEnt {
   int64_t beg;
   uint32_t deg;
   uint32_t du;
+  int32_t v;    // the vertex (CTA-local list only; -1 for hub slices)
+  uint32_t pad;
 };
 
 struct Shared {
@@ -204,6 +218,8 @@ struct Ctx {
   uint32_t hub_min, hubcap;
   uint32_t T;              // fusion threshold (async drain: ring occupancy limit)
   int32_t* farstage;       // CTA-local staging of far-pile pushes (shared memory, kFarStage)
+  uint32_t nv_spilled;     // thread 0: high-degree vertices counted, then spilled (re-counted later)
+  uint32_t big_spills;     // thread 0: edge-threshold spills
   Shared* s;
   uint32_t my_fmin;        // thread-local min far bucket (reduced at phase end)
   bool pre_read;
@@ -330,15 +346,23 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
     }
   }
   if (c.pre_read) {
-    uint32_t cur[K];
+    // pre-read dist[v]; only an improving candidate is written, with a fire-and-forget
+    // red.min, and the pre-read value stands for the atomic's old value. Two threads that
+    // both improve on the same pre-read may both push v: a duplicate entry, which the
+    // dedup bits (far pile) or the staleness probe (bins) absorb; the thread holding the
+    // final minimum always pushes (whoever wrote it first saw a larger value).
 #pragma unroll
-    for (int k = 0; k < K; ++k) cur[k] = (ok & (1u << k)) ? ld_dist(c.dist + e[k].x) : 0u;
+    for (int k = 0; k < K; ++k) old[k] = (ok & (1u << k)) ? ld_dist(c.dist + e[k].x) : 0u;
 #pragma unroll
     for (int k = 0; k < K; ++k)
-      if (!(nd[k] < cur[k])) ok &= ~(1u << k);
-  }
+      if (!(nd[k] < old[k])) ok &= ~(1u << k);
 #pragma unroll
-  for (int k = 0; k < K; ++k) old[k] = (ok & (1u << k)) ? atomicMin(c.dist + e[k].x, nd[k]) : 0u;
+    for (int k = 0; k < K; ++k)
+      if (ok & (1u << k)) red_min(c.dist + e[k].x, nd[k]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k) old[k] = (ok & (1u << k)) ? atomicMin(c.dist + e[k].x, nd[k]) : 0u;
+  }
   // late staleness: the probe of the source vertex (cur, issued with the slot load) was
   // not waited for before the atomics; an entry superseded by a newer one of the same
   // vertex drops its pushes (that entry's relaxations supersede these)
@@ -479,6 +503,7 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
             be.beg = (int64_t)(((uint64_t)hi << 32) | lo);
             be.deg = e[u].y;
             be.du = du[u];
+            be.v = (int32_t)v[u];
             c.big[pos] = be;
           } else {
             push_global(c, (int32_t)v[u]);  // list full: the next group-wide round takes it
@@ -502,7 +527,8 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
 // the degrees) and split evenly over all threads of the CTA, 4 edges per thread per
 // iteration; an edge finds its vertex by binary search in the prefix array.
 template <bool FUSED>
-__device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32_t& ne) {
+__device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32_t& ne,
+                                          unsigned long long spill_edges = 0) {
   constexpr int PER = kBigCap / kBlock;
   unsigned long long loc[PER];
   unsigned long long sum = 0;
@@ -542,6 +568,16 @@ __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32
   }
   __syncthreads();
   const unsigned long long total = s.total;
+  if (spill_edges && total > spill_edges) {
+    // edge-count threshold (SURVEY §8c O5 variant): a drained bin whose high-degree
+    // vertices carry more than spill_edges edges is "copied over to the global bucket"
+    // instead of straggling in this CTA; the next group-wide round
+    // claims it chunk by chunk across every CTA
+    bulk_append(s, nb, [&](uint32_t i) { return c.big[i].v; }, c.qbits_next, c.q_next, c.qcount_next, c.slots);
+    if (threadIdx.x == 0) { c.nv_spilled += nb; ++c.big_spills; }
+    return;
+  }
+  TRACE(12);
   if (threadIdx.x == 0) ne += (uint32_t)total;
   // each thread relaxes kBigK CONSECUTIVE edges per iteration: one binary search for
   // the first, then a forward walk (entries have deg >= 1 except empty hub slices, which
@@ -580,13 +616,14 @@ __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32
     }
     relax_batch<FUSED, kBigK>(c, e, du, valid);
   }
+  TRACE(13);
 }
 
 // Relax every entry of a CTA-local bin (stage A, then stage B when high-degree
 // vertices were found). Starts after and ends with a CTA barrier.
 template <bool FUSED>
 __device__ __forceinline__ void process_bin(Ctx& c, Shared& s, const uint2* in, uint32_t nin,
-                                            bool check_stale, uint32_t& nv, uint32_t& ne) {
+                                            bool check_stale, uint32_t& nv, uint32_t& ne, bool drain = false) {
   if (nin * 8 <= (uint32_t)kBlock) stage_small<FUSED, 1>(c, in, nin, check_stale, nv, ne);
   else stage_small<FUSED, 4>(c, in, nin, check_stale, nv, ne);
   __syncthreads();
@@ -595,7 +632,7 @@ __device__ __forceinline__ void process_bin(Ctx& c, Shared& s, const uint2* in, 
   if (nb) {
     __syncthreads();  // everyone has read bigtail
     if (threadIdx.x == 0) s.bigtail = 0;
-    stage_big<FUSED>(c, s, nb, ne);
+    stage_big<FUSED>(c, s, nb, ne, (FUSED && drain) ? (unsigned long long)kSpillEdges : 0ull);
     __syncthreads();
   }
 }
@@ -1010,6 +1047,8 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     c.s = &s;
     c.pre_read = a.pre_read != 0;
     c.hub_min = a.hub_min;
+    c.nv_spilled = 0;
+    c.big_spills = 0;
     c.hubcap = a.hubcap;
     c.T = T;
     c.farstage = ASYNC ? reinterpret_cast<int32_t*>(s_dyn + (kRing + (kBlock / 32) * 4) * 10)
@@ -1069,6 +1108,9 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
       TRACE(5);
 #ifdef GI_TRACE
       const long long t_busy0 = clock64();
+      if (blockIdx.x == 0 && tid == 0 && p < (uint32_t)kTracePhases) {
+        g_phase[4][p] = s.mode; g_phase[5][p] = s.cnt; g_phase[6][p] = s.hn;
+      }
 #endif
       const uint32_t mode = s.mode;
       if (mode == MODE_DONE) break;
@@ -1216,11 +1258,13 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
             be.beg = he.beg + (int64_t)lo_e;
             be.deg = (uint32_t)(hi_e - lo_e);
             be.du = he.du;
+            be.v = -1;
             c.big[i] = be;
           }
           __syncthreads();
           stage_big<FUSED>(c, s, nh, ne);
           __syncthreads();
+          TRACE(15);
         }
         // ROUND: relax the group's global frontier, one slice per CTA, staged through
         // bin 1 in chunks (pushes go to bin 0, which the drain below consumes)
@@ -1230,7 +1274,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
         // while the current chunk is relaxed): skewed degrees make equal vertex slices
         // unequal work, and a CTA that drew heavy vertices simply claims fewer chunks.
         uint2* stage = s_dyn + kBinCap;
-        const uint32_t claim = max(32u, min((uint32_t)kBinCap, cnt / (4 * G)));
+        const uint32_t claim = max(32u, min((uint32_t)kBinCap, cnt / (kClaimsPerCta * G)));
         uint32_t* qclaim = &ctl->qclaim[p % 3];
         uint32_t next = 0;
         if (tid == 0) next = atomicAdd(qclaim, claim);
@@ -1261,6 +1305,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
             }
           }
           __syncthreads();
+          TRACE(14);
           process_bin<FUSED>(c, s, stage, chunk, false, nv, ne);  // ends with a barrier
         }
         __syncthreads();
@@ -1288,7 +1333,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
           if (tid == 0) { s.cnt3[(k + 1) % 3] = 0; ++subrounds; }
           c.out = s_dyn + (k & 1) * kBinCap;
           c.outcnt = &s.cnt3[k % 3];
-          process_bin<FUSED>(c, s, in, nin, true, nv, ne);
+          process_bin<FUSED>(c, s, in, nin, true, nv, ne, true);
         }
       }
 
@@ -1315,6 +1360,12 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
         }
       }
       tnv += nv; tne += ne; nv = 0; ne = 0;
+      if (tid == 0) {  // spilled high-degree vertices are counted again where they are relaxed
+        tnv -= c.nv_spilled;  // (mod 2^64; the block total stays exact)
+        spills += c.big_spills;
+        c.nv_spilled = 0;
+        c.big_spills = 0;
+      }
       TRACE(8);
 #ifdef GI_TRACE
       if (tid == 0 && p < (uint32_t)kTracePhases) {
@@ -1439,10 +1490,10 @@ int smem_bytes(int kind) {
 #ifdef GI_TRACE
 extern "C" int gi_debug_trace2(unsigned long long* phase, unsigned long long* item, int reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(phase, g_phase, sizeof(unsigned long long) * 4 * kTracePhases);
+  cudaMemcpyFromSymbol(phase, g_phase, sizeof(unsigned long long) * 7 * kTracePhases);
   cudaMemcpyFromSymbol(item, g_item, sizeof(unsigned long long) * 16);
   if (reset) {
-    static unsigned long long z[4 * kTracePhases];
+    static unsigned long long z[7 * kTracePhases];
     cudaMemcpyToSymbol(g_phase, z, sizeof(z));
     cudaMemcpyToSymbol(g_item, z, sizeof(unsigned long long) * 16);
   }

@@ -50,7 +50,7 @@ opt.drain = {"async": 2, "bsp": 1, "unfused": 1}[drain]
 opt.fusion = 0 if drain == "unfused" else 1
 st = gi_stats()
 buf = np.zeros(32, np.uint64)
-ph = np.zeros((4, 16384), np.uint64)
+ph = np.zeros((7, 16384), np.uint64)
 it = np.zeros(16, np.uint64)
 for rep in range(2):
     lib.gi_debug_trace(buf.ctypes.data, 1)
@@ -63,7 +63,8 @@ print(what, "delta", delta, "drain", drain, "max_ctas", max_ctas, "gpu_ms %.3f" 
       st.fused_subrounds, "critical", st.critical_subrounds, "buckets", st.buckets, "kind", st.kernel_kind)
 clk = 1.965e3  # cycles per µs at the max SM clock
 names = {0: "bsp drain loop top", 2: "slot load", 3: "relax", 4: "rest", 5: "decision", 6: "feed (async) / extract",
-         7: "phase work end", 8: "far flush + fmin", 9: "group barrier", 11: "drain (async, CTA 0)"}
+         7: "phase work end", 8: "far flush + fmin", 9: "group barrier", 11: "drain (async, CTA 0)",
+         12: "stage B scan", 13: "stage B edge loop", 14: "ROUND claim+staging", 15: "hub slices (after B)"}
 tot = 0
 for k in range(16):
     c = int(buf[16 + k])
@@ -90,5 +91,7 @@ if m2.any():
     print(f"phases {int(m2.sum())}: sum of max-CTA busy {mx[m2].sum() / clk / 1e3:.3f} ms, sum of mean-CTA busy "
           f"{sm[m2].sum() / G / clk / 1e3:.3f} ms (imbalance {mx[m2].sum() / max(sm[m2].sum() / G, 1):.2f}x); "
           f"gpu_ms {st.gpu_ms:.3f}")
-    top = np.argsort(-mx)[:8]
-    print("  heaviest phases (us max / mean):", [(int(i), round(mx[i] / clk, 1), round(sm[i] / G / clk, 1)) for i in top])
+    top = np.argsort(-mx)[:10]
+    print("  heaviest phases: (phase, us max, us mean, mode 0=ROUND/1=EXTRACT, cnt, hubs)")
+    for i in top:
+        print("   ", int(i), round(mx[i] / clk, 1), round(sm[i] / G / clk, 1), int(ph[4][i]), int(ph[5][i]), int(ph[6][i]))
