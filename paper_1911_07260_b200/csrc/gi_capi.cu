@@ -335,6 +335,7 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   // relaxations (skewed degrees), costs one L2 round trip per level otherwise
   a.pre_read = opt.pre_read == 1 ? 1u : opt.pre_read == 2 ? 0u : (g->max_deg > 32 ? 1u : 0u);
   a.target = target;
+  a.dyn_claim = g->max_deg > 32 ? 1u : 0u;
 
   if ((e = cudaEventRecord(w->ev0, st))) return bail(e, "event");
   if ((e = launch_sssp(a, kind, G * ngroups, st))) return bail(e, "launch sssp_persistent");

@@ -14,7 +14,10 @@ constexpr uint32_t kDefaultTSkewed = 256;  // ... and on skewed graphs (max out-
 constexpr int kSlotEdges = 8;        // ELL slot: up to 8 {col, w} edges inline (64 B per vertex)
 constexpr uint32_t kColEmpty = 0xFFFFFFFFu;  // unused slot entry
 constexpr uint32_t kColBig = 0xFFFFFFFEu;    // deg > 8: all 8 entries {kColBig, payload}; payloads deg, beg_lo, beg_hi
-constexpr int kFarStage = 8192;      // CTA-local staging of far-pile pushes (flushed at phase end)
+#ifndef GI_FARSTAGE
+#define GI_FARSTAGE 8192
+#endif
+constexpr int kFarStage = GI_FARSTAGE;  // CTA-local staging of far-pile pushes (flushed at phase end)
 constexpr uint32_t kDefaultHubMin = 1024;  // default out-degree for the group-wide hub path
 constexpr uint32_t kMinHubMin = 256;       // smallest accepted hub_min (bounds the hub-list size)
 constexpr int kRingLog = 11;
@@ -103,6 +106,7 @@ struct KArgs {
   uint32_t hub_min;     // out-degree >= hub_min -> the vertex's edges are split over the group
   uint32_t hubcap;      // capacity of each hub list
   int32_t target;       // PPSP: stop once the next bucket's lower bound reaches dist[target]; -1 = SSSP
+  uint32_t dyn_claim;   // ROUND phases claim frontier chunks dynamically (skewed degrees) vs equal slices
 };
 
 // Host-side launchers (gi_kernels.cu).

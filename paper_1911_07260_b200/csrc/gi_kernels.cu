@@ -49,14 +49,11 @@ constexpr int kXtr = 4;  // far-pile entries per thread per extraction chunk
 #define GI_BIGK 8
 #endif
 constexpr int kBigK = GI_BIGK;  // stage B: consecutive edges per thread per iteration
-#ifndef GI_SPILL_EDGES
-#define GI_SPILL_EDGES 16384
-#endif
-constexpr unsigned long long kSpillEdges = GI_SPILL_EDGES;
 #ifndef GI_CLAIMS
 #define GI_CLAIMS 4
 #endif
-constexpr uint32_t kClaimsPerCta = GI_CLAIMS;  // ROUND: ~claims per CTA per phase (chunk size)  // drain: spill a bin's big list above this
+constexpr uint32_t kClaimsPerCta = GI_CLAIMS;  // ROUND: ~claims per CTA per phase (chunk size)
+  // drain: spill a bin's big list above this
 
 #ifdef GI_TRACE
 // Debug builds only: cycles between trace points, accumulated by CTA 0 / thread 0 in
@@ -171,8 +168,6 @@ struct BigEnt {
   int64_t beg;
   uint32_t deg;
   uint32_t du;
-  int32_t v;    // the vertex (CTA-local list only; -1 for hub slices)
-  uint32_t pad;
 };
 
 struct Shared {
@@ -218,8 +213,6 @@ struct Ctx {
   uint32_t hub_min, hubcap;
   uint32_t T;              // fusion threshold (async drain: ring occupancy limit)
   int32_t* farstage;       // CTA-local staging of far-pile pushes (shared memory, kFarStage)
-  uint32_t nv_spilled;     // thread 0: high-degree vertices counted, then spilled (re-counted later)
-  uint32_t big_spills;     // thread 0: edge-threshold spills
   Shared* s;
   uint32_t my_fmin;        // thread-local min far bucket (reduced at phase end)
   bool pre_read;
@@ -274,14 +267,42 @@ __device__ __noinline__ void mark_overflow(uint32_t* ovfbits, uint32_t* ovf_cand
   atomicOr(ovf_cand, 1u);
 }
 
-// Block-wide dedup-append of n staged vertices to a global list: the bit test-and-set
-// (atomicOr) of 4 entries per thread is in flight at once and the list positions come
-// from one global atomic per CTA per chunk (block scan), so that a flush of thousands
-// of entries costs a few round trips, not one chain per entry. All threads call it.
+// Warp-aggregated append of the entries v[x] with bit x of `m` set (per lane) to a
+// global list: a warp scan of the per-lane counts and ONE atomicAdd per warp.
+template <int X>
+__device__ __forceinline__ void warp_append(uint32_t m, const int32_t (&v)[X], int32_t* list, uint32_t* count,
+                                            const uint2* slots_pf) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nk = __popc(m);
+  uint32_t incl = nk;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += t;
+  }
+  const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+  if (tot == 0) return;
+  uint32_t base = 0;
+  if (lane == 0) base = atomicAdd(count, tot);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  uint32_t off = base + incl - nk;
+#pragma unroll
+  for (int x = 0; x < X; ++x)
+    if (m & (1u << x)) {
+      if (slots_pf) prefetch_l2(slots_pf + 8 * (size_t)v[x]);
+      list[off++] = v[x];
+    }
+}
+
+// Dedup-append of n staged vertices to a global list: the bit test-and-set (atomicOr)
+// of 4 entries per thread is in flight at once, and the list positions come from one
+// global atomic per WARP per 128 entries (warp scan) — no CTA barrier, so that a small
+// flush costs one round trip and a large one a few, not one chain per entry. All
+// threads call it (warp-uniform trip count).
 template <typename Get>
-__device__ __forceinline__ void bulk_append(Shared& s, uint32_t n, Get get, uint32_t* bits, int32_t* list,
-                                            uint32_t* count, const uint2* slots_pf) {
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__device__ __forceinline__ void bulk_append(uint32_t n, Get get, uint32_t* bits, int32_t* list, uint32_t* count,
+                                            const uint2* slots_pf) {
+  const uint32_t lane = threadIdx.x & 31;
   for (uint32_t base = 0; base < n; base += 4 * kBlock) {
     int32_t v[4];
     uint32_t old[4];
@@ -296,35 +317,7 @@ __device__ __forceinline__ void bulk_append(Shared& s, uint32_t n, Get get, uint
 #pragma unroll
     for (int x = 0; x < 4; ++x)
       if (v[x] >= 0 && !(old[x] & (1u << (v[x] & 31)))) newm |= 1u << x;
-    const uint32_t nk = __popc(newm);
-    uint32_t incl = nk;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= (uint32_t)o) incl += t;
-    }
-    if (lane == 31) s.redw[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t w = lane < kBlock / 32 ? s.redw[lane] : 0u;
-      uint32_t wi = w;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
-        if (lane >= (uint32_t)o) wi += t;
-      }
-      if (lane < kBlock / 32) s.redw[lane] = wi - w;
-      const uint32_t tot = __shfl_sync(0xffffffffu, wi, kBlock / 32 - 1);
-      if (lane == 0) s.xbase = tot ? atomicAdd(count, tot) : 0u;
-    }
-    __syncthreads();
-    uint32_t off = s.xbase + s.redw[warp] + incl - nk;
-#pragma unroll
-    for (int x = 0; x < 4; ++x)
-      if (newm & (1u << x)) {
-        if (slots_pf) prefetch_l2(slots_pf + 8 * (size_t)v[x]);
-        list[off++] = v[x];
-      }
+    warp_append(newm, v, list, count, slots_pf);
   }
 }
 
@@ -503,7 +496,6 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
             be.beg = (int64_t)(((uint64_t)hi << 32) | lo);
             be.deg = e[u].y;
             be.du = du[u];
-            be.v = (int32_t)v[u];
             c.big[pos] = be;
           } else {
             push_global(c, (int32_t)v[u]);  // list full: the next group-wide round takes it
@@ -527,8 +519,7 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
 // the degrees) and split evenly over all threads of the CTA, 4 edges per thread per
 // iteration; an edge finds its vertex by binary search in the prefix array.
 template <bool FUSED>
-__device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32_t& ne,
-                                          unsigned long long spill_edges = 0) {
+__device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32_t& ne) {
   constexpr int PER = kBigCap / kBlock;
   unsigned long long loc[PER];
   unsigned long long sum = 0;
@@ -568,15 +559,6 @@ __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32
   }
   __syncthreads();
   const unsigned long long total = s.total;
-  if (spill_edges && total > spill_edges) {
-    // edge-count threshold (SURVEY §8c O5 variant): a drained bin whose high-degree
-    // vertices carry more than spill_edges edges is "copied over to the global bucket"
-    // instead of straggling in this CTA; the next group-wide round
-    // claims it chunk by chunk across every CTA
-    bulk_append(s, nb, [&](uint32_t i) { return c.big[i].v; }, c.qbits_next, c.q_next, c.qcount_next, c.slots);
-    if (threadIdx.x == 0) { c.nv_spilled += nb; ++c.big_spills; }
-    return;
-  }
   TRACE(12);
   if (threadIdx.x == 0) ne += (uint32_t)total;
   // each thread relaxes kBigK CONSECUTIVE edges per iteration: one binary search for
@@ -623,7 +605,7 @@ __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32
 // vertices were found). Starts after and ends with a CTA barrier.
 template <bool FUSED>
 __device__ __forceinline__ void process_bin(Ctx& c, Shared& s, const uint2* in, uint32_t nin,
-                                            bool check_stale, uint32_t& nv, uint32_t& ne, bool drain = false) {
+                                            bool check_stale, uint32_t& nv, uint32_t& ne) {
   if (nin * 8 <= (uint32_t)kBlock) stage_small<FUSED, 1>(c, in, nin, check_stale, nv, ne);
   else stage_small<FUSED, 4>(c, in, nin, check_stale, nv, ne);
   __syncthreads();
@@ -632,7 +614,7 @@ __device__ __forceinline__ void process_bin(Ctx& c, Shared& s, const uint2* in, 
   if (nb) {
     __syncthreads();  // everyone has read bigtail
     if (threadIdx.x == 0) s.bigtail = 0;
-    stage_big<FUSED>(c, s, nb, ne, (FUSED && drain) ? (unsigned long long)kSpillEdges : 0ull);
+    stage_big<FUSED>(c, s, nb, ne);
     __syncthreads();
   }
 }
@@ -1047,8 +1029,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     c.s = &s;
     c.pre_read = a.pre_read != 0;
     c.hub_min = a.hub_min;
-    c.nv_spilled = 0;
-    c.big_spills = 0;
+
     c.hubcap = a.hubcap;
     c.T = T;
     c.farstage = ASYNC ? reinterpret_cast<int32_t*>(s_dyn + (kRing + (kBlock / 32) * 4) * 10)
@@ -1183,11 +1164,10 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
       } else if (mode == MODE_EXTRACT) {
         // (d)+(a): partition the far pile by recomputed bucket.
         // kXtr entries per thread per chunk with every load in flight together; the
-        // entries kept for later buckets are compacted with one global atomic per CTA
-        // per chunk (block scan), not one per warp per entry.
+        // entries kept for later buckets are compacted with one global atomic per warp
+        // per chunk (warp scan), not one per warp per entry.
         const int32_t* far_src = (j & 1) ? ws.far[0] : ws.far[1];
         uint32_t nlive = 0;
-        const uint32_t lane = tid & 31, warp = tid >> 5;
         for (uint32_t base = lo; base < hi; base += kXtr * kBlock) {
           int32_t v[kXtr];
           uint32_t d[kXtr];
@@ -1211,32 +1191,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
               keepm |= 1u << x;
             }
           }
-          const uint32_t nk = __popc(keepm);
-          uint32_t incl = nk;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= (uint32_t)o) incl += t;
-          }
-          if (lane == 31) s.redw[warp] = incl;
-          __syncthreads();
-          if (warp == 0) {
-            const uint32_t w = lane < kBlock / 32 ? s.redw[lane] : 0u;
-            uint32_t wi = w;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
-              if (lane >= (uint32_t)o) wi += t;
-            }
-            if (lane < kBlock / 32) s.redw[lane] = wi - w;
-            const uint32_t tot = __shfl_sync(0xffffffffu, wi, kBlock / 32 - 1);
-            if (lane == 0) s.xbase = tot ? atomicAdd(c.fcount_live, tot) : 0u;
-          }
-          __syncthreads();
-          uint32_t off = s.xbase + s.redw[warp] + incl - nk;
-#pragma unroll
-          for (int x = 0; x < kXtr; ++x)
-            if (keepm & (1u << x)) c.far_live[off++] = v[x];
+          warp_append(keepm, v, c.far_live, c.fcount_live, nullptr);
         }
         TRACE(6);
         const uint32_t tl = block_sum(nlive, s);  // ends with a barrier: ring fill is final
@@ -1258,7 +1213,6 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
             be.beg = he.beg + (int64_t)lo_e;
             be.deg = (uint32_t)(hi_e - lo_e);
             be.du = he.du;
-            be.v = -1;
             c.big[i] = be;
           }
           __syncthreads();
@@ -1270,23 +1224,30 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
         // bin 1 in chunks (pushes go to bin 0, which the drain below consumes)
         const int32_t* q_in = (p & 1) ? ws.q[1] : ws.q[0];
         uint32_t* qbits_in = (p & 1) ? ws.qbits[1] : ws.qbits[0];
-        // Chunks are CLAIMED dynamically (one atomic per chunk, the next claim in flight
-        // while the current chunk is relaxed): skewed degrees make equal vertex slices
-        // unequal work, and a CTA that drew heavy vertices simply claims fewer chunks.
+        // Skewed graphs (a.dyn_claim): chunks are CLAIMED dynamically (one atomic per
+        // chunk, the next claim in flight while the current chunk is relaxed), since equal
+        // vertex slices are unequal work and a CTA that drew heavy vertices should claim
+        // fewer chunks. The first chunk of every CTA is static (rank * claim), so a small
+        // frontier costs no atomic. Otherwise: equal static slices (one pass per CTA,
+        // every CTA busy — the latency-bound rounds of road graphs).
         uint2* stage = s_dyn + kBinCap;
-        const uint32_t claim = max(32u, min((uint32_t)kBinCap, cnt / (kClaimsPerCta * G)));
+        const uint32_t claim = a.dyn_claim ? max(32u, min((uint32_t)kBinCap, cnt / (kClaimsPerCta * G)))
+                                           : (uint32_t)kBinCap;
+        const uint64_t first = a.dyn_claim ? (uint64_t)G * claim : (uint64_t)cnt;
+        const bool dyn = first < cnt;
         uint32_t* qclaim = &ctl->qclaim[p % 3];
         uint32_t next = 0;
-        if (tid == 0) next = atomicAdd(qclaim, claim);
+        if (tid == 0) {
+          s.claim = rank * claim;
+          if (dyn) next = (uint32_t)first + atomicAdd(qclaim, claim);  // in flight during chunk 1
+        }
+        if (a.dyn_claim) __syncthreads();
+        const uint32_t end = a.dyn_claim ? cnt : hi;
+        uint32_t base_static = lo;
         for (;;) {
-          if (tid == 0) {
-            s.claim = next;
-            if (next < cnt) next = atomicAdd(qclaim, claim);  // in flight during this chunk
-          }
-          __syncthreads();
-          const uint32_t base = s.claim;
-          if (base >= cnt) break;
-          const uint32_t chunk = min(claim, cnt - base);
+          const uint32_t base = a.dyn_claim ? s.claim : base_static;
+          if (base >= end) break;
+          const uint32_t chunk = a.dyn_claim ? min(claim, cnt - base) : min((uint32_t)kBinCap, hi - base);
           for (uint32_t i0 = 0; i0 < chunk; i0 += 4 * kBlock) {  // one pass: chunk <= kBinCap
             int32_t vv[4];
             uint32_t dd[4];
@@ -1307,6 +1268,15 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
           __syncthreads();
           TRACE(14);
           process_bin<FUSED>(c, s, stage, chunk, false, nv, ne);  // ends with a barrier
+          if (a.dyn_claim) {
+            if (tid == 0) {
+              s.claim = dyn ? next : cnt;
+              if (dyn && next < cnt) next = (uint32_t)first + atomicAdd(qclaim, claim);
+            }
+            __syncthreads();
+          } else {
+            base_static = base + chunk;
+          }
         }
         __syncthreads();
       }
@@ -1325,7 +1295,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
           const uint32_t nin = min(s.cnt3[(k - 1) % 3], (uint32_t)kBinCap);
           if (nin == 0) break;
           if (nin >= T) {
-            bulk_append(s, nin, [&](uint32_t i) { return (int32_t)in[i].x; }, c.qbits_next, c.q_next,
+            bulk_append(nin, [&](uint32_t i) { return (int32_t)in[i].x; }, c.qbits_next, c.q_next,
                         c.qcount_next, c.slots);
             if (tid == 0) ++spills;
             break;
@@ -1333,7 +1303,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
           if (tid == 0) { s.cnt3[(k + 1) % 3] = 0; ++subrounds; }
           c.out = s_dyn + (k & 1) * kBinCap;
           c.outcnt = &s.cnt3[k % 3];
-          process_bin<FUSED>(c, s, in, nin, true, nv, ne, true);
+          process_bin<FUSED>(c, s, in, nin, true, nv, ne);
         }
       }
 
@@ -1344,7 +1314,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
       {
         const uint32_t nf = min(s.farcnt, (uint32_t)kFarStage);
         const int32_t* fs = c.farstage;
-        bulk_append(s, nf, [&](uint32_t i) { return fs[i]; }, c.farbits, c.far_live, c.fcount_live, nullptr);
+        bulk_append(nf, [&](uint32_t i) { return fs[i]; }, c.farbits, c.far_live, c.fcount_live, nullptr);
         uint32_t fm = __reduce_min_sync(0xffffffffu, c.my_fmin);
         if ((tid & 31) == 0 && fm != kInf) atomicMin(&s.fmin, fm);
         __syncthreads();
@@ -1360,12 +1330,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
         }
       }
       tnv += nv; tne += ne; nv = 0; ne = 0;
-      if (tid == 0) {  // spilled high-degree vertices are counted again where they are relaxed
-        tnv -= c.nv_spilled;  // (mod 2^64; the block total stays exact)
-        spills += c.big_spills;
-        c.nv_spilled = 0;
-        c.big_spills = 0;
-      }
+
       TRACE(8);
 #ifdef GI_TRACE
       if (tid == 0 && p < (uint32_t)kTracePhases) {
