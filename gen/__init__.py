@@ -199,6 +199,18 @@ def sources(n: int, k: int, seed: int = 5) -> np.ndarray:
     return out
 
 
+def grid_heuristic(rows: int, cols: int, target: int, scale: int) -> np.ndarray:
+    """A* input for a row-major rows x cols grid (id = r*cols + c): h(v) = scale x the
+    Chebyshev distance from v to target. With scale <= the smallest edge weight it is
+    admissible and consistent on 4-neighbour grids with diagonals (an edge changes the
+    Chebyshev distance by at most 1). Coordinates only; no shortest-path arithmetic."""
+    r = np.arange(rows * cols, dtype=np.int64) // cols
+    c = np.arange(rows * cols, dtype=np.int64) % cols
+    tr, tc = divmod(int(target), cols)
+    h = np.maximum(np.abs(r - tr), np.abs(c - tc)) * int(scale)
+    return np.minimum(h, 0xFFFFFFFE).astype(np.uint32)
+
+
 def max_degree_vertex(g: CSR) -> int:
     """Highest out-degree vertex, ties -> smallest id."""
     return int(np.argmax(g.degrees()))

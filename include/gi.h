@@ -156,6 +156,23 @@ gi_status gi_ppsp_delta(const gi_graph* g, int32_t src, int32_t dst, uint32_t de
 gi_status gi_ppsp_delta_ex(const gi_graph* g, int32_t src, int32_t dst, uint32_t delta, const gi_options* opt,
                            uint32_t* dist_st, gi_stats* stats);
 
+/* A* search: PPSP whose bucket priority is the ESTIMATED distance of the
+ * path through v, dist(v) + h(v) — "uses the estimated distance of the shortest path that
+ * goes from the source to the target vertex that passes through the current vertex as the
+ * priority". A priority below the current bucket is raised to it, the
+ * bucket form of the monotone max(f + h, g[src]) of the paper's Fig. 11.
+ *   h        uint32[n], host or device (on the graph's device): the heuristic, an estimate
+ *            of the remaining distance to dst (e.g. w_min x grid Chebyshev distance). It is
+ *            COPIED (host) or read in place (device) for the call.
+ *   src/dst/delta/dist_st as gi_ppsp_delta.
+ * dist_st = δ(src, dst) exactly when h is admissible (h(v) <= δ(v, dst) for every v); an
+ * inadmissible h may return a longer path length (never a shorter one). GI_ERR_UNSUPPORTED
+ * with the async drain (opt->drain == 2). */
+gi_status gi_astar_delta(const gi_graph* g, int32_t src, int32_t dst, uint32_t delta, const uint32_t* h,
+                         uint32_t* dist_st);
+gi_status gi_astar_delta_ex(const gi_graph* g, int32_t src, int32_t dst, uint32_t delta, const uint32_t* h,
+                            const gi_options* opt, uint32_t* dist_st, gi_stats* stats);
+
 /* Thread-local description of the last non-OK status returned on this thread. */
 const char* gi_last_error(void);
 

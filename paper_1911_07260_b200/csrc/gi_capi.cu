@@ -66,6 +66,8 @@ struct Workspace {
   int srccap = 0;
   uint32_t* d_stage = nullptr;  // staging for host dist_out
   size_t stagecap = 0;
+  uint32_t* d_h = nullptr;      // staging for a host A* heuristic
+  size_t hcap = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
@@ -75,6 +77,7 @@ struct Workspace {
     if (d_qstats) cudaFree(d_qstats);
     if (d_srcs) cudaFree(d_srcs);
     if (d_stage) cudaFree(d_stage);
+    if (d_h) cudaFree(d_h);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
@@ -216,7 +219,7 @@ void fill_stats(gi_stats* st, const QStats& q, float ms, int ctas, int groups, i
 
 gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, uint32_t delta,
                       const gi_options* opt_in, uint32_t* dist_out, gi_stats* stats, bool batch,
-                      int32_t target = -1) {
+                      int32_t target = -1, const uint32_t* heur = nullptr) {
   gi_graph* g = const_cast<gi_graph*>(cg_);
   if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "graph is NULL");
   if (nsrc < 0) return fail(GI_ERR_INVALID_ARGUMENT, "nsrc < 0");
@@ -253,6 +256,7 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
 
   const bool fused = opt.fusion != 0;
   if (opt.drain > 2) return fail(GI_ERR_INVALID_ARGUMENT, "drain must be 0 (auto), 1 (bsp) or 2 (async)");
+  if (heur && fused && opt.drain == 2) return fail(GI_ERR_UNSUPPORTED, "A* runs with the bsp drain (drain 0/1)");
   if (fused && opt.drain == 2 && g->max_deg > kAsyncMaxDeg)
     return fail(GI_ERR_UNSUPPORTED, "async drain needs max out-degree <= %u (graph has %u)", kAsyncMaxDeg,
                 g->max_deg);
@@ -309,6 +313,25 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
     }
     d_dist = w->d_stage;
   }
+  const uint32_t* d_h = nullptr;  // A*: the heuristic on the device (caller's or staged)
+  if (heur) {
+    bool hwrong = false;
+    if (is_device_ptr(heur, g->device, &hwrong)) {
+      if (hwrong) { ws_release(g, w, true); return fail(GI_ERR_INVALID_ARGUMENT, "h on another device"); }
+      d_h = heur;
+    } else {
+      if (w->hcap < (size_t)g->n) {
+        if (w->d_h) cudaFree(w->d_h);
+        w->d_h = nullptr;
+        w->hcap = 0;
+        if ((e = cudaMalloc(&w->d_h, (size_t)g->n * 4)) != cudaSuccess) return bail(e, "alloc heuristic");
+        w->hcap = (size_t)g->n;
+      }
+      if ((e = cudaMemcpyAsync(w->d_h, heur, (size_t)g->n * 4, cudaMemcpyHostToDevice, st)))
+        return bail(e, "copy heuristic");
+      d_h = w->d_h;
+    }
+  }
   if ((e = cudaMemcpyAsync(w->d_srcs, hsrc.data(), sizeof(int32_t) * nsrc, cudaMemcpyHostToDevice, st)))
     return bail(e, "copy srcs");
   if ((e = cudaMemsetAsync(w->d_qstats, 0, sizeof(QStats) * nsrc, st))) return bail(e, "memset qstats");
@@ -336,6 +359,7 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   a.pre_read = opt.pre_read == 1 ? 1u : opt.pre_read == 2 ? 0u : (g->max_deg > 32 ? 1u : 0u);
   a.target = target;
   a.dyn_claim = g->max_deg > 32 ? 1u : 0u;
+  a.h = d_h;
 
   if ((e = cudaEventRecord(w->ev0, st))) return bail(e, "event");
   if ((e = launch_sssp(a, kind, G * ngroups, st))) return bail(e, "launch sssp_persistent");
@@ -536,6 +560,18 @@ gi_status gi_ppsp_delta_ex(const gi_graph* g, int32_t src, int32_t dst, uint32_t
 
 gi_status gi_ppsp_delta(const gi_graph* g, int32_t src, int32_t dst, uint32_t delta, uint32_t* dist_st) {
   return gi_ppsp_delta_ex(g, src, dst, delta, nullptr, dist_st, nullptr);
+}
+
+gi_status gi_astar_delta_ex(const gi_graph* g, int32_t src, int32_t dst, uint32_t delta, const uint32_t* h,
+                            const gi_options* opt, uint32_t* dist_st, gi_stats* stats) {
+  if (dst < 0) return fail(GI_ERR_OUT_OF_RANGE, "target %d < 0", dst);
+  if (!h) return fail(GI_ERR_INVALID_ARGUMENT, "heuristic h is NULL");
+  return run_queries(g, &src, 1, delta, opt, dist_st, stats, false, dst, h);
+}
+
+gi_status gi_astar_delta(const gi_graph* g, int32_t src, int32_t dst, uint32_t delta, const uint32_t* h,
+                         uint32_t* dist_st) {
+  return gi_astar_delta_ex(g, src, dst, delta, h, nullptr, dist_st, nullptr);
 }
 
 }  // extern "C"

@@ -6,7 +6,14 @@
 namespace gi {
 
 constexpr uint32_t kInf = 0xFFFFFFFFu;
-constexpr int kBlock = 512;          // threads per persistent CTA
+#ifndef GI_BLOCK
+#define GI_BLOCK 512
+#endif
+#ifndef GI_MINB
+#define GI_MINB 1
+#endif
+constexpr int kBlock = GI_BLOCK;     // threads per persistent CTA
+constexpr int kMinBlocksPerSm = GI_MINB;
 constexpr int kBinCap = 2048;        // CTA-local current-bucket bin of uint2 {v, d}; two (ping-pong) per CTA
 constexpr int kBigCap = 2048;        // CTA-local list of high-degree vertices (deg > 8) per bin
 constexpr uint32_t kDefaultT = 1024; // fusion threshold default (vertices per CTA bin), max out-degree <= 32
@@ -107,6 +114,7 @@ struct KArgs {
   uint32_t hubcap;      // capacity of each hub list
   int32_t target;       // PPSP: stop once the next bucket's lower bound reaches dist[target]; -1 = SSSP
   uint32_t dyn_claim;   // ROUND phases claim frontier chunks dynamically (skewed degrees) vs equal slices
+  const uint32_t* h;    // A*: per-vertex heuristic (priority = dist + h); nullptr = 0 (SSSP / PPSP)
 };
 
 // Host-side launchers (gi_kernels.cu).

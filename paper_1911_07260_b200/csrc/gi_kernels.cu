@@ -137,6 +137,14 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
   return (t + ((x - t) >> f.s1)) >> f.s2;
 }
 
+// Bucket of a tentative distance d under the A* priority d + h(v) (the
+// "estimated distance" of the path through v). h = 0 for SSSP/PPSP. A priority past
+// UINT32_MAX-1 lands in the last bucket (a merged top bucket is still exact).
+__device__ __forceinline__ uint32_t prio_bucket(uint32_t d, uint32_t hv, const FastDiv& f) {
+  const uint32_t p = d + hv;
+  return fdiv((p < d || p == kInf) ? kInf - 1u : p, f);
+}
+
 // Barrier over the G CTAs of one group (all co-resident: cooperative launch).
 // One word: arrivals in the low 16 bits, generation in the high 16; the last
 // arriver resets the count and bumps the generation with a single atomic.
@@ -213,6 +221,7 @@ struct Ctx {
   uint32_t hub_min, hubcap;
   uint32_t T;              // fusion threshold (async drain: ring occupancy limit)
   int32_t* farstage;       // CTA-local staging of far-pile pushes (shared memory, kFarStage)
+  const uint32_t* h;       // A* heuristic per vertex (nullptr: SSSP/PPSP)
   Shared* s;
   uint32_t my_fmin;        // thread-local min far bucket (reduced at phase end)
   bool pre_read;
@@ -366,15 +375,20 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
       if (cur[k] < du[k]) stale |= 1u << k;
     ok &= ~stale;
   }
-  // classify the successful lowerings: current bucket (bin) or a future one (far pile)
+  // classify the successful lowerings: current bucket (bin) or a future one (far pile).
+  // A*: priority bucket of nd + h(v), raised to the current bucket if an inconsistent
+  // heuristic would put it below (the monotone max(f + h, g[src]) of SPEC.md:355-358).
+  uint32_t hv[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) hv[k] = (c.h && (ok & (1u << k))) ? __ldg(c.h + e[k].x) : 0u;
   uint32_t curm = 0, farm = 0;
   uint32_t bk[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    bk[k] = fdiv(nd[k], c.div);
+    bk[k] = max(prio_bucket(nd[k], hv[k], c.div), c.b);
     if ((ok & (1u << k)) && nd[k] < old[k]) {
       if (bk[k] == c.b) curm |= 1u << k;
-      else farm |= 1u << k;  // bk > b: nd >= du >= bΔ
+      else farm |= 1u << k;  // bk > b
     }
   }
   // warp-aggregated appends: one ballot per item slot, one shared atomic per warp
@@ -968,7 +982,7 @@ __device__ __forceinline__ void async_feed(Ctx& c, Shared& s, const Ring& r, boo
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
+__global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs a) {
   constexpr bool FUSED = KIND != KIND_UNFUSED;
   constexpr bool ASYNC = KIND == KIND_FUSED_ASYNC;
   // bsp: bins [2][kBinCap] uint2, high-degree list [kBigCap], its prefix [kBigCap], far staging
@@ -1029,6 +1043,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
     c.s = &s;
     c.pre_read = a.pre_read != 0;
     c.hub_min = a.hub_min;
+    c.h = a.h;
 
     c.hubcap = a.hubcap;
     c.T = T;
@@ -1182,7 +1197,7 @@ __global__ void __launch_bounds__(kBlock, 1) sssp_persistent(KArgs a) {
 #pragma unroll
           for (int x = 0; x < kXtr; ++x) {
             if (v[x] < 0) continue;
-            const uint32_t bk = fdiv(d[x], c.div);
+            const uint32_t bk = prio_bucket(d[x], c.h ? __ldg(c.h + v[x]) : 0u, c.div);
             if (bk <= b) {
               atomicAnd(&ws.farbits[v[x] >> 5], ~(1u << (v[x] & 31)));
               if (bk == b) { ++nlive; push_cur<FUSED>(c, v[x], d[x]); }  // else: stale (settled)

@@ -27,7 +27,8 @@ STATUS = {0: "GI_OK", 1: "GI_ERR_INVALID_ARGUMENT", 2: "GI_ERR_OUT_OF_RANGE", 3:
           4: "GI_ERR_OUT_OF_MEMORY", 5: "GI_ERR_CUDA", 6: "GI_ERR_OVERFLOW", 7: "GI_ERR_UNSUPPORTED"}
 EXPORTS = ["gi_graph_create", "gi_graph_destroy", "gi_graph_info", "gi_sssp_delta", "gi_sssp_batch",
            "gi_options_default", "gi_sssp_delta_ex", "gi_sssp_batch_ex", "gi_last_error",
-           "gi_status_string", "gi_version", "gi_ppsp_delta", "gi_ppsp_delta_ex"]
+           "gi_status_string", "gi_version", "gi_ppsp_delta", "gi_ppsp_delta_ex", "gi_astar_delta",
+           "gi_astar_delta_ex"]
 
 
 class GiError(RuntimeError):
@@ -75,12 +76,15 @@ _lib.gi_sssp_delta_ex.argtypes = [_vp, _i32, _u32, ctypes.POINTER(gi_options), _
 _lib.gi_sssp_batch_ex.argtypes = [_vp, _vp, _i32, _u32, ctypes.POINTER(gi_options), _vp, ctypes.POINTER(gi_stats)]
 _lib.gi_ppsp_delta.argtypes = [_vp, _i32, _i32, _u32, _vp]
 _lib.gi_ppsp_delta_ex.argtypes = [_vp, _i32, _i32, _u32, ctypes.POINTER(gi_options), _vp, ctypes.POINTER(gi_stats)]
+_lib.gi_astar_delta.argtypes = [_vp, _i32, _i32, _u32, _vp, _vp]
+_lib.gi_astar_delta_ex.argtypes = [_vp, _i32, _i32, _u32, _vp, ctypes.POINTER(gi_options), _vp,
+                                   ctypes.POINTER(gi_stats)]
 _lib.gi_last_error.restype = ctypes.c_char_p
 _lib.gi_status_string.argtypes = [ctypes.c_int]
 _lib.gi_status_string.restype = ctypes.c_char_p
 _lib.gi_version.restype = _i32
 for _f in ("gi_graph_create", "gi_graph_info", "gi_sssp_delta", "gi_sssp_batch", "gi_sssp_delta_ex",
-           "gi_sssp_batch_ex", "gi_ppsp_delta", "gi_ppsp_delta_ex"):
+           "gi_sssp_batch_ex", "gi_ppsp_delta", "gi_ppsp_delta_ex", "gi_astar_delta", "gi_astar_delta_ex"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 
@@ -226,6 +230,25 @@ def ppsp(g: Graph, src: int, dst: int, delta: int, **opts):
     Python int, UINT32_MAX if unreachable; stats dict)."""
     out = np.zeros(1, np.uint32)
     st = gi_ppsp_delta(g, src, dst, delta, out, make_options(**opts) if opts else None)
+    return int(out[0]), st.to_dict()
+
+
+def gi_astar_delta(g: Graph, src: int, dst: int, delta: int, h, dist_st, options: gi_options | None = None,
+                   want_stats: bool = True):
+    """C-ABI gi_astar_delta_ex. h: uint32 (or int32 bits) [n] array/tensor, host or device."""
+    st = gi_stats() if want_stats else None
+    _check(_lib.gi_astar_delta_ex(g.handle, int(src), int(dst), int(delta), _ptr(h),
+                                  ctypes.byref(options) if options else None, _ptr(dist_st),
+                                  ctypes.byref(st) if st is not None else None))
+    return st
+
+
+def astar(g: Graph, src: int, dst: int, delta: int, h, **opts):
+    """A* (Δ-stepping on the priority dist + h, PPSP stop). Returns (distance, stats dict)."""
+    if isinstance(h, np.ndarray) and h.dtype != np.uint32:
+        h = h.astype(np.uint32)
+    out = np.zeros(1, np.uint32)
+    st = gi_astar_delta(g, src, dst, delta, h, out, make_options(**opts) if opts else None)
     return int(out[0]), st.to_dict()
 
 

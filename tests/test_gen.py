@@ -127,3 +127,21 @@ def test_bin_cache_roundtrip(tmp_path):
     gen.save_bin(g, p)
     h = gen.load_bin(p)
     assert np.array_equal(g.offsets, h.offsets) and np.array_equal(g.cols, h.cols) and np.array_equal(g.w, h.w)
+
+
+def test_grid_heuristic_admissible_and_consistent():
+    """A* input: w_min x Chebyshev distance on the road-like grid recipe
+    (deletions + diagonals) never exceeds the true remaining distance (admissible, checked
+    against the Dijkstra oracle from the target on the symmetric graph) and drops by at most
+    w(u,v) along every edge (consistent)."""
+    import oracle
+    rows, cols = 48, 40
+    g = gen.grid(rows, cols, 3, 50, 9, p_del=0.05, p_diag=0.2)
+    t = 17 * cols + 23
+    h = gen.grid_heuristic(rows, cols, t, 3).astype(np.int64)
+    assert h[t] == 0
+    d, rc = oracle.dijkstra(g, t)
+    reach = d != 0xFFFFFFFF
+    assert np.all(h[reach] <= d[reach].astype(np.int64))
+    src = np.repeat(np.arange(g.n), np.diff(g.offsets))
+    assert np.all(h[src] <= g.w.astype(np.int64) + h[g.cols])

@@ -337,3 +337,60 @@ def test_ppsp_overflow_only_for_the_target(gi):
     assert gi.ppsp(G, 0, 1, 1)[0] == 2**32 - 2
     with pytest.raises(gi.OverflowDistance):
         gi.ppsp(G, 0, 2, 1)
+
+
+def test_astar_matches_oracle(gi, config_graph):
+    """A* (PAPER.md:979-982): priority dist + h, PPSP stop. With an
+    admissible h (consistent: w_min x Chebyshev; inconsistent: random fractions of the true
+    remaining distance; perfect: the true remaining distance) the result equals the Dijkstra
+    oracle's dist[t]; h = 0 reproduces PPSP; an inadmissible h (x10) never
+    returns less than the true distance (documents the non-guarantee)."""
+    rng = np.random.default_rng(41)
+    rows, cols = 256, 256
+    g = config_graph(1)
+    G = gi.Graph.from_csr(g)
+    wmin = int(g.w.min())
+    for _ in range(12):
+        s, t = (int(x) for x in rng.integers(0, g.n, 2))
+        ref, _ = oracle.dijkstra(g, s)
+        to_t, _ = oracle.dijkstra(g, t)  # symmetric graph: δ(v, t) = δ(t, v)
+        hc = gen.grid_heuristic(rows, cols, t, wmin)
+        hr = (to_t.astype(np.float64) * rng.random(g.n)).astype(np.uint32)
+        for delta, o in ((1000, dict()), (250, dict(fusion=False)), (64, dict(threshold=4))):
+            for h in (hc, hr, to_t):
+                d, st = gi.astar(G, s, t, delta, h, **o)
+                assert d == int(ref[t]), (s, t, delta, o)
+            d0, st0 = gi.astar(G, s, t, delta, np.zeros(g.n, np.uint32), **o)
+            dp, stp = gi.ppsp(G, s, t, delta, **o)
+            assert d0 == dp == int(ref[t]) and st0["buckets"] == stp["buckets"]
+            d10, _ = gi.astar(G, s, t, delta, np.minimum(to_t.astype(np.uint64) * 10, 2**32 - 2).astype(np.uint32))
+            assert d10 >= int(ref[t])
+    # road-like recipe with diagonals, device-resident h, and the async drain rejected
+    import torch
+    h = gen.grid_heuristic(rows, cols, 5, wmin)
+    hd = torch.from_numpy(h.view(np.int32)).cuda()
+    out = torch.zeros(1, dtype=torch.int32, device="cuda")
+    gi.gi_astar_delta(G, 60000, 5, 1000, hd, out)
+    assert int(out.item()) == int(oracle.dijkstra(g, 60000)[0][5])
+    with pytest.raises(gi.GiError) as e:
+        gi.astar(G, 0, 5, 1000, h, drain="async")
+    assert e.value.status == 7
+
+
+def test_astar_random_symmetric_graphs(gi):
+    rng = np.random.default_rng(43)
+    for trial in range(25):
+        n = int(rng.integers(2, 500))
+        und = [(int(rng.integers(0, n)), int(rng.integers(0, n))) for _ in range(int(rng.integers(0, 4 * n)))]
+        edges = []
+        for u, v in und:
+            w = int(rng.integers(0, 30))
+            edges += [(u, v, w), (v, u, w)]
+        g = gen.from_edges(n, edges)
+        G = gi.Graph.from_csr(g)
+        s, t = int(rng.integers(0, n)), int(rng.integers(0, n))
+        ref, _ = oracle.dijkstra(g, s)
+        to_t, _ = oracle.dijkstra(g, t)
+        h = np.where(to_t == 0xFFFFFFFF, 0, (to_t * rng.random(n)).astype(np.uint32)).astype(np.uint32)
+        for delta in (1, 4, 1 << 20):
+            assert gi.astar(G, s, t, delta, h)[0] == int(ref[t]), (trial, s, t, delta)
