@@ -168,6 +168,55 @@ def cpu_baseline(g, src, budget_s=12.0):
                       f"(oracle/oracle.c), mean {t:.3f} s each"}
 
 
+def run_app(args, g, G, delta, opts, rank, world):
+    """PPSP / A* on the config's source and a seeded target; checked
+    against the Dijkstra oracle's dist[target] (rank 0) and timed with CUDA events."""
+    import torch
+    import oracle
+    from paper_1911_07260_b200 import gi
+    cfg = args.config
+    src = gen.config_source(cfg, g)
+    tgt = int(gen.sources(g.n, 1, seed=7)[0])
+    out = torch.zeros(1, dtype=torch.int32, device="cuda")
+    h = None
+    if args.app == "astar":
+        if g.meta.get("kind") != "grid":
+            raise SystemExit("--app astar needs a grid config (1, 2): the heuristic uses grid coordinates")
+        hh = gen.grid_heuristic(g.meta["rows"], g.meta["cols"], tgt, int(g.w.min()))
+        h = torch.from_numpy(hh.view(np.int32)).cuda()
+
+    def step():
+        o = gi.make_options(**opts)
+        if h is None:
+            return gi.gi_ppsp_delta(G, src, tgt, delta, out, o)
+        return gi.gi_astar_delta(G, src, tgt, delta, h, out, o)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    stream = opts["stream"]
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    sts = [step() for _ in range(args.steps)]
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if rank != 0:
+        return 0
+    got = int(out.item()) & 0xFFFFFFFF
+    ref = int(oracle.dijkstra(g, src)[0][tgt])
+    st = sts[-1]
+    line = {"metric": f"{args.app} time per query (and m / time)", "value": g.m / (ms * 1e-3) / 1e9, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": WORKLOAD[cfg], "app": args.app, "source": src, "target": tgt, "delta": delta},
+            "result": got, "oracle": ref, "parity": got == ref,
+            "counters": {k: getattr(st, k) for k in ("buckets", "rounds", "grid_syncs", "vertices_processed",
+                                                      "edges_relaxed", "critical_subrounds", "kernel_kind")}}
+    print(json.dumps(line), flush=True)
+    return 0 if got == ref else 1
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -185,6 +234,8 @@ def main():
     ap.add_argument("--drain", default="auto", choices=["auto", "bsp", "async"],
                     help="fused drain: per-sub-round CTA barriers (default) or the barrier-free async ring")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--app", default="sssp", choices=["sssp", "ppsp", "astar"],
+                    help="next rows (SURVEY §8(f)): point-to-point Δ-stepping or A* to a seeded target (grids)")
     ap.add_argument("--no-compare", action="store_true", help="skip the fusion on/off counter comparison")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -225,6 +276,8 @@ def main():
             return st
         units_per_step = len(srcs_all) * g.m  # whole job: all 64 sources
         launches_per_step = 1
+    elif args.app != "sssp":
+        return run_app(args, g, G, delta, opts, rank, world)
     else:
         src = gen.config_source(cfg, g)
         out = torch.empty(g.n, dtype=torch.int32, device="cuda")
