@@ -21,6 +21,10 @@ Functions and what they follow:
   claim on the hand example Ex5.
 * ``frontier_bellman_ford`` — pure-Python frontier Bellman-Ford (PAPER.md:157-161,
   :1555-1562) counting updates, for the same pin.
+* ``kcore`` — coreness by the textbook serial min-degree peel (oracle.c; Matula & Beck,
+  Batagelj & Zaversnik), the definition of; pinned by
+  ``kcore_bruteforce`` (the k-core definition by repeated deletion, every k, tiny graphs)
+  and closed forms (clique, cycle, star, path, full grid).
 """
 from __future__ import annotations
 
@@ -59,7 +63,9 @@ def _L():
         _lib.oracle_bellman_ford.argtypes = [i64, vp, vp, vp, ctypes.c_int32, vp]
         _lib.oracle_transpose.argtypes = [i64, i64, vp, vp, vp, vp, vp, vp]
         _lib.oracle_certificate.argtypes = [i64, vp, vp, vp, vp, vp, vp, ctypes.c_int32, vp, vp]
-        for f in ("oracle_dijkstra", "oracle_bellman_ford", "oracle_transpose", "oracle_certificate"):
+        _lib.oracle_kcore.argtypes = [i64, vp, vp, vp]
+        for f in ("oracle_dijkstra", "oracle_bellman_ford", "oracle_transpose", "oracle_certificate",
+                  "oracle_kcore"):
             getattr(_lib, f).restype = ctypes.c_int
     return _lib
 
@@ -233,3 +239,35 @@ def frontier_bellman_ford(g, src: int):
                     nxt.add(d)
         frontier = sorted(nxt)
     return dict(dist=np.array(dist, dtype=np.uint64), rounds=rounds, updates=updates)
+
+
+def kcore(g):
+    """Coreness of every vertex (uint32[n]) by the serial min-degree peel (oracle.c)."""
+    off, col, _ = _arrs(g)
+    core = np.zeros(g.n, np.uint32)
+    rc = _L().oracle_kcore(g.n, off.ctypes.data, col.ctypes.data, core.ctypes.data)
+    if rc != 0:
+        raise ValueError(f"oracle_kcore rc={rc}")
+    return core
+
+
+def kcore_bruteforce(g):
+    """The definition, for tiny graphs: for each k, delete vertices whose degree inside the
+    remaining set is < k until none is left to delete (the k-core); coreness[v] = the
+    largest k whose k-core contains v. Degrees count CSR entries."""
+    off = np.asarray(g.offsets)
+    col = np.asarray(g.cols)
+    n = g.n
+    core = np.zeros(n, np.uint32)
+    maxdeg = int(np.diff(off).max(initial=0))
+    for k in range(1, maxdeg + 1):
+        alive = np.ones(n, bool)
+        changed = True
+        while changed:
+            changed = False
+            for v in range(n):
+                if alive[v] and sum(1 for e in range(off[v], off[v + 1]) if alive[col[e]]) < k:
+                    alive[v] = False
+                    changed = True
+        core[alive] = k
+    return core

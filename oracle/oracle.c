@@ -203,3 +203,56 @@ int oracle_certificate(int64_t n, const int64_t* off, const int32_t* col, const 
   }
   return 0;
 }
+
+/* ---- k-core ----------------------------------------------------
+ * Coreness by the textbook serial min-degree peel (Matula & Beck 1983, in the O(n+m)
+ * bin-sort form of Batagelj & Zaversnik 2003) — NOT the paper's bucketed priority queue.
+ * The k-core of G is the maximal subgraph whose vertices all have induced degree >= k;
+ * coreness[v] = max k with v in the k-core ("computes the maximum k-core
+ * that u is contained in ... using a peeling procedure"). Degrees count stored CSR
+ * entries (a parallel edge counts twice, a self-loop once), the convention the GPU path
+ * also uses. Peel: repeatedly remove a vertex of minimum current degree d; its coreness is
+ * d (kept monotone: never below the previous removal's value); each remaining neighbour's
+ * current degree drops by one per connecting entry.
+ * Returns 0, or ORACLE_BAD_INPUT / ORACLE_NOMEM. */
+int oracle_kcore(int64_t n, const int64_t* off, const int32_t* col, uint32_t* core) {
+  if (n < 1) return ORACLE_BAD_INPUT;
+  int64_t md = 0;
+  int64_t* deg = (int64_t*)malloc(sizeof(int64_t) * n);
+  int64_t* pos = (int64_t*)malloc(sizeof(int64_t) * n);
+  int32_t* vert = (int32_t*)malloc(sizeof(int32_t) * n);
+  char* gone = (char*)calloc((size_t)n, 1);
+  if (!deg || !pos || !vert || !gone) { free(deg); free(pos); free(vert); free(gone); return ORACLE_NOMEM; }
+  for (int64_t v = 0; v < n; ++v) {
+    deg[v] = off[v + 1] - off[v];
+    if (deg[v] > md) md = deg[v];
+  }
+  int64_t* bin = (int64_t*)calloc((size_t)(md + 2), sizeof(int64_t));
+  if (!bin) { free(deg); free(pos); free(vert); free(gone); return ORACLE_NOMEM; }
+  /* counting sort of the vertices by degree: bin[d] = first position of degree d */
+  for (int64_t v = 0; v < n; ++v) bin[deg[v]]++;
+  int64_t start = 0;
+  for (int64_t d = 0; d <= md; ++d) { int64_t c = bin[d]; bin[d] = start; start += c; }
+  for (int64_t v = 0; v < n; ++v) { pos[v] = bin[deg[v]]; vert[pos[v]] = (int32_t)v; bin[deg[v]]++; }
+  for (int64_t d = md; d >= 1; --d) bin[d] = bin[d - 1];
+  bin[0] = 0;
+  /* peel in order of current degree: vert[i] has the minimum current degree among
+     the vertices not yet removed */
+  for (int64_t i = 0; i < n; ++i) {
+    int32_t v = vert[i];
+    core[v] = (uint32_t)deg[v];
+    gone[v] = 1;
+    for (int64_t e = off[v]; e < off[v + 1]; ++e) {
+      int32_t u = col[e];
+      if (gone[u] || deg[u] <= deg[v]) continue;
+      /* move u to the front of its degree bin, then shrink its degree by one */
+      int64_t du = deg[u], pu = pos[u], pw = bin[du];
+      int32_t w = vert[pw];
+      if (u != w) { pos[u] = pw; vert[pu] = w; pos[w] = pu; vert[pw] = u; }
+      bin[du]++;
+      deg[u]--;
+    }
+  }
+  free(deg); free(pos); free(vert); free(gone); free(bin);
+  return ORACLE_OK;
+}

@@ -199,3 +199,47 @@ def test_dijkstra_many_threads():
     for i, a in enumerate(srcs):
         for j, b in enumerate(srcs):
             assert out[i][b] == out[j][a]
+
+
+# ---- k-core oracle pins ----
+
+def _sym(n, und):
+    edges = []
+    for u, v in und:
+        edges += [(u, v, 1), (v, u, 1)]
+    return gen.from_edges(n, edges)
+
+
+def test_kcore_closed_forms():
+    tri = _sym(3, [(0, 1), (1, 2), (0, 2)])
+    assert oracle.kcore(tri).tolist() == [2, 2, 2]
+    star = _sym(5, [(0, i) for i in range(1, 5)])
+    assert oracle.kcore(star).tolist() == [1] * 5
+    for n in (1, 2, 5, 9):
+        k = _sym(n, [(i, j) for i in range(n) for j in range(i + 1, n)])
+        assert oracle.kcore(k).tolist() == [n - 1] * n  # clique K_n
+    cyc = _sym(7, [(i, (i + 1) % 7) for i in range(7)])
+    assert oracle.kcore(cyc).tolist() == [2] * 7
+    path = _sym(6, [(i, i + 1) for i in range(5)])
+    assert oracle.kcore(path).tolist() == [1] * 6
+    grid = gen.grid(20, 30, 1, 2, 0)  # full 4-neighbour grid: its 2-core is everything, no 3-core
+    assert set(oracle.kcore(grid).tolist()) == {2}
+    iso = gen.from_edges(4, [])
+    assert oracle.kcore(iso).tolist() == [0] * 4
+    # two cliques K5 and K3 joined by a bridge: 4 on the K5, 2 on the K3
+    und = [(i, j) for i in range(5) for j in range(i + 1, 5)] + [(5, 6), (6, 7), (5, 7), (4, 5)]
+    assert oracle.kcore(_sym(8, und)).tolist() == [4] * 5 + [2] * 3
+
+
+def test_kcore_matches_definition_bruteforce():
+    rng = np.random.default_rng(5)
+    for t in range(60):
+        n = int(rng.integers(1, 30))
+        und = [(int(rng.integers(0, n)), int(rng.integers(0, n))) for _ in range(int(rng.integers(0, 4 * n)))]
+        g = _sym(n, und)  # includes parallel edges and self-loops (a self-loop stores 2 entries)
+        assert np.array_equal(oracle.kcore(g), oracle.kcore_bruteforce(g)), t
+    g = gen.uniform_random(64, 512, 1, 2, 7)  # SPEC.md:370 corpus shape, symmetrised
+    src = np.repeat(np.arange(g.n), np.diff(g.offsets))
+    und = list(zip(src.tolist(), g.cols.tolist()))
+    s = _sym(64, und)
+    assert np.array_equal(oracle.kcore(s), oracle.kcore_bruteforce(s))
