@@ -168,6 +168,46 @@ def cpu_baseline(g, src, budget_s=12.0):
                       f"(oracle/oracle.c), mean {t:.3f} s each"}
 
 
+def run_kcore(args, g, G, opts, rank, world):
+    """k-core on the config's symmetric graph: coreness of every vertex,
+    checked element by element against the serial peeling oracle; the oracle is timed on
+    the host beside it (one full peel)."""
+    import torch
+    import oracle
+    from paper_1911_07260_b200 import gi
+    out = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    o = gi.make_options(**{k: v for k, v in opts.items() if k in ("max_ctas", "stream")})
+    for _ in range(max(args.warmup, 3)):
+        gi.gi_kcore(G, out, o)
+    stream = opts["stream"]
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    sts = [gi.gi_kcore(G, out, o) for _ in range(args.steps)]
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if rank != 0:
+        return 0
+    got = gi.as_uint32(out)
+    t0 = time.perf_counter()
+    ref = oracle.kcore(g)
+    t_or = time.perf_counter() - t0
+    st = sts[-1]
+    line = {"metric": "k-core time per full peel (and m / time)", "value": g.m / (ms * 1e-3) / 1e9, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": WORKLOAD[args.config], "app": "kcore", "n": g.n, "m": g.m},
+            "parity": bool(np.array_equal(got, ref)), "max_core": int(ref.max()),
+            "cpu_baseline": {"value": g.m / t_or / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"one serial peel (oracle/oracle.c), {t_or:.3f} s"},
+            "counters": {k: getattr(st, k) for k in ("buckets", "rounds", "grid_syncs", "vertices_processed",
+                                                      "edges_relaxed", "empty_extractions", "kernel_kind")}}
+    print(json.dumps(line), flush=True)
+    return 0 if line["parity"] else 1
+
+
 def run_app(args, g, G, delta, opts, rank, world):
     """PPSP / A* on the config's source and a seeded target; checked
     against the Dijkstra oracle's dist[target] (rank 0) and timed with CUDA events."""
@@ -175,6 +215,8 @@ def run_app(args, g, G, delta, opts, rank, world):
     import oracle
     from paper_1911_07260_b200 import gi
     cfg = args.config
+    if args.app == "kcore":
+        return run_kcore(args, g, G, opts, rank, world)
     src = gen.config_source(cfg, g)
     tgt = int(gen.sources(g.n, 1, seed=7)[0])
     out = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -234,8 +276,9 @@ def main():
     ap.add_argument("--drain", default="auto", choices=["auto", "bsp", "async"],
                     help="fused drain: per-sub-round CTA barriers (default) or the barrier-free async ring")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--app", default="sssp", choices=["sssp", "ppsp", "astar"],
-                    help="next rows (SURVEY §8(f)): point-to-point Δ-stepping or A* to a seeded target (grids)")
+    ap.add_argument("--app", default="sssp", choices=["sssp", "ppsp", "astar", "kcore"],
+                    help="next rows (SURVEY §8(f)): point-to-point Δ-stepping, A* to a seeded target (grids), "
+                         "k-core (coreness of every vertex)")
     ap.add_argument("--no-compare", action="store_true", help="skip the fusion on/off counter comparison")
     args = ap.parse_args()
     if args.impl == "reference":

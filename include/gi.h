@@ -127,7 +127,7 @@ typedef struct {
   int32_t threads_per_cta;
   int32_t groups;              /* concurrent query groups (1 for single source) */
   int32_t kernel_kind;         /* persistent kernel that ran: 0 unfused, 1 fused + bsp drain,
-                                  2 fused + async drain */
+                                  2 fused + async drain, 3 k-core */
 } gi_stats;
 
 /* Fill *opt with defaults (fusion on, library-default threshold, all CTAs). */
@@ -172,6 +172,20 @@ gi_status gi_astar_delta(const gi_graph* g, int32_t src, int32_t dst, uint32_t d
                          uint32_t* dist_st);
 gi_status gi_astar_delta_ex(const gi_graph* g, int32_t src, int32_t dst, uint32_t delta, const uint32_t* h,
                             const gi_options* opt, uint32_t* dist_st, gi_stats* stats);
+
+/* k-core: coreness of every vertex, "the maximum k-core that u is
+ * contained in ... using a peeling procedure", by the paper's bucketed
+ * peel with lazy bucket updates and the constant-sum reduction (Fig. 10, PAPER.md:1591-1618;
+ * PAPER.md:802-837): priorities start at the degrees, the minimum bucket k is finished with
+ * coreness k, neighbours' priorities drop by their count of finished neighbours, floored
+ * at k. No priority coarsening.
+ *   core_out  uint32[n], host or device (on the graph's device): coreness[v].
+ * The graph should be symmetric (undirected, both directions stored); degrees count CSR
+ * entries (a parallel edge counts twice). Synchronous. stats: buckets = distinct coreness
+ * values peeled, rounds = frontier passes, grid_syncs, vertices_processed (= n),
+ * edges_relaxed, gpu_ms; kernel_kind = 3. */
+gi_status gi_kcore(const gi_graph* g, uint32_t* core_out);
+gi_status gi_kcore_ex(const gi_graph* g, const gi_options* opt, uint32_t* core_out, gi_stats* stats);
 
 /* Thread-local description of the last non-OK status returned on this thread. */
 const char* gi_last_error(void);

@@ -68,6 +68,9 @@ struct Workspace {
   size_t stagecap = 0;
   uint32_t* d_h = nullptr;      // staging for a host A* heuristic
   size_t hcap = 0;
+  uint32_t* kc_prio = nullptr;  // k-core: priorities [n]
+  KcCtl* kc_ctl = nullptr;
+  KcStats* kc_stats = nullptr;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
@@ -78,6 +81,9 @@ struct Workspace {
     if (d_srcs) cudaFree(d_srcs);
     if (d_stage) cudaFree(d_stage);
     if (d_h) cudaFree(d_h);
+    if (kc_prio) cudaFree(kc_prio);
+    if (kc_ctl) cudaFree(kc_ctl);
+    if (kc_stats) cudaFree(kc_stats);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
@@ -95,6 +101,7 @@ struct gi_graph {
   uint32_t max_deg = 0;
   int sm_count = 0;
   int bps[3] = {0, 0, 0};  // co-resident CTAs per SM, by KernelKind
+  int bps_kcore = 0;
   std::mutex mu;
   std::vector<std::unique_ptr<Workspace>> pool;
 };
@@ -441,6 +448,8 @@ gi_status gi_graph_create(int64_t n, int64_t m, const int64_t* row_offsets, cons
   g->n = n;
   g->m = m;
   g->sm_count = prop.multiProcessorCount;
+  GI_CUDA(kcore_occupancy(&g->bps_kcore), "occupancy");
+  if (g->bps_kcore < 1) return fail(GI_ERR_CUDA, "k-core kernel cannot be resident");
   for (int k = 0; k < 3; ++k) {
     GI_CUDA(query_occupancy(k, &g->bps[k]), "occupancy");
     if (g->bps[k] < 1) return fail(GI_ERR_CUDA, "persistent kernel variant %d cannot be resident", k);
@@ -573,5 +582,104 @@ gi_status gi_astar_delta(const gi_graph* g, int32_t src, int32_t dst, uint32_t d
                          uint32_t* dist_st) {
   return gi_astar_delta_ex(g, src, dst, delta, h, nullptr, dist_st, nullptr);
 }
+
+gi_status gi_kcore_ex(const gi_graph* cg_, const gi_options* opt_in, uint32_t* core_out, gi_stats* stats) {
+  gi_graph* g = const_cast<gi_graph*>(cg_);
+  if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "graph is NULL");
+  if (!core_out) return fail(GI_ERR_INVALID_ARGUMENT, "core_out is NULL");
+  gi_options opt;
+  gi_options_default(&opt);
+  if (opt_in) {
+    if (opt_in->struct_size != sizeof(gi_options)) return fail(GI_ERR_INVALID_ARGUMENT, "gi_options.struct_size mismatch");
+    opt = *opt_in;
+  }
+  DeviceGuard dg(g->device);
+  bool wrongdev = false;
+  const bool dev_out = is_device_ptr(core_out, g->device, &wrongdev);
+  if (wrongdev) return fail(GI_ERR_INVALID_ARGUMENT, "core_out on another device");
+  Workspace* w = ws_acquire(g);
+  gi_status s = ws_prepare(g, w, 1, 1);
+  if (s) { ws_release(g, w, false); return s; }
+  cudaStream_t st = opt.cuda_stream ? (cudaStream_t)opt.cuda_stream : w->stream;
+  if (opt.cuda_stream) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventRecord(e, w->stream);
+    cudaStreamWaitEvent(st, e, 0);
+    cudaEventDestroy(e);
+  }
+  auto bail = [&](cudaError_t e, const char* what) {
+    cudaStreamSynchronize(st);
+    ws_release(g, w, false);
+    return cuda_fail(e, what);
+  };
+  cudaError_t e;
+  const size_t n = (size_t)g->n;
+  if (!w->kc_prio) {
+    if ((e = cudaMalloc(&w->kc_prio, n * 4))) return bail(e, "alloc k-core priorities");
+    if ((e = cudaMalloc(&w->kc_ctl, sizeof(KcCtl)))) return bail(e, "alloc k-core control");
+    if ((e = cudaMalloc(&w->kc_stats, sizeof(KcStats)))) return bail(e, "alloc k-core stats");
+  }
+  uint32_t* d_core = core_out;
+  if (!dev_out) {
+    if (w->stagecap < n) {
+      if (w->d_stage) cudaFree(w->d_stage);
+      w->d_stage = nullptr;
+      w->stagecap = 0;
+      if ((e = cudaMalloc(&w->d_stage, n * 4))) return bail(e, "alloc core stage");
+      w->stagecap = n;
+    }
+    d_core = w->d_stage;
+  }
+  KcCtl hc;
+  memset(&hc, 0, sizeof(hc));
+  hc.pcount[0] = (uint32_t)n;
+  for (int k = 0; k < 3; ++k) hc.kmin[k] = 0xFFFFFFFFu;
+  if ((e = cudaMemcpyAsync(w->kc_ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice, st))) return bail(e, "init k-core control");
+  if ((e = cudaMemsetAsync(w->kc_stats, 0, sizeof(KcStats), st))) return bail(e, "memset k-core stats");
+  KcArgs a;
+  a.off = g->d_off;
+  a.edges = g->d_edges;
+  a.n = g->n;
+  a.prio = w->kc_prio;
+  a.core = d_core;
+  a.pile[0] = w->h_groups[0].far[0];
+  a.pile[1] = w->h_groups[0].far[1];
+  a.q[0] = w->h_groups[0].q[0];
+  a.q[1] = w->h_groups[0].q[1];
+  a.ctl = w->kc_ctl;
+  a.stats = w->kc_stats;
+  int grid = g->sm_count * g->bps_kcore;
+  if (opt.max_ctas > 0 && opt.max_ctas < grid) grid = opt.max_ctas;
+  if ((e = cudaEventRecord(w->ev0, st))) return bail(e, "event");
+  if ((e = launch_kcore(a, grid, st))) return bail(e, "launch kcore_persistent");
+  if ((e = cudaEventRecord(w->ev1, st))) return bail(e, "event");
+  KcStats hs;
+  if ((e = cudaMemcpyAsync(&hs, w->kc_stats, sizeof(hs), cudaMemcpyDeviceToHost, st))) return bail(e, "copy stats");
+  if (!dev_out && (e = cudaMemcpyAsync(core_out, d_core, n * 4, cudaMemcpyDeviceToHost, st)))
+    return bail(e, "copy coreness");
+  if ((e = cudaStreamSynchronize(st))) return bail(e, "kcore kernel");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, w->ev0, w->ev1);
+  ws_release(g, w, true);
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    stats->buckets = hs.buckets;
+    stats->rounds = hs.rounds;
+    stats->grid_syncs = hs.phases;
+    stats->kernel_launches = 1;
+    stats->vertices_processed = hs.vertices;
+    stats->edges_relaxed = hs.edges;
+    stats->empty_extractions = hs.empty;
+    stats->gpu_ms = ms;
+    stats->ctas = grid;
+    stats->threads_per_cta = 512;
+    stats->groups = 1;
+    stats->kernel_kind = 3;
+  }
+  return GI_OK;
+}
+
+gi_status gi_kcore(const gi_graph* g, uint32_t* core_out) { return gi_kcore_ex(g, nullptr, core_out, nullptr); }
 
 }  // extern "C"

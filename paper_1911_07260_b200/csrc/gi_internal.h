@@ -117,6 +117,34 @@ struct KArgs {
   const uint32_t* h;    // A*: per-vertex heuristic (priority = dist + h); nullptr = 0 (SSSP / PPSP)
 };
 
+// k-core (gi_kcore.cu): control block, statistics and arguments.
+struct alignas(128) KcCtl {
+  uint32_t qcount[3];   // frontier sizes, by phase mod 3
+  uint32_t pcount[3];   // pile (unfinished vertices) sizes, by extraction mod 3
+  uint32_t kmin[3];     // min priority of the unfinished vertices, by extraction mod 3
+  uint32_t qclaim[3];   // ROUND: next unclaimed frontier position, by phase mod 3
+  uint32_t xfin[3];     // vertices finished by an extraction, by extraction mod 3
+  uint32_t pad0[17];
+  uint32_t bar;         // group barrier word, own 128 B line
+  uint32_t pad1[31];
+};
+
+struct KcStats {
+  unsigned long long buckets, rounds, phases, vertices, edges, empty;
+};
+
+struct KcArgs {
+  const int64_t* off;   // [n+1] CSR offsets (device)
+  const uint2* edges;   // [m] {col, w}; only col is read
+  int64_t n;
+  uint32_t* prio;       // [n] workspace: current priority (starts at the degree)
+  uint32_t* core;       // [n] result: coreness
+  int32_t* pile[2];     // [n] unfinished vertices, double-buffered across extractions
+  int32_t* q[2];        // [n] frontier, double-buffered across phases
+  KcCtl* ctl;
+  KcStats* stats;
+};
+
 // Host-side launchers (gi_kernels.cu).
 cudaError_t launch_sssp(const KArgs& a, int kind, int grid, cudaStream_t st);
 cudaError_t query_occupancy(int kind, int* blocks_per_sm);
@@ -128,5 +156,7 @@ cudaError_t launch_max_degree(const int64_t* off, int64_t n, uint32_t* max_deg, 
 cudaError_t launch_validate_offsets(const int64_t* off, int64_t n, int64_t m, uint32_t* bad_flag,
                                     cudaStream_t st);
 int smem_bytes(int kind);
+cudaError_t launch_kcore(const KcArgs& a, int grid, cudaStream_t st);  // gi_kcore.cu
+cudaError_t kcore_occupancy(int* blocks_per_sm);
 
 }  // namespace gi

@@ -35,6 +35,7 @@
 // the CTA ring as (vertex, distance) pairs (eager) and the
 // vertex's slot is prefetched into L2 for the next sub-round.
 #include "gi_internal.h"
+#include "gi_device.cuh"
 
 #include <cooperative_groups.h>
 
@@ -103,17 +104,12 @@ __device__ unsigned long long g_item[16];
 #define TRACE_FLUSH() do {} while (0)
 #endif
 
-__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
+using dev::fence_acq_rel;
+using dev::ld_relaxed;
 
 __device__ __forceinline__ void red_min(uint32_t* p, uint32_t v) {
   asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-
-__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // dist[] is written by atomics inside this kernel: read it coherently from L2,
 // never through the non-coherent/L1 path (SURVEY §7 hard part 1).
@@ -145,25 +141,7 @@ __device__ __forceinline__ uint32_t prio_bucket(uint32_t d, uint32_t hv, const F
   return fdiv((p < d || p == kInf) ? kInf - 1u : p, f);
 }
 
-// Barrier over the G CTAs of one group (all co-resident: cooperative launch).
-// One word: arrivals in the low 16 bits, generation in the high 16; the last
-// arriver resets the count and bumps the generation with a single atomic.
-__device__ __forceinline__ void group_barrier(Ctl* ctl, uint32_t G) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    fence_acq_rel();  // publish this CTA's writes (cumulative over the bar.sync above)
-    const uint32_t old = atomicAdd(&ctl->bar, 1u);
-    if ((old & 0xFFFFu) == G - 1) {
-      atomicAdd(&ctl->bar, 0x10000u - G);
-    } else {
-      const uint32_t gen = old >> 16;
-      while ((ld_relaxed(&ctl->bar) >> 16) == gen) {
-      }
-    }
-    fence_acq_rel();
-  }
-  __syncthreads();
-}
+__device__ __forceinline__ void group_barrier(Ctl* ctl, uint32_t G) { dev::group_barrier(&ctl->bar, G); }
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T x) {

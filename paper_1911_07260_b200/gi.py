@@ -28,7 +28,7 @@ STATUS = {0: "GI_OK", 1: "GI_ERR_INVALID_ARGUMENT", 2: "GI_ERR_OUT_OF_RANGE", 3:
 EXPORTS = ["gi_graph_create", "gi_graph_destroy", "gi_graph_info", "gi_sssp_delta", "gi_sssp_batch",
            "gi_options_default", "gi_sssp_delta_ex", "gi_sssp_batch_ex", "gi_last_error",
            "gi_status_string", "gi_version", "gi_ppsp_delta", "gi_ppsp_delta_ex", "gi_astar_delta",
-           "gi_astar_delta_ex"]
+           "gi_astar_delta_ex", "gi_kcore", "gi_kcore_ex"]
 
 
 class GiError(RuntimeError):
@@ -77,6 +77,8 @@ _lib.gi_sssp_batch_ex.argtypes = [_vp, _vp, _i32, _u32, ctypes.POINTER(gi_option
 _lib.gi_ppsp_delta.argtypes = [_vp, _i32, _i32, _u32, _vp]
 _lib.gi_ppsp_delta_ex.argtypes = [_vp, _i32, _i32, _u32, ctypes.POINTER(gi_options), _vp, ctypes.POINTER(gi_stats)]
 _lib.gi_astar_delta.argtypes = [_vp, _i32, _i32, _u32, _vp, _vp]
+_lib.gi_kcore.argtypes = [_vp, _vp]
+_lib.gi_kcore_ex.argtypes = [_vp, ctypes.POINTER(gi_options), _vp, ctypes.POINTER(gi_stats)]
 _lib.gi_astar_delta_ex.argtypes = [_vp, _i32, _i32, _u32, _vp, ctypes.POINTER(gi_options), _vp,
                                    ctypes.POINTER(gi_stats)]
 _lib.gi_last_error.restype = ctypes.c_char_p
@@ -84,7 +86,7 @@ _lib.gi_status_string.argtypes = [ctypes.c_int]
 _lib.gi_status_string.restype = ctypes.c_char_p
 _lib.gi_version.restype = _i32
 for _f in ("gi_graph_create", "gi_graph_info", "gi_sssp_delta", "gi_sssp_batch", "gi_sssp_delta_ex",
-           "gi_sssp_batch_ex", "gi_ppsp_delta", "gi_ppsp_delta_ex", "gi_astar_delta", "gi_astar_delta_ex"):
+           "gi_sssp_batch_ex", "gi_ppsp_delta", "gi_ppsp_delta_ex", "gi_astar_delta", "gi_astar_delta_ex", "gi_kcore", "gi_kcore_ex"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 
@@ -250,6 +252,24 @@ def astar(g: Graph, src: int, dst: int, delta: int, h, **opts):
     out = np.zeros(1, np.uint32)
     st = gi_astar_delta(g, src, dst, delta, h, out, make_options(**opts) if opts else None)
     return int(out[0]), st.to_dict()
+
+
+def gi_kcore(g: Graph, core_out, options: gi_options | None = None, want_stats: bool = True):
+    """C-ABI gi_kcore_ex. core_out: uint32/int32 [n], host or device."""
+    st = gi_stats() if want_stats else None
+    _check(_lib.gi_kcore_ex(g.handle, ctypes.byref(options) if options else None, _ptr(core_out),
+                            ctypes.byref(st) if st is not None else None))
+    return st
+
+
+def kcore(g: Graph, out=None, **opts):
+    """Coreness of every vertex (bucketed peel on the GPU). Returns (int32 tensor [n]
+    holding uint32 values, stats dict)."""
+    import torch
+    if out is None:
+        out = torch.empty(g.n, dtype=torch.int32, device=f"cuda:{g.device}")
+    st = gi_kcore(g, out, make_options(**opts) if opts else None)
+    return out, st.to_dict()
 
 
 def as_uint32(t) -> np.ndarray:

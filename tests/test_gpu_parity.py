@@ -394,3 +394,42 @@ def test_astar_random_symmetric_graphs(gi):
         h = np.where(to_t == 0xFFFFFFFF, 0, (to_t * rng.random(n)).astype(np.uint32)).astype(np.uint32)
         for delta in (1, 4, 1 << 20):
             assert gi.astar(G, s, t, delta, h)[0] == int(ref[t]), (trial, s, t, delta)
+
+
+def _sym_graph(n, und):
+    edges = []
+    for u, v in und:
+        edges += [(u, v, 1), (v, u, 1)]
+    return gen.from_edges(n, edges)
+
+
+def test_kcore_matches_oracle(gi, config_graph):
+    """k-core (Fig. 10): coreness of every vertex equals
+    the serial peeling oracle, element by element — closed forms, random symmetric
+    multigraphs (parallel edges, self-loops, isolated vertices), every CTA count, the full
+    grid of config 1 (all 2) and RMAT-22 (config 3: skewed degrees, hubs)."""
+    tri = gi.Graph.from_csr(_sym_graph(3, [(0, 1), (1, 2), (0, 2)]))
+    assert gi.as_uint32(gi.kcore(tri)[0]).tolist() == [2, 2, 2]
+    star = gi.Graph.from_csr(_sym_graph(5, [(0, i) for i in range(1, 5)]))
+    assert gi.as_uint32(gi.kcore(star)[0]).tolist() == [1] * 5
+    rng = np.random.default_rng(47)
+    for t in range(40):
+        n = int(rng.integers(1, 2000))
+        und = [(int(rng.integers(0, n)), int(rng.integers(0, n))) for _ in range(int(rng.integers(0, 6 * n)))]
+        g = _sym_graph(n, und)
+        G = gi.Graph.from_csr(g)
+        ref = oracle.kcore(g)
+        for o in (dict(), dict(max_ctas=1), dict(max_ctas=7)):
+            got, st = gi.kcore(G, **o)
+            assert np.array_equal(gi.as_uint32(got), ref), (t, o)
+            assert st["vertices_processed"] == n and st["buckets"] == len(set(ref.tolist()))
+    g1 = config_graph(1)
+    c1, _ = gi.kcore(gi.Graph.from_csr(g1))
+    assert set(gi.as_uint32(c1).tolist()) == {2}
+    host = np.zeros(g1.n, np.uint32)
+    gi.gi_kcore(gi.Graph.from_csr(g1), host)
+    assert set(host.tolist()) == {2}
+    g3 = config_graph(3)
+    c3, st3 = gi.kcore(gi.Graph.from_csr(g3))
+    assert np.array_equal(gi.as_uint32(c3), oracle.kcore(g3))
+    assert st3["edges_relaxed"] == g3.m  # every vertex is peeled once: each CSR entry is scanned once
