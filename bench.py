@@ -273,6 +273,8 @@ def main():
     ap.add_argument("--group-ctas", type=int, default=0)
     ap.add_argument("--hub-min", type=int, default=0)
     ap.add_argument("--pre-read", type=int, default=0, help="0 auto, 1 on, 2 off")
+    ap.add_argument("--cta-threads", type=int, default=0, choices=[0, 512, 1024],
+                    help="threads per persistent CTA (0 = auto: 1024 on skewed graphs)")
     ap.add_argument("--drain", default="auto", choices=["auto", "bsp", "async"],
                     help="fused drain: per-sub-round CTA barriers (default) or the barrier-free async ring")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -302,7 +304,7 @@ def main():
     stream = torch.cuda.current_stream()
     opts = dict(fusion=not args.no_fusion, threshold=args.threshold, max_ctas=args.max_ctas,
                 group_ctas=args.group_ctas, hub_min=args.hub_min, pre_read=args.pre_read, drain=args.drain,
-                stream=stream)
+                stream=stream, cta_threads=args.cta_threads)
 
     if cfg == 5:
         from paper_1911_07260_b200.dist import padded_shard

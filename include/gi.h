@@ -106,6 +106,9 @@ typedef struct {
                                 1 = on, 2 = off */
   void* cuda_stream;         /* cudaStream_t to run on (NULL = library stream); calls still
                                 synchronise that stream before returning */
+  int32_t cta_threads;       /* threads per persistent CTA: 0 = auto (1024 when the max out-degree
+                                is > 32, else 512), 512 or 1024 */
+  int32_t reserved2;         /* must be 0 */
 } gi_options;
 
 /* Counters of one query (SURVEY §8(a) "Counter definitions"). */

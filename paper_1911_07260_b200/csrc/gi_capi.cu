@@ -100,7 +100,7 @@ struct gi_graph {
   uint2* d_slots = nullptr;  // ELL adjacency slots, 64 B per vertex
   uint32_t max_deg = 0;
   int sm_count = 0;
-  int bps[3] = {0, 0, 0};  // co-resident CTAs per SM, by KernelKind
+  int bps[2][3] = {{0, 0, 0}, {0, 0, 0}};  // co-resident CTAs per SM, by width (512, 1024) and KernelKind
   int bps_kcore = 0;
   std::mutex mu;
   std::vector<std::unique_ptr<Workspace>> pool;
@@ -205,7 +205,7 @@ void ws_release(gi_graph* g, Workspace* w, bool healthy) {
   g->pool.emplace_back(w);
 }
 
-void fill_stats(gi_stats* st, const QStats& q, float ms, int ctas, int groups, int kind) {
+void fill_stats(gi_stats* st, const QStats& q, float ms, int ctas, int groups, int kind, int threads) {
   st->buckets = q.buckets;
   st->rounds = q.rounds;
   st->grid_syncs = q.phases;
@@ -219,7 +219,7 @@ void fill_stats(gi_stats* st, const QStats& q, float ms, int ctas, int groups, i
   st->critical_subrounds = q.critical_subrounds;
   st->gpu_ms = ms;
   st->ctas = ctas;
-  st->threads_per_cta = kBlock;
+  st->threads_per_cta = threads;
   st->groups = groups;
   st->kernel_kind = kind;
 }
@@ -271,7 +271,12 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   // async drain (every adjacency inline in its ELL slot) is opt-in — measured slower on
   // configs 1-2, kept as the comparison point
   const int kind = !fused ? KIND_UNFUSED : opt.drain == 2 ? KIND_FUSED_ASYNC : KIND_FUSED_BSP;
-  const int bps = g->bps[kind];
+  // CTA width: 1024 threads on skewed graphs (memory-level parallelism in stage B),
+  // 512 otherwise (the latency-bound chains of road graphs); gi_options.cta_threads overrides
+  if (opt.cta_threads != 0 && opt.cta_threads != 512 && opt.cta_threads != 1024)
+    return fail(GI_ERR_INVALID_ARGUMENT, "cta_threads must be 0, 512 or 1024");
+  const int wide = opt.cta_threads ? (opt.cta_threads == 1024) : (g->max_deg > 32 ? 1 : 0);
+  const int bps = g->bps[wide][kind];
   int total = g->sm_count * bps;
   // group sizing: single source -> one group of every CTA (capped by max_ctas);
   // batch -> several groups in flight, each of group_ctas CTAs
@@ -369,7 +374,8 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   a.h = d_h;
 
   if ((e = cudaEventRecord(w->ev0, st))) return bail(e, "event");
-  if ((e = launch_sssp(a, kind, G * ngroups, st))) return bail(e, "launch sssp_persistent");
+  if ((e = wide ? v1024::launch_sssp(a, kind, G * ngroups, st) : v512::launch_sssp(a, kind, G * ngroups, st)))
+    return bail(e, "launch sssp_persistent");
   if ((e = cudaEventRecord(w->ev1, st))) return bail(e, "event");
   std::vector<QStats> hq(nsrc);
   if ((e = cudaMemcpyAsync(hq.data(), w->d_qstats, sizeof(QStats) * nsrc, cudaMemcpyDeviceToHost, st)))
@@ -390,7 +396,7 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   bool ovf = false;
   for (int i = 0; i < nsrc; ++i) {
     if (hq[i].overflow) ovf = true;
-    if (stats) fill_stats(&stats[i], hq[i], ms, G, ngroups, kind);
+    if (stats) fill_stats(&stats[i], hq[i], ms, G, ngroups, kind, wide ? 1024 : 512);
   }
   if (ovf) return fail(GI_ERR_OVERFLOW, "a reachable vertex has distance >= UINT32_MAX");
   return GI_OK;
@@ -451,8 +457,10 @@ gi_status gi_graph_create(int64_t n, int64_t m, const int64_t* row_offsets, cons
   GI_CUDA(kcore_occupancy(&g->bps_kcore), "occupancy");
   if (g->bps_kcore < 1) return fail(GI_ERR_CUDA, "k-core kernel cannot be resident");
   for (int k = 0; k < 3; ++k) {
-    GI_CUDA(query_occupancy(k, &g->bps[k]), "occupancy");
-    if (g->bps[k] < 1) return fail(GI_ERR_CUDA, "persistent kernel variant %d cannot be resident", k);
+    GI_CUDA(v512::query_occupancy(k, &g->bps[0][k]), "occupancy");
+    GI_CUDA(v1024::query_occupancy(k, &g->bps[1][k]), "occupancy");
+    if (g->bps[0][k] < 1 || g->bps[1][k] < 1)
+      return fail(GI_ERR_CUDA, "persistent kernel variant %d cannot be resident", k);
   }
 
   cudaStream_t st;

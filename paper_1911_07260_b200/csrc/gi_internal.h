@@ -146,8 +146,17 @@ struct KcArgs {
 };
 
 // Host-side launchers (gi_kernels.cu).
+// The SSSP-family persistent kernels, compiled once per CTA width (gi_kernels.cu).
+namespace v512 {
 cudaError_t launch_sssp(const KArgs& a, int kind, int grid, cudaStream_t st);
 cudaError_t query_occupancy(int kind, int* blocks_per_sm);
+int smem_bytes(int kind);
+}  // namespace v512
+namespace v1024 {
+cudaError_t launch_sssp(const KArgs& a, int kind, int grid, cudaStream_t st);
+cudaError_t query_occupancy(int kind, int* blocks_per_sm);
+int smem_bytes(int kind);
+}  // namespace v1024
 cudaError_t launch_interleave(const int32_t* cols, const uint32_t* w, uint2* edges, int64_t count,
                               int64_t n, uint32_t* bad_flag, cudaStream_t st);
 cudaError_t launch_build_slots(const int64_t* off, const uint2* edges, uint2* slots, int64_t n,
@@ -155,7 +164,6 @@ cudaError_t launch_build_slots(const int64_t* off, const uint2* edges, uint2* sl
 cudaError_t launch_max_degree(const int64_t* off, int64_t n, uint32_t* max_deg, cudaStream_t st);
 cudaError_t launch_validate_offsets(const int64_t* off, int64_t n, int64_t m, uint32_t* bad_flag,
                                     cudaStream_t st);
-int smem_bytes(int kind);
 cudaError_t launch_kcore(const KcArgs& a, int grid, cudaStream_t st);  // gi_kcore.cu
 cudaError_t kcore_occupancy(int* blocks_per_sm);
 

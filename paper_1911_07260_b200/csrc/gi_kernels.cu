@@ -37,6 +37,16 @@
 #include "gi_internal.h"
 #include "gi_device.cuh"
 
+// This file is compiled once per CTA width (GI_BLOCK / GI_VARIANT): v512 (the default,
+// and the only one with GI_PRIMARY, which also builds the graph-setup kernels) and
+// v1024 (skewed graphs: twice the warps per SM for memory-level parallelism).
+#ifndef GI_VARIANT
+#define GI_VARIANT v512
+#endif
+#ifndef GI_PRIMARY
+#define GI_PRIMARY 1
+#endif
+
 #include <cooperative_groups.h>
 
 namespace cg = cooperative_groups;
@@ -1439,35 +1449,14 @@ __global__ void validate_offsets_kernel(const int64_t* __restrict__ off, int64_t
 
 }  // namespace
 
+namespace GI_VARIANT {
+
 int smem_bytes(int kind) {
   const int far = kFarStage * (int)sizeof(int32_t);
   if (kind == KIND_FUSED_ASYNC) return (kRing + (kBlock / 32) * 4) * (int)(sizeof(uint4) * 5) + far;
   return 2 * kBinCap * (int)sizeof(uint2) + kBigCap * ((int)sizeof(BigEnt) + (int)sizeof(unsigned long long)) + far;
 }
 
-#ifdef GI_TRACE
-extern "C" int gi_debug_trace2(unsigned long long* phase, unsigned long long* item, int reset) {
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(phase, g_phase, sizeof(unsigned long long) * 7 * kTracePhases);
-  cudaMemcpyFromSymbol(item, g_item, sizeof(unsigned long long) * 16);
-  if (reset) {
-    static unsigned long long z[7 * kTracePhases];
-    cudaMemcpyToSymbol(g_phase, z, sizeof(z));
-    cudaMemcpyToSymbol(g_item, z, sizeof(unsigned long long) * 16);
-  }
-  return 0;
-}
-
-extern "C" int gi_debug_trace(unsigned long long* out, int reset) {
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 32);
-  if (reset) {
-    unsigned long long z[32] = {0};
-    cudaMemcpyToSymbol(g_trace, z, sizeof(z));
-  }
-  return 0;
-}
-#endif
 
 static const void* kernel_fn(int kind) {
   switch (kind) {
@@ -1501,6 +1490,33 @@ cudaError_t launch_sssp(const KArgs& a, int kind, int grid, cudaStream_t st) {
   return cudaLaunchCooperativeKernel(kernel_fn(kind), dim3(grid), dim3(kBlock), params, smem_bytes(kind), st);
 }
 
+}  // namespace GI_VARIANT
+
+#if GI_PRIMARY
+#ifdef GI_TRACE
+extern "C" int gi_debug_trace2(unsigned long long* phase, unsigned long long* item, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(phase, g_phase, sizeof(unsigned long long) * 7 * kTracePhases);
+  cudaMemcpyFromSymbol(item, g_item, sizeof(unsigned long long) * 16);
+  if (reset) {
+    static unsigned long long z[7 * kTracePhases];
+    cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+    cudaMemcpyToSymbol(g_item, z, sizeof(unsigned long long) * 16);
+  }
+  return 0;
+}
+
+extern "C" int gi_debug_trace(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 32);
+  if (reset) {
+    unsigned long long z[32] = {0};
+    cudaMemcpyToSymbol(g_trace, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
+
 static unsigned grid_for(int64_t count) {
   int64_t blocks = (count + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
@@ -1531,5 +1547,7 @@ cudaError_t launch_validate_offsets(const int64_t* off, int64_t n, int64_t m, ui
   validate_offsets_kernel<<<grid_for(n), 256, 0, st>>>(off, n, m, bad_flag);
   return cudaGetLastError();
 }
+
+#endif  // GI_PRIMARY
 
 }  // namespace gi

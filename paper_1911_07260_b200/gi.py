@@ -46,7 +46,8 @@ class gi_options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("fusion", ctypes.c_int32),
                 ("fusion_threshold", ctypes.c_uint32), ("max_ctas", ctypes.c_int32),
                 ("hub_min", ctypes.c_uint32), ("drain", ctypes.c_uint32),
-                ("group_ctas", ctypes.c_int32), ("pre_read", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p)]
+                ("group_ctas", ctypes.c_int32), ("pre_read", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p),
+                ("cta_threads", ctypes.c_int32), ("reserved2", ctypes.c_int32)]
 
 
 class gi_stats(ctypes.Structure):
@@ -122,7 +123,7 @@ def _ptr(x):
 
 
 def make_options(fusion=True, threshold=0, max_ctas=0, group_ctas=0, pre_read=0, hub_min=0,
-                 drain=0, stream=None) -> gi_options:
+                 drain=0, stream=None, cta_threads=0) -> gi_options:
     o = gi_options()
     _lib.gi_options_default(ctypes.byref(o))
     o.fusion = 1 if fusion else 0
@@ -132,6 +133,7 @@ def make_options(fusion=True, threshold=0, max_ctas=0, group_ctas=0, pre_read=0,
     o.pre_read = pre_read
     o.hub_min = hub_min
     o.drain = {"auto": 0, "bsp": 1, "async": 2}.get(drain, drain)
+    o.cta_threads = cta_threads
     if stream is not None:
         o.cuda_stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     return o

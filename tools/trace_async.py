@@ -12,10 +12,17 @@ import numpy as np  # noqa: E402
 import gen  # noqa: E402
 
 so = "/tmp/libgi_trace.so"
-src = [os.path.join(ROOT, "paper_1911_07260_b200/csrc", f) for f in ("gi_kernels.cu", "gi_capi.cu")]
+CS = os.path.join(ROOT, "paper_1911_07260_b200/csrc")
 if not os.path.exists(so) or os.environ.get("REBUILD"):
-    subprocess.check_call(["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-DGI_TRACE",
-                           "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"), "-o", so] + src)
+    nv = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-DGI_TRACE", "-Xcompiler",
+          "-fPIC", "-I", os.path.join(ROOT, "include")]
+    objs = []
+    for src, defs, obj in ((f"{CS}/gi_kernels.cu", ["-DGI_BLOCK=512", "-DGI_VARIANT=v512", "-DGI_PRIMARY=1"], "/tmp/tk512.o"),
+                           (f"{CS}/gi_kernels.cu", ["-DGI_BLOCK=1024", "-DGI_VARIANT=v1024", "-DGI_PRIMARY=0"], "/tmp/tk1024.o"),
+                           (f"{CS}/gi_capi.cu", [], "/tmp/tcapi.o"), (f"{CS}/gi_kcore.cu", [], "/tmp/tkcore.o")):
+        subprocess.check_call(nv + defs + ["-c", src, "-o", obj])
+        objs.append(obj)
+    subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", so] + objs)
 lib = ctypes.CDLL(so)
 vp, i64, i32, u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32
 lib.gi_debug_trace.argtypes = [vp, ctypes.c_int]
