@@ -100,7 +100,7 @@ struct gi_graph {
   uint2* d_slots = nullptr;  // ELL adjacency slots, 64 B per vertex
   uint32_t max_deg = 0;
   int sm_count = 0;
-  int bps[2][3] = {{0, 0, 0}, {0, 0, 0}};  // co-resident CTAs per SM, by width (512, 1024) and KernelKind
+  int bps[2][KIND_COUNT] = {};  // co-resident CTAs per SM, by width (512, 1024) and KernelKind
   int bps_kcore = 0;
   std::mutex mu;
   std::vector<std::unique_ptr<Workspace>> pool;
@@ -270,7 +270,11 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   // default: the CTA-barrier (BSP) drain with the degree-binned stages; the barrier-free
   // async drain (every adjacency inline in its ELL slot) is opt-in — measured slower on
   // configs 1-2, kept as the comparison point
-  const int kind = !fused ? KIND_UNFUSED : opt.drain == 2 ? KIND_FUSED_ASYNC : KIND_FUSED_BSP;
+  int kind = !fused ? KIND_UNFUSED : opt.drain == 2 ? KIND_FUSED_ASYNC : KIND_FUSED_BSP;
+  // low-degree specialisation: every adjacency inline in its slot and no pre-read
+  const bool lowdeg = g->max_deg <= kAsyncMaxDeg && opt.pre_read != 1;
+  if (lowdeg && kind == KIND_UNFUSED) kind = KIND_UNFUSED_LD;
+  if (lowdeg && kind == KIND_FUSED_BSP) kind = KIND_FUSED_BSP_LD;
   // CTA width: 1024 threads on skewed graphs (memory-level parallelism in stage B),
   // 512 otherwise (the latency-bound chains of road graphs); gi_options.cta_threads overrides
   if (opt.cta_threads != 0 && opt.cta_threads != 512 && opt.cta_threads != 1024)
@@ -396,7 +400,7 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   bool ovf = false;
   for (int i = 0; i < nsrc; ++i) {
     if (hq[i].overflow) ovf = true;
-    if (stats) fill_stats(&stats[i], hq[i], ms, G, ngroups, kind, wide ? 1024 : 512);
+    if (stats) fill_stats(&stats[i], hq[i], ms, G, ngroups, base_kind(kind), wide ? 1024 : 512);
   }
   if (ovf) return fail(GI_ERR_OVERFLOW, "a reachable vertex has distance >= UINT32_MAX");
   return GI_OK;
@@ -456,7 +460,7 @@ gi_status gi_graph_create(int64_t n, int64_t m, const int64_t* row_offsets, cons
   g->sm_count = prop.multiProcessorCount;
   GI_CUDA(kcore_occupancy(&g->bps_kcore), "occupancy");
   if (g->bps_kcore < 1) return fail(GI_ERR_CUDA, "k-core kernel cannot be resident");
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < KIND_COUNT; ++k) {
     GI_CUDA(v512::query_occupancy(k, &g->bps[0][k]), "occupancy");
     GI_CUDA(v1024::query_occupancy(k, &g->bps[1][k]), "occupancy");
     if (g->bps[0][k] < 1 || g->bps[1][k] < 1)

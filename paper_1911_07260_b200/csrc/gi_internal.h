@@ -33,7 +33,14 @@ constexpr uint32_t kRingSafe = kRing - 16 * 32 - 64;  // admission limit (see th
 constexpr uint32_t kAsyncMaxDeg = kSlotEdges;  // async drain needs every adjacency inline in its ELL slot
 
 // Persistent-kernel variants.
-enum KernelKind : int { KIND_UNFUSED = 0, KIND_FUSED_BSP = 1, KIND_FUSED_ASYNC = 2 };
+enum KernelKind : int {
+  KIND_UNFUSED = 0, KIND_FUSED_BSP = 1, KIND_FUSED_ASYNC = 2,
+  // low-degree specialisations (every adjacency inline in its ELL slot, no pre-read): the
+  // high-degree stages compiled out of the sub-round's serial path
+  KIND_UNFUSED_LD = 3, KIND_FUSED_BSP_LD = 4,
+  KIND_COUNT = 5
+};
+inline int base_kind(int k) { return k == KIND_UNFUSED_LD ? KIND_UNFUSED : k == KIND_FUSED_BSP_LD ? KIND_FUSED_BSP : k; }
 
 // Division by the invariant Δ (Granlund & Montgomery 1994, round-up method):
 // q = (t + ((x - t) >> s1)) >> s2 with t = umulhi(mul, x).

@@ -322,7 +322,7 @@ __device__ __forceinline__ void bulk_append(uint32_t n, Get get, uint32_t* bits,
 // bit k of `valid` clear do nothing. Every load and atomic of the batch is issued
 // before any result is consumed (memory-level parallelism on the critical chain).
 // Must be called by all 32 lanes of the warp (the appends are warp-aggregated).
-template <bool FUSED, int K>
+template <bool FUSED, int K, bool LD = false>
 __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], const uint32_t (&du)[K],
                                                 uint32_t valid, const uint32_t* cur = nullptr) {
   uint32_t nd[K], old[K];
@@ -335,7 +335,7 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
       else ok |= 1u << k;
     }
   }
-  if (c.pre_read) {
+  if (!LD && c.pre_read) {
     // pre-read dist[v]; only an improving candidate is written, with a fire-and-forget
     // red.min, and the pre-read value stands for the atomic's old value. Two threads that
     // both improve on the same pre-read may both push v: a duplicate entry, which the
@@ -441,7 +441,7 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
 // the 8 lanes of an octet share one entry and lane k relaxes entry k of its 64-byte
 // ELL slot (one coalesced 64 B load per octet). Each thread holds U items in flight.
 // Vertices with deg > 8 are appended to the CTA's high-degree list for stage B.
-template <bool FUSED, int U>
+template <bool FUSED, int U, bool LD = false>
 __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t nin, bool check_stale,
                                             uint32_t& nv, uint32_t& ne) {
   const uint32_t nitems = nin * 8;
@@ -472,7 +472,7 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (!(have & (1u << u))) continue;
-      if (e[u].x == kColBig) {  // octet-uniform: every entry of a big slot is kColBig
+      if (!LD && e[u].x == kColBig) {  // octet-uniform: every entry of a big slot is kColBig
         const uint32_t om = 0xFFu << (threadIdx.x & 24);
         const uint32_t lo = __shfl_sync(om, e[u].y, 1, 8);
         const uint32_t hi = __shfl_sync(om, e[u].y, 2, 8);
@@ -508,7 +508,7 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
         if (e[u].x != kColEmpty) valid |= 1u << u;
       }
     }
-    const uint32_t stale = relax_batch<FUSED, U>(c, e, du, valid, check_stale ? cur : nullptr);
+    const uint32_t stale = relax_batch<FUSED, U, LD>(c, e, du, valid, check_stale ? cur : nullptr);
     // counters: non-stale entries and their edges (stale is per lane; each lane saw
     // its own probe of the same word)
     nv += __popc(heads & ~stale);
@@ -605,13 +605,14 @@ __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32
 
 // Relax every entry of a CTA-local bin (stage A, then stage B when high-degree
 // vertices were found). Starts after and ends with a CTA barrier.
-template <bool FUSED>
+template <bool FUSED, bool LD = false>
 __device__ __forceinline__ void process_bin(Ctx& c, Shared& s, const uint2* in, uint32_t nin,
                                             bool check_stale, uint32_t& nv, uint32_t& ne) {
-  if (nin * 8 <= (uint32_t)kBlock) stage_small<FUSED, 1>(c, in, nin, check_stale, nv, ne);
-  else stage_small<FUSED, 4>(c, in, nin, check_stale, nv, ne);
+  if (nin * 8 <= (uint32_t)kBlock) stage_small<FUSED, 1, LD>(c, in, nin, check_stale, nv, ne);
+  else stage_small<FUSED, 4, LD>(c, in, nin, check_stale, nv, ne);
   __syncthreads();
   TRACE(4);
+  if constexpr (LD) return;  // no high-degree list on a low-degree graph
   const uint32_t nb = min(s.bigtail, (uint32_t)kBigCap);
   if (nb) {
     __syncthreads();  // everyone has read bigtail
@@ -971,8 +972,9 @@ __device__ __forceinline__ void async_feed(Ctx& c, Shared& s, const Ring& r, boo
 
 template <int KIND>
 __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs a) {
-  constexpr bool FUSED = KIND != KIND_UNFUSED;
+  constexpr bool FUSED = KIND != KIND_UNFUSED && KIND != KIND_UNFUSED_LD;
   constexpr bool ASYNC = KIND == KIND_FUSED_ASYNC;
+  constexpr bool LOWDEG = KIND == KIND_UNFUSED_LD || KIND == KIND_FUSED_BSP_LD;
   // bsp: bins [2][kBinCap] uint2, high-degree list [kBigCap], its prefix [kBigCap], far staging
   // [kFarStage]; async: ring [kRing] (+ per-warp queues), far staging
   extern __shared__ uint2 s_dyn[];
@@ -1270,7 +1272,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           }
           __syncthreads();
           TRACE(14);
-          process_bin<FUSED>(c, s, stage, chunk, false, nv, ne);  // ends with a barrier
+          process_bin<FUSED, LOWDEG>(c, s, stage, chunk, false, nv, ne);  // ends with a barrier
           if (a.dyn_claim) {
             if (tid == 0) {
               s.claim = dyn ? next : cnt;
@@ -1306,7 +1308,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           if (tid == 0) { s.cnt3[(k + 1) % 3] = 0; ++subrounds; }
           c.out = s_dyn + (k & 1) * kBinCap;
           c.outcnt = &s.cnt3[k % 3];
-          process_bin<FUSED>(c, s, in, nin, true, nv, ne);
+          process_bin<FUSED, LOWDEG>(c, s, in, nin, true, nv, ne);
         }
       }
 
@@ -1462,11 +1464,13 @@ static const void* kernel_fn(int kind) {
   switch (kind) {
     case KIND_UNFUSED: return (const void*)sssp_persistent<KIND_UNFUSED>;
     case KIND_FUSED_BSP: return (const void*)sssp_persistent<KIND_FUSED_BSP>;
+    case KIND_UNFUSED_LD: return (const void*)sssp_persistent<KIND_UNFUSED_LD>;
+    case KIND_FUSED_BSP_LD: return (const void*)sssp_persistent<KIND_FUSED_BSP_LD>;
     default: return (const void*)sssp_persistent<KIND_FUSED_ASYNC>;
   }
 }
 
-static bool g_attr_set[3] = {false, false, false};
+static bool g_attr_set[KIND_COUNT] = {};
 
 static cudaError_t set_attrs(int kind) {
   if (g_attr_set[kind]) return cudaSuccess;

@@ -43,7 +43,7 @@ __global__ void hop(uint32_t* dist, const uint4* slots, int steps, int mode, int
   *sink = acc;
 }
 
-int main() {
+int main_hop() {
   const size_t N = 1u << 24;
   uint32_t* dist;
   uint4* slots;
@@ -67,4 +67,66 @@ int main() {
     }
   }
   return 0;
+}
+
+// Minimal BSP sub-round on a path (one CTA of 512 threads): octet 0 reads the bin entry
+// (smem), loads the vertex's 64 B slot (8 B per lane), atomicMins the successor, pushes
+// it into the other bin, and every thread meets at __syncthreads. Cycles per sub-round.
+__global__ void bsp_chain(uint32_t* dist, const uint2* slots, int steps, long long* out) {
+  __shared__ uint2 bin[2][64];
+  __shared__ uint32_t cnt[2];
+  if (threadIdx.x == 0) { bin[0][0] = make_uint2(0, 0); cnt[0] = 1; cnt[1] = 0; }
+  __syncthreads();
+  long long t0 = clock64();
+  for (int s = 0; s < steps; ++s) {
+    const int cur = s & 1;
+    const uint32_t n = cnt[cur];
+    if (threadIdx.x < 8 * n) {
+      const uint2 it = bin[cur][threadIdx.x >> 3];
+      const uint2 e = __ldg(slots + 8 * (size_t)it.x + (threadIdx.x & 7));
+      if (e.x != 0xFFFFFFFFu) {
+        const uint32_t nd = it.y + e.y;
+        const uint32_t old = atomicMin(dist + e.x, nd);
+        if (nd < old) {
+          const uint32_t p = atomicAdd(&cnt[cur ^ 1], 1u);
+          bin[cur ^ 1][p & 63] = make_uint2(e.x, nd);
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) cnt[cur] = 0;
+    __syncthreads();
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[0] = (t1 - t0) / steps;
+}
+
+int main_bsp() {
+  const int n = 100000;
+  uint32_t* dist;
+  uint2* slots;
+  cudaMalloc(&dist, n * 4);
+  cudaMalloc(&slots, (size_t)n * 64);
+  uint2* h = new uint2[(size_t)n * 8];
+  for (int v = 0; v < n; ++v)
+    for (int k = 0; k < 8; ++k) h[(size_t)v * 8 + k] = make_uint2(0xFFFFFFFFu, 0);
+  for (int v = 0; v < n; ++v) {
+    if (v + 1 < n) h[(size_t)v * 8 + 0] = make_uint2(v + 1, 1);
+    if (v > 0) h[(size_t)v * 8 + 1] = make_uint2(v - 1, 1);
+  }
+  cudaMemcpy(slots, h, (size_t)n * 64, cudaMemcpyHostToDevice);
+  long long* out;
+  cudaMallocManaged(&out, 64);
+  for (int rep = 0; rep < 2; ++rep) {
+    cudaMemset(dist, 0xFF, n * 4);
+    bsp_chain<<<1, 512>>>(dist, slots, 20000, out);
+    cudaDeviceSynchronize();
+  }
+  printf("minimal BSP sub-round (path, 1 CTA x 512): %lld cycles\n", out[0]);
+  return 0;
+}
+
+int main() {
+  main_hop();
+  return main_bsp();
 }

@@ -6,7 +6,7 @@ import gen
 from paper_1911_07260_b200 import gi
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--config", type=int, default=2, help="0 = path graph of 20000 vertices (one chain)")
 ap.add_argument("--delta", type=int, default=1 << 16)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--no-fusion", action="store_true")
@@ -15,9 +15,9 @@ ap.add_argument("--max-ctas", type=int, default=0)
 ap.add_argument("--pre-read", type=int, default=0)
 ap.add_argument("--drain", default="auto")
 a = ap.parse_args()
-g = gen.config_graph(a.config)
+g = gen.config_graph(a.config) if a.config else gen.path(20000)
 G = gi.Graph.from_csr(g)
-src = gen.config_source(a.config, g)
+src = gen.config_source(a.config, g) if a.config else 0
 for i in range(a.reps):
     d, st = gi.sssp(G, src, a.delta, fusion=not a.no_fusion, threshold=a.threshold, max_ctas=a.max_ctas, pre_read=a.pre_read,
                      drain=a.drain)
