@@ -659,6 +659,9 @@ gi_status gi_kcore_ex(const gi_graph* cg_, const gi_options* opt_in, uint32_t* c
   a.pile[1] = w->h_groups[0].far[1];
   a.q[0] = w->h_groups[0].q[0];
   a.q[1] = w->h_groups[0].q[1];
+  a.hub[0] = w->h_groups[0].hub[0];
+  a.hub[1] = w->h_groups[0].hub[1];
+  a.hubcap = w->hubcap;
   a.ctl = w->kc_ctl;
   a.stats = w->kc_stats;
   int grid = g->sm_count * g->bps_kcore;
@@ -683,6 +686,8 @@ gi_status gi_kcore_ex(const gi_graph* cg_, const gi_options* opt_in, uint32_t* c
     stats->vertices_processed = hs.vertices;
     stats->edges_relaxed = hs.edges;
     stats->empty_extractions = hs.empty;
+    stats->fused_subrounds = hs.subrounds;
+    stats->spills = hs.spills;
     stats->gpu_ms = ms;
     stats->ctas = grid;
     stats->threads_per_cta = 512;

@@ -131,13 +131,14 @@ struct alignas(128) KcCtl {
   uint32_t kmin[3];     // min priority of the unfinished vertices, by extraction mod 3
   uint32_t qclaim[3];   // ROUND: next unclaimed frontier position, by phase mod 3
   uint32_t xfin[3];     // vertices finished by an extraction, by extraction mod 3
-  uint32_t pad0[17];
+  uint32_t hcount[3];   // group hub-list sizes, by phase mod 3
+  uint32_t pad0[14];
   uint32_t bar;         // group barrier word, own 128 B line
   uint32_t pad1[31];
 };
 
 struct KcStats {
-  unsigned long long buckets, rounds, phases, vertices, edges, empty;
+  unsigned long long buckets, rounds, phases, vertices, edges, empty, subrounds, spills;
 };
 
 struct KcArgs {
@@ -148,6 +149,8 @@ struct KcArgs {
   uint32_t* core;       // [n] result: coreness
   int32_t* pile[2];     // [n] unfinished vertices, double-buffered across extractions
   int32_t* q[2];        // [n] frontier, double-buffered across phases
+  struct HubEnt* hub[2];  // [hubcap] group hub lists (degree >= 1024), by phase parity
+  uint32_t hubcap;
   KcCtl* ctl;
   KcStats* stats;
 };

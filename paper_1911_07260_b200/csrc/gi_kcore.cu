@@ -25,23 +25,54 @@
 //                k belongs to a finished vertex, which every later edge skips.
 // Frontier chunks are claimed dynamically (skewed degrees) and relaxed edge-balanced:
 // block scan of the chunk's degrees, 8 consecutive edges per thread per iteration.
+// Bucket fusion carries over (the current bucket k is processed eagerly, R1): vertices
+// finished by an extraction or a crossing go to a CTA-local bin drained with CTA barriers
+// while it holds < T vertices; a larger bin spills to the global frontier.
 #include "gi_internal.h"
 #include "gi_device.cuh"
+
+#include <cooperative_groups.h>
 
 namespace gi {
 namespace {
 
+namespace cg = cooperative_groups;
+
 constexpr int kKcBlock = 512;
 constexpr int kKcEdges = 8;     // consecutive edges per thread per iteration
-constexpr int kKcChunk = 2048;  // frontier vertices staged per claim (max)
+constexpr int kKcChunk = 2048;  // frontier vertices staged per claim / per local bin (max)
+constexpr uint32_t kKcT = 1024; // bucket fusion threshold: a local bin of >= T vertices spills
+constexpr uint32_t kKcHub = 1024;  // out-degree >= this: edges split over every CTA in the next round
 constexpr uint32_t kUnset = 0xFFFFFFFFu;
 
 enum : uint32_t { KC_ROUND = 0, KC_EXTRACT = 1, KC_DONE = 2 };
 
 struct KcShared {
-  uint32_t mode, k, cnt, claim, kmin;
+  uint32_t mode, k, cnt, claim, kmin, hn;
+  uint32_t bincnt[3];           // local bin fills, rotating by drain iteration
   unsigned long long total;
   unsigned long long red[kKcBlock / 32];
+};
+
+struct KcSmem {
+  long long* beg;               // [kKcChunk] staged edge offsets
+  uint32_t* deg;                // [kKcChunk] staged degrees
+  unsigned long long* pre;      // [kKcChunk] exclusive prefix of the staged degrees
+  int32_t* bin[2];              // [kKcChunk] local bins (bucket fusion of the current k)
+};
+
+// Per-phase relaxation context.
+struct KcCtx {
+  uint32_t k;
+  int32_t* q_next;              // global frontier (spill target)
+  uint32_t* qcount_next;
+  int32_t* out;                 // local bin receiving crossings (shared memory)
+  uint32_t* outcnt;
+  HubEnt* hub_next;             // group hub list receiving this phase's hubs
+  uint32_t* hcount_next;
+  uint32_t hubcap;
+  uint32_t my_kmin;
+  unsigned long long nfin, nedge;
 };
 
 __device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) { return __ldcg(p); }
@@ -57,11 +88,157 @@ __device__ __forceinline__ void kc_append(bool want, int32_t v, int32_t* list, u
   if (want) list[base + __popc(m & ((1u << lane) - 1u))] = v;
 }
 
+// A vertex finished at k joins the current bucket's frontier: the CTA-local bin (bucket
+// fusion: drained in this phase, no group barrier) or, when the bin is full, the global
+// frontier (the next group-wide round). Called by all 32 lanes.
+__device__ __forceinline__ void kc_push(KcCtx& c, bool want, int32_t v) {
+  const uint32_t m = __ballot_sync(0xffffffffu, want);
+  if (!m) return;
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  if (lane == 0) base = atomicAdd(c.outcnt, (uint32_t)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
+  const bool spill = want && pos >= (uint32_t)kKcChunk;
+  if (want && !spill) c.out[pos] = v;
+  kc_append(spill, v, c.q_next, c.qcount_next);
+}
+
+// Stage the cnt (<= kKcChunk) frontier vertices of `list` (global or shared) as (offset,
+// degree) entries; a vertex of degree >= kKcHub goes to the group hub list instead (its
+// edges are split over every CTA in the next round) and is staged with degree 0.
+__device__ __forceinline__ void kc_stage_vertices(const KcArgs& a, const KcSmem& m, KcCtx& c, const int32_t* list,
+                                                  uint32_t cnt) {
+  for (uint32_t i = threadIdx.x; i < cnt; i += kKcBlock) {
+    const int32_t v = list[i];
+    const long long b0 = a.off[v], b1 = a.off[v + 1];
+    uint32_t d = (uint32_t)(b1 - b0);
+    if (d >= kKcHub) {
+      const uint32_t hp = atomicAdd(c.hcount_next, 1u);
+      if (hp < c.hubcap) {
+        HubEnt he;
+        he.beg = b0;
+        he.deg = d;
+        he.du = 0;
+        c.hub_next[hp] = he;
+        d = 0;
+      }
+    }
+    m.beg[i] = b0;
+    m.deg[i] = d;
+  }
+  __syncthreads();
+}
+
+// Relax every edge of the cnt staged entries (m.beg, m.deg): block scan of the degrees,
+// 8 consecutive edges per thread per iteration. Starts after and ends with a CTA barrier;
+// all threads call it.
+__device__ __forceinline__ void kc_relax_entries(const KcArgs& a, KcShared& s, const KcSmem& m, KcCtx& c,
+                                                 uint32_t cnt) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  const uint32_t k = c.k;
+  unsigned long long sum = 0;
+  constexpr int PER = kKcChunk / kKcBlock;
+  unsigned long long loc[PER];
+#pragma unroll
+  for (int x = 0; x < PER; ++x) {
+    const uint32_t i = tid * PER + x;
+    loc[x] = sum;
+    if (i < cnt) sum += m.deg[i];
+  }
+  unsigned long long incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += t;
+  }
+  if (lane == 31) s.red[tid >> 5] = incl;
+  __syncthreads();
+  if (tid < 32) {
+    const unsigned long long w = lane < kKcBlock / 32 ? s.red[lane] : 0ull;
+    unsigned long long wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= (uint32_t)o) wi += t;
+    }
+    if (lane < kKcBlock / 32) s.red[lane] = wi - w;
+    if (lane == kKcBlock / 32 - 1) s.total = wi;
+  }
+  __syncthreads();
+  const unsigned long long off0 = s.red[tid >> 5] + incl - sum;
+#pragma unroll
+  for (int x = 0; x < PER; ++x) {
+    const uint32_t i = tid * PER + x;
+    if (i < cnt) m.pre[i] = off0 + loc[x];
+  }
+  __syncthreads();
+  const unsigned long long total = s.total;
+  if (tid == 0) c.nedge += total;
+  for (unsigned long long k0 = 0; k0 < total; k0 += (unsigned long long)kKcEdges * kKcBlock) {
+    int32_t tv[kKcEdges];
+#pragma unroll
+    for (int u = 0; u < kKcEdges; ++u) tv[u] = -1;
+    const unsigned long long kt = k0 + (unsigned long long)kKcEdges * tid;
+    if (kt < total) {
+      uint32_t lo = 0, hi = cnt;  // last i with pre[i] <= kt
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (m.pre[mid] <= kt) lo = mid; else hi = mid;
+      }
+      unsigned long long nxt = lo + 1 < cnt ? m.pre[lo + 1] : total;
+      long long rel = m.beg[lo] - (long long)m.pre[lo];
+#pragma unroll
+      for (int u = 0; u < kKcEdges; ++u) {
+        const unsigned long long e = kt + u;
+        if (e < total) {
+          while (e >= nxt) {  // next frontier vertex (skipping degree-0 ones)
+            ++lo;
+            rel = m.beg[lo] - (long long)nxt;
+            nxt = lo + 1 < cnt ? m.pre[lo + 1] : total;
+          }
+          tv[u] = (int32_t)__ldg(&a.edges[rel + (long long)e].x);
+        }
+      }
+    }
+    // skip finished endpoints (coherent read; finished is final)
+    uint32_t cv[kKcEdges];
+#pragma unroll
+    for (int u = 0; u < kKcEdges; ++u) cv[u] = tv[u] >= 0 ? ld_cg(a.core + tv[u]) : 0u;
+#pragma unroll
+    for (int u = 0; u < kKcEdges; ++u) {
+      const bool want = tv[u] >= 0 && cv[u] == kUnset;
+      // constant-sum reduction: one atomic per distinct endpoint per warp
+      const uint32_t key = want ? (uint32_t)tv[u] : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, key);
+      const bool leader = want && (__ffs(peers) - 1) == (int)lane;
+      bool cross = false;
+      if (leader) {
+        const uint32_t cntp = __popc(peers);
+        const uint32_t old = atomicSub(a.prio + tv[u], cntp);
+        if (old > k && old - cntp <= k) {
+          cross = true;  // this subtraction took the priority to <= k: finished at k
+          a.core[tv[u]] = k;
+        } else if (old > k) {
+          c.my_kmin = min(c.my_kmin, old - cntp);
+        }
+      }
+      c.nfin += cross;
+      kc_push(c, cross, tv[u]);
+    }
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
-  extern __shared__ unsigned long long kc_dyn[];  // beg [kKcChunk] int64, pre [kKcChunk] u64
+  extern __shared__ unsigned long long kc_dyn[];  // beg, pre [kKcChunk] 8 B; bins [2][kKcChunk] 4 B
   __shared__ KcShared s;
-  long long* sbeg = reinterpret_cast<long long*>(kc_dyn);
-  unsigned long long* spre = kc_dyn + kKcChunk;
+  KcSmem sm;
+  sm.beg = reinterpret_cast<long long*>(kc_dyn);
+  sm.pre = kc_dyn + kKcChunk;
+  sm.bin[0] = reinterpret_cast<int32_t*>(kc_dyn + 2 * kKcChunk);
+  sm.bin[1] = sm.bin[0] + kKcChunk;
+  sm.deg = reinterpret_cast<uint32_t*>(sm.bin[1] + kKcChunk);
   const uint32_t G = gridDim.x, rank = blockIdx.x, tid = threadIdx.x;
   const uint32_t lane = tid & 31;
   const int64_t n = a.n;
@@ -73,19 +250,20 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
     uint32_t mn = kUnset;
     for (int64_t v = (int64_t)rank * kKcBlock + tid; v < n; v += (int64_t)G * kKcBlock) {
       const int64_t d = a.off[v + 1] - a.off[v];
-      const uint32_t p = d >= (int64_t)kUnset ? kUnset - 1u : (uint32_t)d;
-      a.prio[v] = p;
+      const uint32_t pv = d >= (int64_t)kUnset ? kUnset - 1u : (uint32_t)d;
+      a.prio[v] = pv;
       a.core[v] = kUnset;
       a.pile[0][v] = (int32_t)v;
-      mn = min(mn, p);
+      mn = min(mn, pv);
     }
     mn = __reduce_min_sync(0xffffffffu, mn);
     if (lane == 0 && mn != kUnset) atomicMin(&ctl->kmin[0], mn);
   }
   dev::group_barrier(&ctl->bar, G);
 
-  unsigned long long nfin = 0, nedge = 0;     // per thread
-  unsigned long long buckets = 0, rounds = 0, phases = 0, empty = 0;  // rank 0 / thread 0
+  KcCtx c;
+  c.nfin = 0; c.nedge = 0;
+  unsigned long long buckets = 0, rounds = 0, phases = 0, empty = 0, subrounds = 0, spills = 0;
   uint32_t p = 0, j = 0, k = 0, prev = KC_DONE;
   for (;;) {
     if (tid == 0) {
@@ -95,14 +273,17 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
         if (__ldcg(&ctl->xfin[j % 3])) ++buckets; else ++empty;
       }
       const uint32_t qn = __ldcg(&ctl->qcount[p % 3]);
+      const uint32_t hn = __ldcg(&ctl->hcount[p % 3]);
       const uint32_t pc = __ldcg(&ctl->pcount[j % 3]);
       const uint32_t km = __ldcg(&ctl->kmin[j % 3]);
       uint32_t mode;
-      if (qn > 0) { mode = KC_ROUND; s.cnt = qn; }
+      s.hn = min(hn, a.hubcap);
+      if (qn > 0 || hn > 0) { mode = KC_ROUND; s.cnt = qn; }
       else if (pc > 0) { mode = KC_EXTRACT; s.cnt = pc; s.k = km; }
       else mode = KC_DONE;
       s.mode = mode;
       s.kmin = kUnset;
+      s.bincnt[0] = 0; s.bincnt[1] = 0;
     }
     __syncthreads();
     const uint32_t mode = s.mode;
@@ -111,6 +292,7 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
     if (mode == KC_EXTRACT) { ++j; k = s.k; }
     if (rank == 0 && tid == 0) {
       ctl->qcount[(p + 2) % 3] = 0;
+      ctl->hcount[(p + 2) % 3] = 0;
       ctl->qclaim[(p + 1) % 3] = 0;  // last used in phase p-2, which every CTA has left
       if (mode == KC_EXTRACT) {
         ctl->pcount[(j + 1) % 3] = 0; ctl->kmin[(j + 1) % 3] = kUnset; ctl->xfin[(j + 1) % 3] = 0;
@@ -118,10 +300,16 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
         ++rounds;
       }
     }
-    int32_t* q_next = (p & 1) ? a.q[0] : a.q[1];
-    uint32_t* qcount_next = &ctl->qcount[(p + 1) % 3];
+    c.k = k;
+    c.q_next = (p & 1) ? a.q[0] : a.q[1];
+    c.qcount_next = &ctl->qcount[(p + 1) % 3];
+    c.out = sm.bin[0];
+    c.outcnt = &s.bincnt[0];
+    c.hub_next = (p & 1) ? a.hub[0] : a.hub[1];
+    c.hcount_next = &ctl->hcount[(p + 1) % 3];
+    c.hubcap = a.hubcap;
+    c.my_kmin = kUnset;
     uint32_t* kmin_live = &ctl->kmin[j % 3];  // the min for the NEXT extraction
-    uint32_t my_kmin = kUnset;
 
     if (mode == KC_EXTRACT) {
       // dequeue_ready_set: the pile entries whose priority is <= k
@@ -130,24 +318,51 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
       uint32_t* pcount_live = &ctl->pcount[j % 3];
       const uint32_t lo = (uint32_t)(((uint64_t)cnt * rank) / G), hi = (uint32_t)(((uint64_t)cnt * (rank + 1)) / G);
       uint32_t nx = 0;
-      for (uint32_t i0 = lo; i0 < hi; i0 += kKcBlock) {  // warp-uniform trip count
-        const uint32_t i = i0 + tid;
-        const bool in = i < hi;
-        const int32_t v = in ? pile_src[i] : 0;
-        const uint32_t c = in ? ld_cg(a.core + v) : 0u;
-        const uint32_t pr = in ? ld_cg(a.prio + v) : 0u;
-        const bool live = in && c == kUnset;       // finished entries are dropped
-        const bool fin = live && pr <= k;
-        const bool keep = live && pr > k;
-        if (fin) { a.core[v] = k; ++nfin; ++nx; }
-        if (keep) my_kmin = min(my_kmin, pr);
-        kc_append(fin, v, q_next, qcount_next);
-        kc_append(keep, v, pile_live, pcount_live);
+      constexpr int X = 4;  // pile entries per thread per iteration, all loads in flight together
+      for (uint32_t i0 = lo; i0 < hi; i0 += X * kKcBlock) {  // warp-uniform trip count
+        int32_t v[X];
+        uint32_t cc[X], pr[X];
+#pragma unroll
+        for (int x = 0; x < X; ++x) {
+          const uint32_t i = i0 + x * kKcBlock + tid;
+          v[x] = i < hi ? pile_src[i] : -1;
+        }
+#pragma unroll
+        for (int x = 0; x < X; ++x) {
+          cc[x] = v[x] >= 0 ? ld_cg(a.core + v[x]) : 0u;
+          pr[x] = v[x] >= 0 ? ld_cg(a.prio + v[x]) : 0u;
+        }
+#pragma unroll
+        for (int x = 0; x < X; ++x) {
+          const bool live = v[x] >= 0 && cc[x] == kUnset;  // finished entries are dropped
+          const bool fin = live && pr[x] <= k;
+          const bool keep = live && pr[x] > k;
+          if (fin) { a.core[v[x]] = k; ++c.nfin; ++nx; }
+          if (keep) c.my_kmin = min(c.my_kmin, pr[x]);
+          kc_push(c, fin, v[x]);
+          kc_append(keep, v[x], pile_live, pcount_live);
+        }
       }
       nx = __reduce_add_sync(0xffffffffu, nx);
       if (lane == 0 && nx) atomicAdd(&ctl->xfin[j % 3], nx);
+      __syncthreads();
     } else {
-      // edges.from(frontier).applyUpdatePriority(apply_f)
+      // edges.from(frontier).applyUpdatePriority(apply_f). Hubs queued in
+      // the previous phase first: every CTA relaxes its 1/G slice of every hub's edges.
+      const uint32_t hn = s.hn;
+      const HubEnt* hub_in = (p & 1) ? a.hub[1] : a.hub[0];
+      for (uint32_t h0 = 0; h0 < hn; h0 += kKcChunk) {
+        const uint32_t nh = min((uint32_t)kKcChunk, hn - h0);
+        for (uint32_t i = tid; i < nh; i += kKcBlock) {
+          const HubEnt he = hub_in[h0 + i];
+          const uint64_t lo_e = (uint64_t)he.deg * rank / G, hi_e = (uint64_t)he.deg * (rank + 1) / G;
+          sm.beg[i] = he.beg + (long long)lo_e;
+          sm.deg[i] = (uint32_t)(hi_e - lo_e);
+        }
+        __syncthreads();
+        kc_relax_entries(a, s, sm, c, nh);
+      }
+      // then the global frontier in claimed chunks; crossings go to the local bin
       const int32_t* q_in = (p & 1) ? a.q[1] : a.q[0];
       const uint32_t claim = max(32u, min((uint32_t)kKcChunk, cnt / (4 * G)));
       const uint64_t first = (uint64_t)G * claim;
@@ -163,103 +378,8 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
         const uint32_t base = s.claim;
         if (base >= cnt) break;
         const uint32_t chunk = min(claim, cnt - base);
-        // stage (beg, deg) and block-scan the degrees
-        unsigned long long sum = 0;
-        constexpr int PER = kKcChunk / kKcBlock;
-        unsigned long long loc[PER];
-#pragma unroll
-        for (int x = 0; x < PER; ++x) {
-          const uint32_t i = tid * PER + x;
-          loc[x] = sum;
-          if (i < chunk) {
-            const int32_t v = q_in[base + i];
-            const long long b0 = a.off[v], b1 = a.off[v + 1];
-            sbeg[i] = b0;
-            sum += (unsigned long long)(b1 - b0);
-          }
-        }
-        unsigned long long incl = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= (uint32_t)o) incl += t;
-        }
-        if (lane == 31) s.red[tid >> 5] = incl;
-        __syncthreads();
-        if (tid < 32) {
-          const unsigned long long w = lane < kKcBlock / 32 ? s.red[lane] : 0ull;
-          unsigned long long wi = w;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long t = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= (uint32_t)o) wi += t;
-          }
-          if (lane < kKcBlock / 32) s.red[lane] = wi - w;
-          if (lane == kKcBlock / 32 - 1) s.total = wi;
-        }
-        __syncthreads();
-        const unsigned long long off0 = s.red[tid >> 5] + incl - sum;
-#pragma unroll
-        for (int x = 0; x < PER; ++x) {
-          const uint32_t i = tid * PER + x;
-          if (i < chunk) spre[i] = off0 + loc[x];
-        }
-        __syncthreads();
-        const unsigned long long total = s.total;
-        if (tid == 0) nedge += total;
-        for (unsigned long long k0 = 0; k0 < total; k0 += (unsigned long long)kKcEdges * kKcBlock) {
-          int32_t tv[kKcEdges];
-#pragma unroll
-          for (int u = 0; u < kKcEdges; ++u) tv[u] = -1;
-          const unsigned long long kt = k0 + (unsigned long long)kKcEdges * tid;
-          if (kt < total) {
-            uint32_t lo = 0, hi = chunk;  // last i with spre[i] <= kt
-            while (hi - lo > 1) {
-              const uint32_t mid = (lo + hi) >> 1;
-              if (spre[mid] <= kt) lo = mid; else hi = mid;
-            }
-            unsigned long long nxt = lo + 1 < chunk ? spre[lo + 1] : total;
-            long long rel = sbeg[lo] - (long long)spre[lo];
-#pragma unroll
-            for (int u = 0; u < kKcEdges; ++u) {
-              const unsigned long long e = kt + u;
-              if (e < total) {
-                while (e >= nxt) {  // next frontier vertex (skipping degree-0 ones)
-                  ++lo;
-                  rel = sbeg[lo] - (long long)nxt;
-                  nxt = lo + 1 < chunk ? spre[lo + 1] : total;
-                }
-                tv[u] = (int32_t)__ldg(&a.edges[rel + (long long)e].x);
-              }
-            }
-          }
-          // skip finished endpoints (coherent read; finished is final)
-          uint32_t cv[kKcEdges];
-#pragma unroll
-          for (int u = 0; u < kKcEdges; ++u) cv[u] = tv[u] >= 0 ? ld_cg(a.core + tv[u]) : 0u;
-#pragma unroll
-          for (int u = 0; u < kKcEdges; ++u) {
-            const bool want = tv[u] >= 0 && cv[u] == kUnset;
-            // constant-sum reduction: one atomic per distinct endpoint per warp
-            const uint32_t key = want ? (uint32_t)tv[u] : 0xFFFFFFFFu;
-            const uint32_t peers = __match_any_sync(0xffffffffu, key);
-            const bool leader = want && (__ffs(peers) - 1) == (int)lane;
-            bool cross = false;
-            if (leader) {
-              const uint32_t c = __popc(peers);
-              const uint32_t old = atomicSub(a.prio + tv[u], c);
-              if (old > k && old - c <= k) {
-                cross = true;  // this subtraction took the priority to <= k: finished at k
-                a.core[tv[u]] = k;
-              } else if (old > k) {
-                my_kmin = min(my_kmin, old - c);
-              }
-            }
-            nfin += cross;
-            kc_append(cross, tv[u], q_next, qcount_next);
-          }
-        }
-        __syncthreads();
+        kc_stage_vertices(a, sm, c, q_in + base, chunk);
+        kc_relax_entries(a, s, sm, c, chunk);
         if (tid == 0) {
           s.claim = dyn ? next : cnt;
           if (dyn && next < cnt) next = (uint32_t)first + atomicAdd(qclaim, claim);
@@ -268,10 +388,32 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
       }
     }
 
+    // bucket fusion (applied here to k-core's current bucket): drain
+    // the CTA-local bin while it stays below T, with CTA barriers only; a bin of >= T
+    // vertices goes to the global frontier (the next group-wide round)
+    for (uint32_t it = 1;; ++it) {
+      const uint32_t nin = min(s.bincnt[(it - 1) % 3], (uint32_t)kKcChunk);
+      const int32_t* in = sm.bin[(it - 1) & 1];
+      if (nin == 0) break;
+      if (nin >= kKcT) {
+        for (uint32_t i0 = 0; i0 < nin; i0 += kKcBlock) {
+          const uint32_t i = i0 + tid;
+          kc_append(i < nin, i < nin ? in[i] : 0, c.q_next, c.qcount_next);
+        }
+        if (tid == 0) ++spills;
+        break;
+      }
+      if (tid == 0) { s.bincnt[(it + 1) % 3] = 0; ++subrounds; }
+      c.out = sm.bin[it & 1];
+      c.outcnt = &s.bincnt[it % 3];
+      kc_stage_vertices(a, sm, c, in, nin);
+      kc_relax_entries(a, s, sm, c, nin);  // ends with a barrier
+    }
+
     // next k: the exact minimum priority of the unfinished vertices (kept entries and
     // every non-crossing decrement), warp min -> smem -> one global atomic per CTA
-    my_kmin = __reduce_min_sync(0xffffffffu, my_kmin);
-    if (lane == 0 && my_kmin != kUnset) atomicMin(&s.kmin, my_kmin);
+    const uint32_t km = __reduce_min_sync(0xffffffffu, c.my_kmin);
+    if (lane == 0 && km != kUnset) atomicMin(&s.kmin, km);
     __syncthreads();
     if (tid == 0 && s.kmin != kUnset) atomicMin(kmin_live, s.kmin);
     dev::group_barrier(&ctl->bar, G);
@@ -281,10 +423,12 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
   }
 
   // statistics
-  nfin = __reduce_add_sync(0xffffffffu, (unsigned)nfin) ;
-  if (lane == 0 && nfin) atomicAdd(&a.stats->vertices, nfin);
+  const unsigned nf = __reduce_add_sync(0xffffffffu, (unsigned)c.nfin);
+  if (lane == 0 && nf) atomicAdd(&a.stats->vertices, (unsigned long long)nf);
   if (tid == 0) {
-    if (nedge) atomicAdd(&a.stats->edges, nedge);
+    if (c.nedge) atomicAdd(&a.stats->edges, c.nedge);
+    if (subrounds) atomicAdd(&a.stats->subrounds, subrounds);
+    if (spills) atomicAdd(&a.stats->spills, spills);
     if (rank == 0) {
       a.stats->buckets = buckets; a.stats->rounds = rounds; a.stats->phases = phases + 1; a.stats->empty = empty;
     }
@@ -293,7 +437,7 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
 
 }  // namespace
 
-int kcore_smem_bytes() { return kKcChunk * (int)(sizeof(long long) + sizeof(unsigned long long)); }
+int kcore_smem_bytes() { return kKcChunk * (int)(sizeof(long long) + sizeof(unsigned long long) + 3 * sizeof(int32_t)); }
 
 cudaError_t kcore_occupancy(int* blocks_per_sm) {
   cudaError_t e = cudaFuncSetAttribute(kcore_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1,1 +1,2 @@
-timeout 1500 python -m pytest tests/ -x -q -m gpu -k "not config4" 2>&1 | tail -3
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "kcore" 2>&1 | tail -2
+for c in 2 3; do echo -n "kcore cfg$c: "; timeout 300 python bench.py --config $c --app kcore --steps 5 --warmup 3 2>&1 | tail -1 | python -c "import json,sys; j=json.loads(sys.stdin.read()); print(round(j['ms_per_step'],3), j['parity'], j['counters'])"; done
