@@ -56,6 +56,13 @@ namespace {
 
 enum : uint32_t { MODE_ROUND = 0, MODE_EXTRACT = 1, MODE_DONE = 2, MODE_NONE = 3, MODE_STOP = 4 };
 constexpr int kXtr = 4;  // far-pile entries per thread per extraction chunk
+// A/B switches for measurements only (tools/ab_time.py); all 0 in the product build
+#ifndef GI_X_NOPF
+#define GI_X_NOPF 0
+#endif
+#ifndef GI_X_NOSTALE
+#define GI_X_NOSTALE 0
+#endif
 #ifndef GI_BIGK
 #define GI_BIGK 8
 #endif
@@ -299,7 +306,6 @@ __device__ __forceinline__ void warp_append(uint32_t m, const int32_t (&v)[X], i
 template <typename Get>
 __device__ __forceinline__ void bulk_append(uint32_t n, Get get, uint32_t* bits, int32_t* list, uint32_t* count,
                                             const uint2* slots_pf) {
-  const uint32_t lane = threadIdx.x & 31;
   for (uint32_t base = 0; base < n; base += 4 * kBlock) {
     int32_t v[4];
     uint32_t old[4];
@@ -366,14 +372,20 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
   // classify the successful lowerings: current bucket (bin) or a future one (far pile).
   // A*: priority bucket of nd + h(v), raised to the current bucket if an inconsistent
   // heuristic would put it below (the monotone max(f + h, g[src]) of SPEC.md:355-358).
-  uint32_t hv[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) hv[k] = (c.h && (ok & (1u << k))) ? __ldg(c.h + e[k].x) : 0u;
   uint32_t curm = 0, farm = 0;
   uint32_t bk[K];
+  if (c.h) {  // uniform branch: SSSP / PPSP never pay for the heuristic
+    uint32_t hv[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) hv[k] = (ok & (1u << k)) ? __ldg(c.h + e[k].x) : 0u;
+#pragma unroll
+    for (int k = 0; k < K; ++k) bk[k] = max(prio_bucket(nd[k], hv[k], c.div), c.b);
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k) bk[k] = fdiv(nd[k], c.div);  // nd >= du >= bΔ: bk >= b
+  }
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    bk[k] = max(prio_bucket(nd[k], hv[k], c.div), c.b);
     if ((ok & (1u << k)) && nd[k] < old[k]) {
       if (bk[k] == c.b) curm |= 1u << k;
       else farm |= 1u << k;  // bk > b
@@ -399,7 +411,7 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
         if ((curm >> k) & 1u) {
           const uint32_t pos = base + pre[k] + __popc(mk[k] & lt);
           if (pos < (uint32_t)kBinCap) {
-            prefetch_own(c.slots + 8 * (size_t)e[k].x);
+            if (!GI_X_NOPF) prefetch_own(c.slots + 8 * (size_t)e[k].x);
             c.out[pos] = make_uint2(e[k].x, nd[k]);
           }
           else push_global(c, (int32_t)e[k].x);  // bin full: next group-wide round
@@ -508,7 +520,7 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
         if (e[u].x != kColEmpty) valid |= 1u << u;
       }
     }
-    const uint32_t stale = relax_batch<FUSED, U, LD>(c, e, du, valid, check_stale ? cur : nullptr);
+    const uint32_t stale = relax_batch<FUSED, U, LD>(c, e, du, valid, (check_stale && !GI_X_NOSTALE) ? cur : nullptr);
     // counters: non-stale entries and their edges (stale is per lane; each lane saw
     // its own probe of the same word)
     nv += __popc(heads & ~stale);
@@ -1392,6 +1404,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
   TRACE_FLUSH();
 }
 
+#if GI_PRIMARY
 __global__ void interleave_kernel(const int32_t* __restrict__ cols, const uint32_t* __restrict__ w,
                                   uint2* __restrict__ edges, int64_t count, int64_t n, uint32_t* bad) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
@@ -1448,6 +1461,8 @@ __global__ void validate_offsets_kernel(const int64_t* __restrict__ off, int64_t
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && (off[0] != 0 || off[n] != m)) atomicOr(bad, 1u);
 }
+
+#endif  // GI_PRIMARY
 
 }  // namespace
 
