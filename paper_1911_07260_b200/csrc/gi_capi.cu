@@ -66,6 +66,7 @@ struct Workspace {
   int srccap = 0;
   uint32_t* d_stage = nullptr;  // staging for host dist_out
   size_t stagecap = 0;
+  uint32_t* d_src_next = nullptr;  // batch source claim counter
   uint32_t* d_h = nullptr;      // staging for a host A* heuristic
   size_t hcap = 0;
   uint32_t* kc_prio = nullptr;  // k-core: priorities [n]
@@ -81,6 +82,7 @@ struct Workspace {
     if (d_srcs) cudaFree(d_srcs);
     if (d_stage) cudaFree(d_stage);
     if (d_h) cudaFree(d_h);
+    if (d_src_next) cudaFree(d_src_next);
     if (kc_prio) cudaFree(kc_prio);
     if (kc_ctl) cudaFree(kc_ctl);
     if (kc_stats) cudaFree(kc_stats);
@@ -351,6 +353,7 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   if ((e = cudaMemcpyAsync(w->d_srcs, hsrc.data(), sizeof(int32_t) * nsrc, cudaMemcpyHostToDevice, st)))
     return bail(e, "copy srcs");
   if ((e = cudaMemsetAsync(w->d_qstats, 0, sizeof(QStats) * nsrc, st))) return bail(e, "memset qstats");
+  if (!w->d_src_next && (e = cudaMalloc(&w->d_src_next, sizeof(uint32_t)))) return bail(e, "alloc claim counter");
 
   KArgs a;
   a.slots = g->d_slots;
@@ -375,6 +378,8 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   a.pre_read = opt.pre_read == 1 ? 1u : opt.pre_read == 2 ? 0u : (g->max_deg > 32 ? 1u : 0u);
   a.target = target;
   a.dyn_claim = g->max_deg > 32 ? 1u : 0u;
+  if ((e = cudaMemsetAsync(w->d_src_next, 0, sizeof(uint32_t), st))) return bail(e, "init claim counter");
+  a.src_next = w->d_src_next;  // claims count from 0; sources 0..ngroups-1 are taken statically
   a.h = d_h;
 
   if ((e = cudaEventRecord(w->ev0, st))) return bail(e, "event");

@@ -71,7 +71,8 @@ struct alignas(128) Ctl {
   uint32_t hcount[3];   // group hub-list sizes, by phase mod 3
   uint32_t qclaim[3];   // ROUND phases: next unclaimed global-frontier position, by phase mod 3
   uint32_t tdist[3];    // PPSP: min over CTAs of dist[target] read at the phase end, by phase mod 3
-  uint32_t pad0[7];
+  int32_t next_si;      // batch: the source index this group runs next (claimed by its CTA 0)
+  uint32_t pad0[6];
   uint32_t bar;         // group barrier: arrivals (low 16 bits) | generation (high 16), own 128 B line
   uint32_t pad1[31];
 };
@@ -122,6 +123,7 @@ struct KArgs {
   int32_t target;       // PPSP: stop once the next bucket's lower bound reaches dist[target]; -1 = SSSP
   uint32_t dyn_claim;   // ROUND phases claim frontier chunks dynamically (skewed degrees) vs equal slices
   const uint32_t* h;    // A*: per-vertex heuristic (priority = dist + h); nullptr = 0 (SSSP / PPSP)
+  uint32_t* src_next;   // batch: claims so far (source index = ngroups + claim)
 };
 
 // k-core (gi_kcore.cu): control block, statistics and arguments.

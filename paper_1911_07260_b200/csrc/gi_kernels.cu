@@ -1002,7 +1002,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
   const uint32_t T = a.T;
   TRACE_INIT();
 
-  for (int32_t si = (int32_t)gid; si < a.nsrc; si += a.ngroups) {
+  // Batch: each group runs one query at a time; after the first (static: source gid) it
+  // CLAIMS the next source, so that groups that drew cheap sources run more of them.
+  for (int32_t si = (int32_t)gid; si < a.nsrc;) {
     uint32_t* dist = a.dist + (size_t)si * (size_t)n;
     const int32_t src = a.srcs[si];
 
@@ -1399,7 +1401,12 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
         q->critical_subrounds = critical;
       }
     }
+    if (rank == 0 && tid == 0) ctl->next_si = a.ngroups + (int32_t)atomicAdd(a.src_next, 1u);
     group_barrier(ctl, G);  // the next query re-initialises ctl
+    if (tid == 0) s.cnt = (uint32_t)__ldcg(&ctl->next_si);
+    __syncthreads();
+    si = (int32_t)s.cnt;
+    __syncthreads();  // s.cnt is rewritten by the next query's first decision
   }
   TRACE_FLUSH();
 }
