@@ -217,8 +217,9 @@ __device__ __forceinline__ void kc_relax_entries(const KcArgs& a, KcShared& s, c
         const uint32_t cntp = __popc(peers);
         const uint32_t old = atomicSub(a.prio + tv[u], cntp);
         if (old > k && old - cntp <= k) {
-          cross = true;  // this subtraction took the priority to <= k: finished at k
-          a.core[tv[u]] = k;
+          // this subtraction took the priority to <= k: finished at k — claimed with a CAS,
+          // since another CTA's extraction scan (same phase) may see the lowered priority
+          cross = atomicCAS(a.core + tv[u], kUnset, k) == kUnset;
         } else if (old > k) {
           c.my_kmin = min(c.my_kmin, old - cntp);
         }
@@ -335,9 +336,11 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
 #pragma unroll
         for (int x = 0; x < X; ++x) {
           const bool live = v[x] >= 0 && cc[x] == kUnset;  // finished entries are dropped
-          const bool fin = live && pr[x] <= k;
+          // a vertex is finished exactly once (its edges are decrements, not idempotent):
+          // the extraction and a concurrent crossing in another CTA's drain race for it
+          const bool fin = live && pr[x] <= k && atomicCAS(a.core + v[x], kUnset, k) == kUnset;
           const bool keep = live && pr[x] > k;
-          if (fin) { a.core[v[x]] = k; ++c.nfin; ++nx; }
+          if (fin) { ++c.nfin; ++nx; }
           if (keep) c.my_kmin = min(c.my_kmin, pr[x]);
           kc_push(c, fin, v[x]);
           kc_append(keep, v[x], pile_live, pcount_live);

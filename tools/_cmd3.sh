@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "batch or host_output or config5 or hand" 2>&1 | tail -2
-for gc in 9 16 18; do echo -n "cfg5 gc$gc: "; timeout 300 python bench.py --config 5 --group-ctas $gc --steps 2 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; j=json.loads(sys.stdin.read()); print(round(j['ms_per_step'],2), round(j['value'],2), j['counters']['groups'])"; done
+for i in 1 2 3; do timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "kcore" 2>&1 | tail -1; done
+for c in 2 3; do echo -n "kcore cfg$c: "; timeout 300 python bench.py --config $c --app kcore --steps 10 --warmup 3 2>&1 | tail -1 | python -c "import json,sys; j=json.loads(sys.stdin.read()); print(round(j['ms_per_step'],3), j['parity'])"; done
