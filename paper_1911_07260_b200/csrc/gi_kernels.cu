@@ -55,7 +55,10 @@ namespace gi {
 namespace {
 
 enum : uint32_t { MODE_ROUND = 0, MODE_EXTRACT = 1, MODE_DONE = 2, MODE_NONE = 3, MODE_STOP = 4 };
-constexpr int kXtr = 4;  // far-pile entries per thread per extraction chunk
+#ifndef GI_XTR
+#define GI_XTR 4
+#endif
+constexpr int kXtr = GI_XTR;  // far-pile entries per thread per extraction chunk
 // A/B switches for measurements only (tools/ab_time.py); all 0 in the product build
 #ifndef GI_X_NOPF
 #define GI_X_NOPF 0
@@ -71,6 +74,12 @@ constexpr int kBigK = GI_BIGK;  // stage B: consecutive edges per thread per ite
 #define GI_CLAIMS 4
 #endif
 constexpr uint32_t kClaimsPerCta = GI_CLAIMS;  // ROUND: ~claims per CTA per phase (chunk size)
+#ifndef GI_MAXCLAIM
+#define GI_MAXCLAIM 2048
+#endif
+// largest claim (= kBinCap, the staging size). Smaller caps (256, 512) were measured
+// slower on configs 3-4 (more chunk passes), despite smaller straggler chunks
+constexpr uint32_t kMaxClaim = GI_MAXCLAIM;
   // drain: spill a bin's big list above this
 
 #ifdef GI_TRACE
@@ -1250,7 +1259,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
         // frontier costs no atomic. Otherwise: equal static slices (one pass per CTA,
         // every CTA busy — the latency-bound rounds of road graphs).
         uint2* stage = s_dyn + kBinCap;
-        const uint32_t claim = a.dyn_claim ? max(32u, min((uint32_t)kBinCap, cnt / (kClaimsPerCta * G)))
+        const uint32_t claim = a.dyn_claim ? max(32u, min((uint32_t)kMaxClaim, cnt / (kClaimsPerCta * G)))
                                            : (uint32_t)kBinCap;
         const uint64_t first = a.dyn_claim ? (uint64_t)G * claim : (uint64_t)cnt;
         const bool dyn = first < cnt;

@@ -38,6 +38,8 @@ drain = sys.argv[3] if len(sys.argv) > 3 else "async"
 max_ctas = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 if what == "path":
     g = gen.path(20000); src_v = 0; delta = delta or 10**9
+elif what == "cfg4":
+    g = gen.config_graph(4); src_v = gen.config_source(4, g); delta = delta or 2
 elif what == "cfg3":
     g = gen.config_graph(3); src_v = gen.config_source(3, g); delta = delta or 1
 elif what == "cfg1":
@@ -53,6 +55,7 @@ out = torch.empty(g.n, dtype=torch.int32, device="cuda")
 opt = gi_options()
 lib.gi_options_default(ctypes.byref(opt))
 opt.max_ctas = max_ctas
+opt.cta_threads = 512  # the trace buffers live in the primary (512-thread) build
 opt.drain = {"async": 2, "bsp": 1, "unfused": 1}[drain]
 opt.fusion = 0 if drain == "unfused" else 1
 st = gi_stats()
