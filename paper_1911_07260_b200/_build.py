@@ -34,6 +34,7 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return SO
     nvcc = os.environ.get("NVCC", "nvcc")
+    # -lineinfo: ncu source correlation; measured neutral on every config
     base = [nvcc, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
     if verbose:
         base.insert(1, "-Xptxas=-v")

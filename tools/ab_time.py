@@ -6,15 +6,7 @@ import numpy as np
 import gen
 import torch
 
-class Opt(ctypes.Structure):
-    _fields_ = [("struct_size", ctypes.c_uint32), ("fusion", ctypes.c_int32), ("fusion_threshold", ctypes.c_uint32),
-                ("max_ctas", ctypes.c_int32), ("hub_min", ctypes.c_uint32), ("drain", ctypes.c_uint32),
-                ("group_ctas", ctypes.c_int32), ("pre_read", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p)]
-class St(ctypes.Structure):
-    _fields_ = [(k, ctypes.c_uint64) for k in ("buckets", "rounds", "grid_syncs", "kernel_launches", "fused_subrounds",
-                "spills", "vertices_processed", "edges_relaxed", "empty_extractions", "far_scanned", "critical_subrounds")] + \
-               [("gpu_ms", ctypes.c_float), ("ctas", ctypes.c_int32), ("tpc", ctypes.c_int32), ("groups", ctypes.c_int32),
-                ("kind", ctypes.c_int32), ("pad", ctypes.c_int32 * 8)]
+from paper_1911_07260_b200.gi import gi_options as Opt, gi_stats as St  # noqa: E402 (struct layouts only)
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 delta = int(sys.argv[2]) if len(sys.argv) > 2 else 32768
 g = gen.config_graph(cfg)
@@ -36,5 +28,6 @@ for so in sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__
             assert lib.gi_sssp_delta_ex(h, src, delta, ctypes.byref(o), out.data_ptr(), ctypes.byref(st)) == 0
             ts.append(st.gpu_ms)
         res.append(round(float(np.median(ts[2:])), 3))
-    print(os.path.basename(so), "fused/unfused ms", res, flush=True)
+    print(os.path.basename(so), "fused/unfused ms", res, "ctas", st.ctas, "threads", st.threads_per_cta, "kind",
+          st.kernel_kind, "rounds", st.rounds, "spills", st.spills, "edges", st.edges_relaxed, flush=True)
     lib.gi_graph_destroy(h)
