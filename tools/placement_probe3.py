@@ -1,0 +1,43 @@
+"""Placement effect on config 4, part 3 (one library): which allocation order makes the
+query fast? Each mode builds the graph, the output and the workspace in a different order."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import gen
+from paper_1911_07260_b200 import gi
+
+g = gen.config_graph(4)
+src = gen.config_source(4, g)
+
+
+def timed(G, out, reps=4):
+    ts = []
+    for _ in range(reps):
+        _, st = gi.sssp(G, src, 2, out=out)
+        ts.append(st["gpu_ms"])
+    return round(float(np.median(ts[1:])), 2)
+
+
+mode = sys.argv[1]
+if mode == "out_first":       # output tensor, then graph (the bench order)
+    out = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    G = gi.Graph.from_csr(g)
+    print(mode, timed(G, out))
+elif mode == "graph_first":   # graph, then output
+    G = gi.Graph.from_csr(g)
+    out = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    print(mode, timed(G, out))
+elif mode == "recreate":      # graph, destroy, graph again; output after
+    G = gi.Graph.from_csr(g)
+    G.close()
+    G = gi.Graph.from_csr(g)
+    out = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    print(mode, timed(G, out))
+elif mode == "warm_small":    # a small query first (context, module, workspace pool warm)
+    t = gen.config_graph(1)
+    T = gi.Graph.from_csr(t)
+    gi.sssp(T, 0, 1000)
+    G = gi.Graph.from_csr(g)
+    out = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    print(mode, timed(G, out))
