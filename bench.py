@@ -389,6 +389,16 @@ def main():
                 "note": "latency/sync-bound on road graphs: see DESIGN.md sync floor"}
 
     s_last = stats[-1] if cfg != 5 else stats[-1][0]
+    # the dependent chain that bounds road graphs: levels a CTA had to run
+    # one after another, the time per level, and the bare hop (atomicMin ∥ slot load,
+    # tools/hop_bench.cu: ~650 cycles = 0.33 µs at 1,965 MHz) as its floor
+    chain = None
+    if cfg != 5 and s_last.critical_subrounds:
+        hop_us = 650 / 1965.0
+        chain = {"critical_subrounds": s_last.critical_subrounds, "phases": s_last.grid_syncs,
+                 "us_per_level": kms * 1e3 / s_last.critical_subrounds, "hop_floor_us": hop_us,
+                 "chain_floor_ms": s_last.critical_subrounds * hop_us / 1e3,
+                 "frac_of_chain_floor": (s_last.critical_subrounds * hop_us / 1e3) / kms}
     counters = {k: getattr(s_last, k) for k in ("buckets", "rounds", "grid_syncs", "kernel_launches",
                                                   "fused_subrounds", "spills", "vertices_processed",
                                                   "edges_relaxed", "empty_extractions", "far_scanned", "critical_subrounds",
@@ -452,7 +462,7 @@ def main():
                    "graph_upload_s": t_upload},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
-        "clocks": clocks, "counters": counters, "fusion_compare": compare,
+        "clocks": clocks, "counters": counters, "fusion_compare": compare, "chain": chain,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
