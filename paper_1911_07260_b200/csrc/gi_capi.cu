@@ -100,12 +100,27 @@ struct gi_graph {
   int64_t* d_off = nullptr;
   uint2* d_edges = nullptr;
   uint2* d_slots = nullptr;  // ELL adjacency slots, 64 B per vertex
+  void* d_arena = nullptr;   // one allocation holding offsets, edges and slots (2 MB-aligned parts)
   uint32_t max_deg = 0;
   int sm_count = 0;
   int bps[2][KIND_COUNT] = {};  // co-resident CTAs per SM, by width (512, 1024) and KernelKind
   int bps_kcore = 0;
   std::mutex mu;
   std::vector<std::unique_ptr<Workspace>> pool;
+
+  // device memory is released here, so that every early error return of gi_graph_create
+  // (the unique_ptr going out of scope) frees what was allocated; the caller's current
+  // device is the graph's (DeviceGuard) wherever this runs
+  ~gi_graph() {
+    pool.clear();
+    if (d_arena) {
+      cudaFree(d_arena);
+    } else {
+      if (d_off) cudaFree(d_off);
+      if (d_edges) cudaFree(d_edges);
+      if (d_slots) cudaFree(d_slots);
+    }
+  }
 };
 
 namespace {
@@ -482,14 +497,27 @@ gi_status gi_graph_create(int64_t n, int64_t m, const int64_t* row_offsets, cons
   GI_CUDA(cudaMemsetAsync(d_bad, 0, 4, st), "memset");
 
   bool wrong = false;
-  GI_CUDA(cudaMalloc(&g->d_off, sizeof(int64_t) * (n + 1)), "alloc offsets");
+  // offsets, edges and slots in ONE allocation (2 MB-aligned parts; GI_ARENA=0 disables)
+  const char* arena_env = getenv("GI_ARENA");
+  const bool arena = !(arena_env && arena_env[0] == '0');
+  auto up2m = [](size_t b) { return (b + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1); };
+  const size_t b_off = up2m(sizeof(int64_t) * (n + 1)), b_edges = up2m(sizeof(uint2) * (m > 0 ? m : 1)),
+               b_slots = up2m(sizeof(uint2) * 8 * (size_t)n);
+  if (arena) {
+    GI_CUDA(cudaMalloc(&g->d_arena, b_off + b_edges + b_slots), "alloc graph arena");
+    g->d_off = reinterpret_cast<int64_t*>(g->d_arena);
+    g->d_edges = reinterpret_cast<uint2*>(reinterpret_cast<char*>(g->d_arena) + b_off);
+    g->d_slots = reinterpret_cast<uint2*>(reinterpret_cast<char*>(g->d_arena) + b_off + b_edges);
+  } else {
+    GI_CUDA(cudaMalloc(&g->d_off, sizeof(int64_t) * (n + 1)), "alloc offsets");
+  }
   const bool off_dev = is_device_ptr(row_offsets, device, &wrong);
   if (wrong) return fail(GI_ERR_INVALID_ARGUMENT, "row_offsets on another device");
   GI_CUDA(cudaMemcpyAsync(g->d_off, row_offsets, sizeof(int64_t) * (n + 1),
                           off_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st), "copy offsets");
   GI_CUDA(launch_validate_offsets(g->d_off, n, m, d_bad, st), "validate offsets");
 
-  GI_CUDA(cudaMalloc(&g->d_edges, sizeof(uint2) * (m > 0 ? m : 1)), "alloc edges");
+  if (!arena) GI_CUDA(cudaMalloc(&g->d_edges, sizeof(uint2) * (m > 0 ? m : 1)), "alloc edges");
   if (m > 0) {
     const bool c_dev = is_device_ptr(col_idx, device, &wrong);
     if (wrong) return fail(GI_ERR_INVALID_ARGUMENT, "col_idx on another device");
@@ -521,7 +549,7 @@ gi_status gi_graph_create(int64_t n, int64_t m, const int64_t* row_offsets, cons
   GI_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st), "copy flag");
   GI_CUDA(cudaStreamSynchronize(st), "graph validation");
   if (!bad) {
-    GI_CUDA(cudaMalloc(&g->d_slots, sizeof(uint2) * 8 * (size_t)n), "alloc slots");
+    if (!arena) GI_CUDA(cudaMalloc(&g->d_slots, sizeof(uint2) * 8 * (size_t)n), "alloc slots");
     GI_CUDA(launch_build_slots(g->d_off, g->d_edges, g->d_slots, n, st), "build slots");
     uint32_t* d_maxdeg = d_bad;  // reuse the flag word
     GI_CUDA(cudaMemsetAsync(d_maxdeg, 0, 4, st), "memset");
@@ -529,9 +557,7 @@ gi_status gi_graph_create(int64_t n, int64_t m, const int64_t* row_offsets, cons
     GI_CUDA(cudaMemcpyAsync(&g->max_deg, d_maxdeg, 4, cudaMemcpyDeviceToHost, st), "copy max degree");
     GI_CUDA(cudaStreamSynchronize(st), "graph build");
   }
-  if (bad) {
-    cudaFree(g->d_off);
-    cudaFree(g->d_edges);
+  if (bad) {  // ~gi_graph frees the device memory
     return fail(GI_ERR_INVALID_GRAPH, "offsets not a valid CSR (offsets[0]=0, non-decreasing, offsets[n]=m) "
                                       "or a column id outside [0, n)");
   }
@@ -543,12 +569,8 @@ void gi_graph_destroy(gi_graph* g) {
   if (!g) return;
   {
     DeviceGuard dg(g->device);
-    g->pool.clear();
-    cudaFree(g->d_off);
-    cudaFree(g->d_edges);
-    cudaFree(g->d_slots);
+    delete g;
   }
-  delete g;
 }
 
 gi_status gi_graph_info(const gi_graph* g, int64_t* n, int64_t* m, int32_t* device) {
