@@ -203,7 +203,8 @@ def run_kcore(args, g, G, opts, rank, world):
             "cpu_baseline": {"value": g.m / t_or / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"one serial peel (oracle/oracle.c), {t_or:.3f} s"},
             "counters": {k: getattr(st, k) for k in ("buckets", "rounds", "grid_syncs", "vertices_processed",
-                                                      "edges_relaxed", "empty_extractions", "kernel_kind")}}
+                                                      "edges_relaxed", "empty_extractions", "fused_subrounds",
+                                                      "spills", "kernel_kind")}}
     print(json.dumps(line), flush=True)
     return 0 if line["parity"] else 1
 
