@@ -205,23 +205,29 @@ __device__ __forceinline__ void kc_relax_entries(const KcArgs& a, KcShared& s, c
     uint32_t cv[kKcEdges];
 #pragma unroll
     for (int u = 0; u < kKcEdges; ++u) cv[u] = tv[u] >= 0 ? ld_cg(a.core + tv[u]) : 0u;
+    // constant-sum reduction: one atomic per distinct endpoint per warp; all 8 atomics
+    // of a thread in flight together, then the crossings
+    uint32_t lead = 0, cntp[kKcEdges], old[kKcEdges];
 #pragma unroll
     for (int u = 0; u < kKcEdges; ++u) {
       const bool want = tv[u] >= 0 && cv[u] == kUnset;
-      // constant-sum reduction: one atomic per distinct endpoint per warp
       const uint32_t key = want ? (uint32_t)tv[u] : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, key);
-      const bool leader = want && (__ffs(peers) - 1) == (int)lane;
+      cntp[u] = __popc(peers);
+      if (want && (__ffs(peers) - 1) == (int)lane) lead |= 1u << u;
+    }
+#pragma unroll
+    for (int u = 0; u < kKcEdges; ++u) old[u] = (lead & (1u << u)) ? atomicSub(a.prio + tv[u], cntp[u]) : 0u;
+#pragma unroll
+    for (int u = 0; u < kKcEdges; ++u) {
       bool cross = false;
-      if (leader) {
-        const uint32_t cntp = __popc(peers);
-        const uint32_t old = atomicSub(a.prio + tv[u], cntp);
-        if (old > k && old - cntp <= k) {
+      if (lead & (1u << u)) {
+        if (old[u] > k && old[u] - cntp[u] <= k) {
           // this subtraction took the priority to <= k: finished at k — claimed with a CAS,
           // since another CTA's extraction scan (same phase) may see the lowered priority
           cross = atomicCAS(a.core + tv[u], kUnset, k) == kUnset;
-        } else if (old > k) {
-          c.my_kmin = min(c.my_kmin, old - cntp);
+        } else if (old[u] > k) {
+          c.my_kmin = min(c.my_kmin, old[u] - cntp[u]);
         }
       }
       c.nfin += cross;
