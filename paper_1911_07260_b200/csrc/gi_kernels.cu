@@ -67,7 +67,11 @@ constexpr int kXtr = GI_XTR;  // far-pile entries per thread per extraction chun
 #define GI_X_NOSTALE 0
 #endif
 #ifndef GI_BIGK
+#if GI_BLOCK >= 1024
+#define GI_BIGK 4  // 64 registers per thread at 1024 threads: fewer edges in flight per thread, less spill
+#else
 #define GI_BIGK 8
+#endif
 #endif
 constexpr int kBigK = GI_BIGK;  // stage B: consecutive edges per thread per iteration
 #ifndef GI_CLAIMS
