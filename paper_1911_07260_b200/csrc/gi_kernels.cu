@@ -59,6 +59,8 @@ enum : uint32_t { MODE_ROUND = 0, MODE_EXTRACT = 1, MODE_DONE = 2, MODE_NONE = 3
 #define GI_XTR 4
 #endif
 constexpr int kXtr = GI_XTR;  // far-pile entries per thread per extraction chunk
+constexpr int kFarSeg = kFarStage / (kBlock / 32);  // bsp: far staging entries per warp
+static_assert(kFarSeg >= 32 * 8, "a warp's far segment must hold one relax batch (32 lanes x 8 edges)");
 // A/B switches for measurements only (tools/ab_time.py); all 0 in the product build
 #ifndef GI_X_NOPF
 #define GI_X_NOPF 0
@@ -189,7 +191,8 @@ struct BigEnt {
 struct Shared {
   uint32_t cnt3[3];         // current-bucket bin fills, rotating by sub-round
   uint32_t bigtail;         // fill of the high-degree list
-  uint32_t farcnt;          // fill of the far staging buffer
+  uint32_t farcnt;          // fill of the far staging buffer (async drain: one CTA-wide region)
+  uint32_t wfar[kBlock / 32];  // bsp kernels: fill of each warp's segment of the far staging
   uint32_t mode, b, cnt, hn;
   uint32_t claim;           // ROUND: base of the chunk this CTA claimed
   uint32_t redw[kBlock / 32];  // EXTRACT: per-warp exclusive offsets of kept far entries
@@ -337,6 +340,30 @@ __device__ __forceinline__ void bulk_append(uint32_t n, Get get, uint32_t* bits,
   }
 }
 
+// A warp's segment of the far staging is full (or the phase ends): dedup-append its n
+// entries (atomicOr of 4 per lane in flight, one append atomic per 128 entries). Only this
+// warp touches its segment, so no CTA barrier is needed mid-phase.
+__device__ __forceinline__ void warp_flush_far(Ctx& c, const int32_t* seg, uint32_t n) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t base = 0; base < n; base += 4 * 32) {
+    int32_t v[4];
+    uint32_t old[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const uint32_t i = base + x * 32 + lane;
+      v[x] = i < n ? seg[i] : -1;
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x) old[x] = v[x] >= 0 ? atomicOr(&c.farbits[v[x] >> 5], 1u << (v[x] & 31)) : ~0u;
+    uint32_t newm = 0;
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      if (v[x] >= 0 && !(old[x] & (1u << (v[x] & 31)))) newm |= 1u << x;
+    warp_append(newm, v, c.far_live, c.fcount_live, nullptr);
+  }
+  __syncwarp();
+}
+
 // Relax K edges per thread (u -> e[k].x, weight e[k].y, from du[k]); lanes with
 // bit k of `valid` clear do nothing. Every load and atomic of the batch is issued
 // before any result is consumed (memory-level parallelism on the critical chain).
@@ -445,18 +472,24 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
       tot += __popc(mk[k]);
     }
     if (tot) {
-      uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(&c.s->farcnt, tot);
-      base = __shfl_sync(0xffffffffu, base, 0);
+      // this warp's segment of the far staging; flushed by the warp itself when full
+      const uint32_t warp = threadIdx.x >> 5;
+      int32_t* seg = c.farstage + warp * kFarSeg;
+      uint32_t base = c.s->wfar[warp];
+      if (base + tot > (uint32_t)kFarSeg) {  // warp-uniform
+        warp_flush_far(c, seg, base);
+        base = 0;
+      }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         if ((farm >> k) & 1u) {
           c.my_fmin = min(c.my_fmin, bk[k]);
-          const uint32_t pos = base + pre[k] + __popc(mk[k] & lt);
-          if (pos < (uint32_t)kFarStage) c.farstage[pos] = (int32_t)e[k].x;
-          else push_far_global(c, (int32_t)e[k].x);
+          seg[base + pre[k] + __popc(mk[k] & lt)] = (int32_t)e[k].x;
         }
       }
+      __syncwarp();
+      if (lane == 0) c.s->wfar[warp] = base + tot;
+      __syncwarp();
     }
   }
   return stale;
@@ -1109,6 +1142,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
         s.cnt3[1] = 0;
         s.bigtail = 0;
         s.farcnt = 0;
+        for (int w = 0; w < kBlock / 32; ++w) s.wfar[w] = 0;
         s.fmin = kInf;
         if constexpr (ASYNC) {
           s.head = 0; s.tail = 0; s.done = 0u - (uint32_t)(kBlock / 32); s.maxdep = 0; s.spilled = 0;
@@ -1344,9 +1378,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
       __syncthreads();
       TRACE(7);
       {
-        const uint32_t nf = min(s.farcnt, (uint32_t)kFarStage);
-        const int32_t* fs = c.farstage;
-        bulk_append(nf, [&](uint32_t i) { return fs[i]; }, c.farbits, c.far_live, c.fcount_live, nullptr);
+        if constexpr (ASYNC) {
+          const uint32_t nf = min(s.farcnt, (uint32_t)kFarStage);
+          const int32_t* fs = c.farstage;
+          bulk_append(nf, [&](uint32_t i) { return fs[i]; }, c.farbits, c.far_live, c.fcount_live, nullptr);
+        } else {  // each warp flushes its own segment
+          const uint32_t w = tid >> 5;
+          warp_flush_far(c, c.farstage + w * kFarSeg, s.wfar[w]);
+        }
         uint32_t fm = __reduce_min_sync(0xffffffffu, c.my_fmin);
         if ((tid & 31) == 0 && fm != kInf) atomicMin(&s.fmin, fm);
         __syncthreads();

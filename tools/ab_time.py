@@ -12,7 +12,7 @@ delta = int(sys.argv[2]) if len(sys.argv) > 2 else 32768
 g = gen.config_graph(cfg)
 src = gen.config_source(cfg, g)
 out = torch.empty(g.n, dtype=torch.int32, device="cuda")
-for so in sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "ab", "libgi_*.so"))):
+for so in sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ.get("AB_DIR", "ab"), "libgi_*.so"))):
     lib = ctypes.CDLL(so)
     vp = ctypes.c_void_p
     lib.gi_graph_create.argtypes = [ctypes.c_int64, ctypes.c_int64, vp, vp, vp, ctypes.c_int, ctypes.POINTER(vp)]
