@@ -252,23 +252,6 @@ __device__ __forceinline__ void push_global(Ctx& c, int32_t v) {
   }
 }
 
-// Current-bucket push: CTA-local ring (fusion) or the global frontier.
-template <bool FUSED>
-__device__ __forceinline__ void push_cur(Ctx& c, int32_t v, uint32_t d) {
-  if constexpr (FUSED) {
-    prefetch_own(c.slots + 8 * (size_t)v);
-    cg::coalesced_group g = cg::coalesced_threads();
-    uint32_t base = 0;
-    if (g.thread_rank() == 0) base = atomicAdd(c.outcnt, g.size());
-    base = g.shfl(base, 0);
-    const uint32_t pos = base + g.thread_rank();
-    if (pos < (uint32_t)kBinCap) c.out[pos] = make_uint2((uint32_t)v, d);
-    else push_global(c, v);  // bin full: the vertex goes to the next group-wide round
-  } else {
-    push_global(c, v);
-  }
-}
-
 // Far-pile append, deduplicated: one live entry per vertex.
 __device__ __forceinline__ void push_far_global(Ctx& c, int32_t v) {
   const uint32_t bit = 1u << (v & 31);
@@ -1245,19 +1228,54 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
 #pragma unroll
           for (int x = 0; x < kXtr; ++x) d[x] = v[x] >= 0 ? ld_dist(dist + v[x]) : kInf;
           uint32_t keepm = 0;
+          uint32_t livem = 0;
 #pragma unroll
           for (int x = 0; x < kXtr; ++x) {
             if (v[x] < 0) continue;
             const uint32_t bk = prio_bucket(d[x], c.h ? __ldg(c.h + v[x]) : 0u, c.div);
             if (bk <= b) {
               atomicAnd(&ws.farbits[v[x] >> 5], ~(1u << (v[x] & 31)));
-              if (bk == b) { ++nlive; push_cur<FUSED>(c, v[x], d[x]); }  // else: stale (settled)
+              if (bk == b) { ++nlive; livem |= 1u << x; }  // else: stale (already settled)
             } else {
               c.my_fmin = min(c.my_fmin, bk);
               keepm |= 1u << x;
             }
           }
           warp_append(keepm, v, c.far_live, c.fcount_live, nullptr);
+          // the extracted vertices: the CTA bin (fusion) while it has room, else — and
+          // without fusion — the global frontier, deduplicated with all atomics in flight
+          uint32_t ovm = FUSED ? 0u : livem;
+          if constexpr (FUSED) {
+            const uint32_t lane = tid & 31;
+#pragma unroll
+            for (int x = 0; x < kXtr; ++x) {
+              const uint32_t m = __ballot_sync(0xffffffffu, (livem >> x) & 1u);
+              if (!m) continue;
+              uint32_t base = 0;
+              if (lane == 0) base = atomicAdd(c.outcnt, (uint32_t)__popc(m));
+              base = __shfl_sync(0xffffffffu, base, 0);
+              if ((livem >> x) & 1u) {
+                const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
+                if (pos < (uint32_t)kBinCap) {
+                  prefetch_own(c.slots + 8 * (size_t)v[x]);
+                  c.out[pos] = make_uint2((uint32_t)v[x], d[x]);
+                } else {
+                  ovm |= 1u << x;
+                }
+              }
+            }
+          }
+          if (__any_sync(0xffffffffu, ovm != 0)) {
+            uint32_t old[kXtr];
+#pragma unroll
+            for (int x = 0; x < kXtr; ++x)
+              old[x] = ((ovm >> x) & 1u) ? atomicOr(&c.qbits_next[v[x] >> 5], 1u << (v[x] & 31)) : ~0u;
+            uint32_t newm = 0;
+#pragma unroll
+            for (int x = 0; x < kXtr; ++x)
+              if (((ovm >> x) & 1u) && !(old[x] & (1u << (v[x] & 31)))) newm |= 1u << x;
+            warp_append(newm, v, c.q_next, c.qcount_next, c.slots);
+          }
         }
         TRACE(6);
         const uint32_t tl = block_sum(nlive, s);  // ends with a barrier: ring fill is final
