@@ -417,6 +417,7 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
   // warp-aggregated appends: one ballot per item slot, one shared atomic per warp
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
+  uint32_t ovm = FUSED ? 0u : curm;  // current-bucket pushes bound for the global frontier
   if constexpr (FUSED) {
     uint32_t mk[K], pre[K], tot = 0;
 #pragma unroll
@@ -436,15 +437,26 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
           if (pos < (uint32_t)kBinCap) {
             if (!GI_X_NOPF) prefetch_own(c.slots + 8 * (size_t)e[k].x);
             c.out[pos] = make_uint2(e[k].x, nd[k]);
+          } else {
+            ovm |= 1u << k;  // bin full: next group-wide round
           }
-          else push_global(c, (int32_t)e[k].x);  // bin full: next group-wide round
         }
       }
     }
-  } else {
+  }
+  if (__any_sync(0xffffffffu, ovm != 0)) {  // dedup (qbits) with every atomic in flight, one append per warp
+    uint32_t ob[K];
+    int32_t vv[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      vv[k] = (int32_t)e[k].x;
+      ob[k] = ((ovm >> k) & 1u) ? atomicOr(&c.qbits_next[e[k].x >> 5], 1u << (e[k].x & 31)) : ~0u;
+    }
+    uint32_t newm = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k)
-      if ((curm >> k) & 1u) push_global(c, (int32_t)e[k].x);
+      if (((ovm >> k) & 1u) && !(ob[k] & (1u << (e[k].x & 31)))) newm |= 1u << k;
+    warp_append(newm, vv, c.q_next, c.qcount_next, c.slots);
   }
   {
     uint32_t mk[K], pre[K], tot = 0;
