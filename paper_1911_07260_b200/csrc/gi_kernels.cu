@@ -76,6 +76,7 @@ static_assert(kFarSeg >= 32 * 8, "a warp's far segment must hold one relax batch
 #endif
 #endif
 constexpr int kBigK = GI_BIGK;  // stage B: consecutive edges per thread per iteration
+
 #ifndef GI_CLAIMS
 #define GI_CLAIMS 4
 #endif
@@ -618,11 +619,11 @@ __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32
   if (threadIdx.x == 0) ne += (uint32_t)total;
   // each thread relaxes kBigK CONSECUTIVE edges per iteration: one binary search for
   // the first, then a forward walk (entries have deg >= 1 except empty hub slices, which
-  // the walk skips); a warp covers kBigK*256 B of contiguous edges per iteration
-  for (unsigned long long k0 = 0; k0 < total; k0 += (unsigned long long)kBigK * kBlock) {
-    uint2 e[kBigK];
-    uint32_t du[kBigK];
-    uint32_t valid = 0;
+  // the walk skips); a warp covers kBigK*256 B of contiguous edges per iteration.
+  // (Software-pipelining the next iteration's edge loads was measured slower: spills at
+  // 1024 threads, longer code at 512.)
+  auto fetch = [&](unsigned long long k0, uint2 (&e)[kBigK], uint32_t (&du)[kBigK], uint32_t& valid) {
+    valid = 0;
     const unsigned long long kt = k0 + (unsigned long long)kBigK * threadIdx.x;
 #pragma unroll
     for (int u = 0; u < kBigK; ++u) { e[u] = make_uint2(0, 0); du[u] = 0; }
@@ -651,6 +652,13 @@ __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32
         }
       }
     }
+  };
+  const unsigned long long step = (unsigned long long)kBigK * kBlock;
+  for (unsigned long long k0 = 0; k0 < total; k0 += step) {
+    uint2 e[kBigK];
+    uint32_t du[kBigK];
+    uint32_t valid;
+    fetch(k0, e, du, valid);
     relax_batch<FUSED, kBigK>(c, e, du, valid);
   }
   TRACE(13);
