@@ -38,6 +38,8 @@ drain = sys.argv[3] if len(sys.argv) > 3 else "async"
 max_ctas = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 if what == "path":
     g = gen.path(20000); src_v = 0; delta = delta or 10**9
+elif what == "path1":  # one bucket per vertex: the per-phase cost
+    g = gen.path(5000); src_v = 0; delta = 1
 elif what == "cfg4":
     g = gen.config_graph(4); src_v = gen.config_source(4, g); delta = delta or 2
 elif what == "cfg3":
