@@ -109,12 +109,27 @@ __device__ __forceinline__ void kc_push(KcCtx& c, bool want, int32_t v) {
 // edges are split over every CTA in the next round) and is staged with degree 0.
 __device__ __forceinline__ void kc_stage_vertices(const KcArgs& a, const KcSmem& m, KcCtx& c, const int32_t* list,
                                                   uint32_t cnt) {
-  for (uint32_t i = threadIdx.x; i < cnt; i += kKcBlock) {
-    const int32_t v = list[i];
-    const long long b0 = a.off[v], b1 = a.off[v + 1];
-    uint32_t d = (uint32_t)(b1 - b0);
-    if (d >= kKcHub) {
-      const uint32_t hp = atomicAdd(c.hcount_next, 1u);
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t i0 = 0; i0 < cnt; i0 += kKcBlock) {  // warp-uniform trip count
+    const uint32_t i = i0 + threadIdx.x;
+    const bool in = i < cnt;
+    long long b0 = 0;
+    uint32_t d = 0;
+    if (in) {
+      const int32_t v = list[i];
+      b0 = a.off[v];
+      d = (uint32_t)(a.off[v + 1] - b0);
+    }
+    // hubs: one global atomic per warp (every CTA appends to the same counter)
+    const bool hub = in && d >= kKcHub;
+    const uint32_t mh = __ballot_sync(0xffffffffu, hub);
+    uint32_t hbase = 0;
+    if (mh) {
+      if (lane == 0) hbase = atomicAdd(c.hcount_next, (uint32_t)__popc(mh));
+      hbase = __shfl_sync(0xffffffffu, hbase, 0);
+    }
+    if (hub) {
+      const uint32_t hp = hbase + __popc(mh & ((1u << lane) - 1u));
       if (hp < c.hubcap) {
         HubEnt he;
         he.beg = b0;
@@ -124,8 +139,10 @@ __device__ __forceinline__ void kc_stage_vertices(const KcArgs& a, const KcSmem&
         d = 0;
       }
     }
-    m.beg[i] = b0;
-    m.deg[i] = d;
+    if (in) {
+      m.beg[i] = b0;
+      m.deg[i] = d;
+    }
   }
   __syncthreads();
 }

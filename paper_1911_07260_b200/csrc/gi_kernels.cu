@@ -523,43 +523,62 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
     for (int u = 0; u < U; ++u) cur[u] = (check_stale && (have & (1u << u))) ? ld_dist(c.dist + v[u]) : kInf;
     TRACE(2);
     uint32_t valid = 0, heads = 0;
+    const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (!(have & (1u << u))) continue;
-      if (!LD && e[u].x == kColBig) {  // octet-uniform: every entry of a big slot is kColBig
-        const uint32_t om = 0xFFu << (threadIdx.x & 24);
-        const uint32_t lo = __shfl_sync(om, e[u].y, 1, 8);
-        const uint32_t hi = __shfl_sync(om, e[u].y, 2, 8);
-        if (sub == 0 && !(cur[u] < du[u])) {
-          ++nv;
-          const uint32_t deg = e[u].y;
-          uint32_t hp = 0xFFFFFFFFu;
-          if (deg >= c.hub_min) {  // hub: split over the whole group in the next phase
-            hp = atomicAdd(c.hcount_next, 1u);
-            if (hp < c.hubcap) {
-              HubEnt he;
-              he.beg = (int64_t)(((uint64_t)hi << 32) | lo);
-              he.deg = deg;
-              he.du = du[u];
-              c.hub_next[hp] = he;
-            }
-          }
-          const uint32_t pos = hp < c.hubcap ? 0xFFFFFFFFu : atomicAdd(&c.s->bigtail, 1u);
-          if (hp < c.hubcap) {
-            // queued on the group hub list
-          } else if (pos < (uint32_t)kBigCap) {
+    for (int u = 0; u < U; ++u) {  // warp-uniform: the appends below are warp-aggregated
+      const bool hv_ = (have >> u) & 1u;
+      const bool big = !LD && hv_ && e[u].x == kColBig;  // octet-uniform
+      if (hv_ && !big) {
+        if (sub == 0) heads |= 1u << u;
+        if (e[u].x != kColEmpty) valid |= 1u << u;
+      }
+      if constexpr (!LD) {
+        if (!__any_sync(0xffffffffu, big)) continue;
+        // a big slot holds {kColBig, deg}, {kColBig, beg_lo}, {kColBig, beg_hi}
+        const uint32_t lo = __shfl_sync(0xffffffffu, e[u].y, 1, 8);
+        const uint32_t hi = __shfl_sync(0xffffffffu, e[u].y, 2, 8);
+        const bool mine = big && sub == 0 && !(cur[u] < du[u]);  // fresh entries only
+        const uint32_t deg = e[u].y;
+        const int64_t beg = (int64_t)(((uint64_t)hi << 32) | lo);
+        // hubs (deg >= hub_min): the group hub list, split over every CTA next phase;
+        // one global atomic per warp (every CTA appends to the same counter)
+        const bool hub = mine && deg >= c.hub_min;
+        const uint32_t mh = __ballot_sync(0xffffffffu, hub);
+        uint32_t hbase = 0;
+        if (mh) {
+          if (lane == 0) hbase = atomicAdd(c.hcount_next, (uint32_t)__popc(mh));
+          hbase = __shfl_sync(0xffffffffu, hbase, 0);
+        }
+        const uint32_t hp = hbase + __popc(mh & lt);
+        const bool hub_ok = hub && hp < c.hubcap;
+        if (hub_ok) {
+          HubEnt he;
+          he.beg = beg;
+          he.deg = deg;
+          he.du = du[u];
+          c.hub_next[hp] = he;
+        }
+        // the rest: this CTA's high-degree list (stage B), one shared atomic per warp
+        const bool loc = mine && !hub_ok;
+        const uint32_t ml = __ballot_sync(0xffffffffu, loc);
+        uint32_t lbase = 0;
+        if (ml) {
+          if (lane == 0) lbase = atomicAdd(&c.s->bigtail, (uint32_t)__popc(ml));
+          lbase = __shfl_sync(0xffffffffu, lbase, 0);
+        }
+        if (loc) {
+          const uint32_t pos = lbase + __popc(ml & lt);
+          if (pos < (uint32_t)kBigCap) {
             BigEnt be;
-            be.beg = (int64_t)(((uint64_t)hi << 32) | lo);
-            be.deg = e[u].y;
+            be.beg = beg;
+            be.deg = deg;
             be.du = du[u];
             c.big[pos] = be;
           } else {
             push_global(c, (int32_t)v[u]);  // list full: the next group-wide round takes it
           }
         }
-      } else {
-        if (sub == 0) heads |= 1u << u;
-        if (e[u].x != kColEmpty) valid |= 1u << u;
+        nv += mine;
       }
     }
     const uint32_t stale = relax_batch<FUSED, U, LD>(c, e, du, valid, (check_stale && !GI_X_NOSTALE) ? cur : nullptr);
