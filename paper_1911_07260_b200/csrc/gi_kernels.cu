@@ -92,27 +92,27 @@ constexpr uint32_t kMaxClaim = GI_MAXCLAIM;
 #ifdef GI_TRACE
 // Debug builds only: cycles between trace points, accumulated by CTA 0 / thread 0 in
 // shared memory (so that tracing adds ~no latency) and flushed at kernel exit.
-__device__ unsigned long long g_trace[32];
-__shared__ unsigned long long s_trace[32];
+__device__ unsigned long long g_trace[64];
+__shared__ unsigned long long s_trace[64];
 __shared__ long long s_trace_last;
 #define TRACE(k)                                                   \
   do {                                                             \
     if (blockIdx.x == 0 && threadIdx.x == 0) {                     \
       long long t_ = clock64();                                    \
       s_trace[k] += (unsigned long long)(t_ - s_trace_last);       \
-      s_trace[16 + (k)] += 1;                                      \
+      s_trace[32 + (k)] += 1;                                      \
       s_trace_last = t_;                                           \
     }                                                              \
   } while (0)
 #define TRACE_INIT()                                                          \
   do {                                                                        \
-    if (threadIdx.x < 32) s_trace[threadIdx.x] = 0;                           \
+    if (threadIdx.x < 64) s_trace[threadIdx.x] = 0;                           \
     if (threadIdx.x == 0) s_trace_last = clock64();                           \
     __syncthreads();                                                          \
   } while (0)
 #define TRACE_FLUSH()                                                         \
   do {                                                                        \
-    if (blockIdx.x == 0 && threadIdx.x < 32) atomicAdd(&g_trace[threadIdx.x], s_trace[threadIdx.x]); \
+    if (blockIdx.x == 0 && threadIdx.x < 64) atomicAdd(&g_trace[threadIdx.x], s_trace[threadIdx.x]); \
   } while (0)
 // async drain: per phase max over CTAs of feed+drain cycles / max depth; per item
 // (all CTAs, lane 0 of each warp) claim->atomics-returned, ->push-done, idle spins
@@ -678,7 +678,9 @@ __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32
     uint32_t du[kBigK];
     uint32_t valid;
     fetch(k0, e, du, valid);
+    TRACE(16);
     relax_batch<FUSED, kBigK>(c, e, du, valid);
+    TRACE(17);
   }
   TRACE(13);
 }
@@ -1643,9 +1645,9 @@ extern "C" int gi_debug_trace2(unsigned long long* phase, unsigned long long* it
 
 extern "C" int gi_debug_trace(unsigned long long* out, int reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 32);
+  cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 64);
   if (reset) {
-    unsigned long long z[32] = {0};
+    unsigned long long z[64] = {0};
     cudaMemcpyToSymbol(g_trace, z, sizeof(z));
   }
   return 0;

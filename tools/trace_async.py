@@ -61,7 +61,7 @@ opt.cta_threads = 512  # the trace buffers live in the primary (512-thread) buil
 opt.drain = {"async": 2, "bsp": 1, "unfused": 1}[drain]
 opt.fusion = 0 if drain == "unfused" else 1
 st = gi_stats()
-buf = np.zeros(32, np.uint64)
+buf = np.zeros(64, np.uint64)
 ph = np.zeros((7, 16384), np.uint64)
 it = np.zeros(16, np.uint64)
 for rep in range(2):
@@ -76,10 +76,11 @@ print(what, "delta", delta, "drain", drain, "max_ctas", max_ctas, "gpu_ms %.3f" 
 clk = 1.965e3  # cycles per µs at the max SM clock
 names = {0: "bsp drain loop top", 2: "slot load", 3: "relax", 4: "rest", 5: "decision", 6: "feed (async) / extract",
          7: "phase work end", 8: "far flush + fmin", 9: "group barrier", 11: "drain (async, CTA 0)",
-         12: "stage B scan", 13: "stage B edge loop", 14: "ROUND claim+staging", 15: "hub slices (after B)"}
+         12: "stage B scan", 13: "stage B edge loop", 14: "ROUND claim+staging", 15: "hub slices (after B)",
+         16: "B iter: search + edge-load issue", 17: "B iter: relax_batch (waits)"}
 tot = 0
-for k in range(16):
-    c = int(buf[16 + k])
+for k in range(32):
+    c = int(buf[32 + k])
     if c:
         tot += int(buf[k])
         print(f"CTA0 {k:2d} {names.get(k, '?'):28s} calls={c:8d} cyc/call={int(buf[k]) / c:9.1f} "
