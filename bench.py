@@ -31,7 +31,7 @@ import gen  # noqa: E402
 
 METRIC = "Δ-stepping SSSP GTEPS (m / time per source)"
 UNIT = "GTEPS"
-DEFAULT_DELTA = {1: 1000, 2: 1 << 16, 3: 2, 4: 2, 5: 1 << 15}
+DEFAULT_DELTA = {1: 1000, 2: 1 << 16, 3: 2, 4: 2, 5: 1 << 13}
 WORKLOAD = {
     1: "cfg1: 256x256 4-neighbour grid, w~U[1,1000) seed 1, src 0",
     2: "cfg2: road-like 4096x4096 grid (5% lattice edges deleted, 1% diagonals), w~U[1,10000) seed 2, "

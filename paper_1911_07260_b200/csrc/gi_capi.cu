@@ -302,12 +302,29 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   // group sizing: single source -> one group of every CTA (capped by max_ctas);
   // batch -> several groups in flight, each of group_ctas CTAs
   int G, ngroups;
+  Workspace* w = ws_acquire(g);
   if (!batch || nsrc == 1) {
     G = total;
     if (opt.max_ctas > 0 && opt.max_ctas < G) G = opt.max_ctas;
     ngroups = 1;
   } else {
-    G = opt.group_ctas > 0 ? opt.group_ctas : 16;
+    if (opt.group_ctas > 0) {
+      G = opt.group_ctas;
+    } else {
+      // auto: one group per source, so the batch runs in one wave (a partial last wave
+      // leaves most SMs idle while it runs), with at least 2 CTAs per group, and no more
+      // groups than half the free device memory holds workspaces for. Measured on config
+      // 5 (64 sources): 2 CTAs x 64 groups 228 ms, 16 x 9 258 ms, 3 x 49 266 ms.
+      G = std::max(2, total / nsrc);
+      const int64_t nw = (g->n + 31) / 32;
+      const int64_t hubcap = std::min<int64_t>(2 * (g->m / kMinHubMin) + 64, 0x7FFFFFFF);
+      const size_t per = (size_t)(16 * g->n + 16 * nw) + 2 * (size_t)hubcap * sizeof(HubEnt) + sizeof(Ctl);
+      size_t free_b = 0, total_b = 0;
+      if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+        const int maxg = w->cap_groups + std::max<int64_t>(1, (int64_t)(free_b / 2 / per));
+        if (total / G > maxg) G = (total + maxg - 1) / maxg;
+      }
+    }
     if (opt.max_ctas > 0 && opt.max_ctas < G) G = opt.max_ctas;
     if (G > total) G = total;
     ngroups = total / G;
@@ -315,7 +332,6 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
     if (ngroups < 1) ngroups = 1;
   }
 
-  Workspace* w = ws_acquire(g);
   gi_status s = ws_prepare(g, w, ngroups, nsrc);
   if (s) { ws_release(g, w, false); return s; }
   cudaStream_t st = opt.cuda_stream ? (cudaStream_t)opt.cuda_stream : w->stream;
