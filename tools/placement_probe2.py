@@ -1,6 +1,6 @@
 """Placement effect on config 4, part 2: is the second library instance fast because of its
 module, or because a graph was created and destroyed before? usage: python tools/placement_probe2.py MODE
-MODE: createonly = lib a only creates/destroys a graph; runonly = lib a runs queries on a tiny graph"""
+MODE: createonly | createsmall | nothing | bigalloc | runonly | = lib a only creates/destroys a graph; runonly = lib a runs queries on a tiny graph"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -44,6 +44,17 @@ if mode == "createonly":
     assert a.gi_graph_create(g.n, g.m, g.offsets.ctypes.data, g.cols.ctypes.data, g.w.ctypes.data, 0, ctypes.byref(h)) == 0
     a.gi_graph_destroy(h)
     print("lib a: create+destroy only")
+elif mode == "createsmall":  # lib a creates/destroys a tiny graph: modules loaded, little memory
+    t = gen.config_graph(1)
+    h = vp()
+    assert a.gi_graph_create(t.n, t.m, t.offsets.ctypes.data, t.cols.ctypes.data, t.w.ctypes.data, 0, ctypes.byref(h)) == 0
+    a.gi_graph_destroy(h)
+    print("lib a: tiny create+destroy only")
+elif mode == "nothing":  # lib a loaded, never called
+    print("lib a: loaded only")
+elif mode == "bigalloc":  # a plain 22 GB cudaMalloc/cudaFree through torch before lib b
+    x = torch.empty(22 << 30, dtype=torch.uint8, device="cuda"); x.fill_(1); del x; torch.cuda.empty_cache()
+    print("torch 22 GB touched and freed")
 elif mode == "runonly":
     t = gen.config_graph(1)
     print("lib a on config 1:", run(a, t, 0))

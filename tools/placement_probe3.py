@@ -41,3 +41,15 @@ elif mode == "warm_small":    # a small query first (context, module, workspace 
     G = gi.Graph.from_csr(g)
     out = torch.empty(g.n, dtype=torch.int32, device="cuda")
     print(mode, timed(G, out))
+elif mode == "dummy_alloc":   # a 25 GB allocation made and released first (torch), then graph
+    x = torch.empty(25 << 30, dtype=torch.uint8, device="cuda")
+    del x
+    torch.cuda.empty_cache()
+    G = gi.Graph.from_csr(g)
+    out = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    print(mode, timed(G, out))
+elif mode == "second_alive":  # a second graph created while the first is still alive
+    G1 = gi.Graph.from_csr(g)
+    G = gi.Graph.from_csr(g)
+    out = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    print(mode, "second", timed(G, out), "first", timed(G1, out))

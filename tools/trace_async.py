@@ -104,6 +104,9 @@ if m2.any():
     print(f"phases {int(m2.sum())}: sum of max-CTA busy {mx[m2].sum() / clk / 1e3:.3f} ms, sum of mean-CTA busy "
           f"{sm[m2].sum() / G / clk / 1e3:.3f} ms (imbalance {mx[m2].sum() / max(sm[m2].sum() / G, 1):.2f}x); "
           f"gpu_ms {st.gpu_ms:.3f}")
+    for md, name in ((0, "ROUND"), (1, "EXTRACT")):
+        sel = m2 & (ph[4] == md)
+        print(f"  {name} phases {int(sel.sum())}: sum of max-CTA busy {mx[sel].sum() / clk / 1e3:.3f} ms")
     top = np.argsort(-mx)[:10]
     print("  heaviest phases: (phase, us max, us mean, mode 0=ROUND/1=EXTRACT, cnt, hubs)")
     for i in top:
