@@ -145,6 +145,33 @@ gi_status gi_sssp_delta_ex(const gi_graph* g, int32_t src, uint32_t delta, const
 gi_status gi_sssp_batch_ex(const gi_graph* g, const int32_t* srcs, int32_t nsrc, uint32_t delta,
                            const gi_options* opt, uint32_t* dist_out, gi_stats* per_src);
 
+/* Multi-GPU batch with the gather fused into the kernel (north_star: "sources sharded
+ * evenly over 1/2/4/8 B200s, all distance arrays gathered"). Each rank holds
+ * the full result matrix uint32[total][n]; rank r computes a contiguous block of nsrc rows.
+ *   peer_rows  [npeers] device pointers, each to the FIRST row of this block inside one
+ *              rank's matrix (this rank's own memory for p == self; peer memory made
+ *              accessible from the graph's device — P2P or gi_ipc_open_handle — otherwise);
+ *   self       index of this rank's own matrix in peer_rows: rows are computed in place there.
+ * As soon as a CTA group finishes a source, it writes the row into every other peer_rows[p]
+ * (stores over NVLink), while the remaining groups keep computing; no collective runs
+ * afterwards. The call returns when the kernel has completed; other ranks' rows are in this
+ * rank's matrix once every rank has returned (a barrier between ranks is the caller's).
+ * Errors as gi_sssp_batch_ex; npeers < 1, self out of range or a NULL peer row ->
+ * GI_ERR_INVALID_ARGUMENT; peer_rows[self] not device memory of the graph's device ->
+ * GI_ERR_INVALID_ARGUMENT. */
+gi_status gi_sssp_batch_peers(const gi_graph* g, const int32_t* srcs, int32_t nsrc, uint32_t delta,
+                              const gi_options* opt, uint32_t* const* peer_rows, int32_t npeers,
+                              int32_t self, gi_stats* per_src);
+
+/* Inter-process sharing of a result matrix for gi_sssp_batch_peers (one process per GPU).
+ * gi_ipc_get_handle: handle (64 opaque bytes, written to `handle`) of the device allocation
+ * that contains dptr, and dptr's byte offset inside it. gi_ipc_open_handle: map another
+ * process's allocation on `device` (peer access enabled lazily) and return base + offset.
+ * gi_ipc_close_handle: unmap (dptr and offset as returned/passed by open). */
+gi_status gi_ipc_get_handle(const void* dptr, void* handle, uint64_t* offset);
+gi_status gi_ipc_open_handle(const void* handle, uint64_t offset, int32_t device, void** dptr);
+gi_status gi_ipc_close_handle(void* dptr, uint64_t offset, int32_t device);
+
 /* Point-to-point shortest path: Δ-stepping from src that stops when it
  * enters bucket i with iΔ >= the distance already found to dst — "terminates the program
  * early when it enters iteration i where iΔ is greater than or equal to the shortest

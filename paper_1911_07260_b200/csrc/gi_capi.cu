@@ -1,6 +1,7 @@
 // gi_capi.cu — C ABI (include/gi.h) and host engine: graph residency, validation,
 // workspace pool, launch policy, statistics.
 #include "gi.h"
+#include <cuda.h>
 #include "gi_internal.h"
 
 #include <algorithm>
@@ -67,6 +68,8 @@ struct Workspace {
   uint32_t* d_stage = nullptr;  // staging for host dist_out
   size_t stagecap = 0;
   uint32_t* d_src_next = nullptr;  // batch source claim counter
+  uint32_t** d_peers = nullptr;  // gi_sssp_batch_peers: device copy of the peer row bases
+  int peercap = 0;
   uint32_t* d_h = nullptr;      // staging for a host A* heuristic
   size_t hcap = 0;
   uint32_t* kc_prio = nullptr;  // k-core: priorities [n]
@@ -82,6 +85,7 @@ struct Workspace {
     if (d_srcs) cudaFree(d_srcs);
     if (d_stage) cudaFree(d_stage);
     if (d_h) cudaFree(d_h);
+    if (d_peers) cudaFree(d_peers);
     if (d_src_next) cudaFree(d_src_next);
     if (kc_prio) cudaFree(kc_prio);
     if (kc_ctl) cudaFree(kc_ctl);
@@ -243,7 +247,8 @@ void fill_stats(gi_stats* st, const QStats& q, float ms, int ctas, int groups, i
 
 gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, uint32_t delta,
                       const gi_options* opt_in, uint32_t* dist_out, gi_stats* stats, bool batch,
-                      int32_t target = -1, const uint32_t* heur = nullptr) {
+                      int32_t target = -1, const uint32_t* heur = nullptr,
+                      uint32_t* const* peer_rows = nullptr, int32_t npeers = 0) {
   gi_graph* g = const_cast<gi_graph*>(cg_);
   if (!g) return fail(GI_ERR_INVALID_ARGUMENT, "graph is NULL");
   if (nsrc < 0) return fail(GI_ERR_INVALID_ARGUMENT, "nsrc < 0");
@@ -277,6 +282,8 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   const bool dev_out = is_device_ptr(dist_out, g->device, &wrongdev);
   if (wrongdev) return fail(GI_ERR_INVALID_ARGUMENT, "dist_out on another device");
   const bool ppsp = target >= 0;  // dist_out is ONE value; the distances live in the workspace
+  if (npeers > 0 && !dev_out)
+    return fail(GI_ERR_INVALID_ARGUMENT, "peer_rows[self] must be device memory on the graph's device");
 
   const bool fused = opt.fusion != 0;
   if (opt.drain > 2) return fail(GI_ERR_INVALID_ARGUMENT, "drain must be 0 (auto), 1 (bsp) or 2 (async)");
@@ -412,6 +419,25 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   if ((e = cudaMemsetAsync(w->d_src_next, 0, sizeof(uint32_t), st))) return bail(e, "init claim counter");
   a.src_next = w->d_src_next;  // claims count from 0; sources 0..ngroups-1 are taken statically
   a.h = d_h;
+  a.peers = nullptr;
+  a.npeers = 0;
+  a.peer_vec = 0;
+  if (npeers > 0) {
+    if (w->peercap < npeers) {
+      if (w->d_peers) cudaFree(w->d_peers);
+      w->d_peers = nullptr;
+      w->peercap = 0;
+      if ((e = cudaMalloc(&w->d_peers, sizeof(uint32_t*) * npeers)) != cudaSuccess) return bail(e, "alloc peers");
+      w->peercap = npeers;
+    }
+    if ((e = cudaMemcpyAsync(w->d_peers, peer_rows, sizeof(uint32_t*) * npeers, cudaMemcpyHostToDevice, st)))
+      return bail(e, "copy peers");
+    bool vec = g->n % 4 == 0;
+    for (int i = 0; i < npeers; ++i) vec = vec && ((uintptr_t)peer_rows[i] % 16 == 0);
+    a.peers = w->d_peers;
+    a.npeers = npeers;
+    a.peer_vec = vec ? 1u : 0u;
+  }
 
   if ((e = cudaEventRecord(w->ev0, st))) return bail(e, "event");
   if ((e = wide ? v1024::launch_sssp(a, kind, G * ngroups, st) : v512::launch_sssp(a, kind, G * ngroups, st)))
@@ -609,6 +635,60 @@ gi_status gi_sssp_delta(const gi_graph* g, int32_t src, uint32_t delta, uint32_t
 gi_status gi_sssp_batch_ex(const gi_graph* g, const int32_t* srcs, int32_t nsrc, uint32_t delta,
                            const gi_options* opt, uint32_t* dist_out, gi_stats* per_src) {
   return run_queries(g, srcs, nsrc, delta, opt, dist_out, per_src, true);
+}
+
+gi_status gi_sssp_batch_peers(const gi_graph* g, const int32_t* srcs, int32_t nsrc, uint32_t delta,
+                              const gi_options* opt, uint32_t* const* peer_rows, int32_t npeers, int32_t self,
+                              gi_stats* per_src) {
+  if (npeers < 1 || !peer_rows) return fail(GI_ERR_INVALID_ARGUMENT, "need npeers >= 1 and peer_rows");
+  if (self < 0 || self >= npeers) return fail(GI_ERR_INVALID_ARGUMENT, "self not in [0, npeers)");
+  for (int32_t i = 0; i < npeers; ++i)
+    if (!peer_rows[i]) return fail(GI_ERR_INVALID_ARGUMENT, "peer_rows[%d] is NULL", i);
+  return run_queries(g, srcs, nsrc, delta, opt, peer_rows[self], per_src, true, -1, nullptr, peer_rows, npeers);
+}
+
+gi_status gi_ipc_get_handle(const void* dptr, void* handle, uint64_t* offset) {
+  if (!dptr || !handle || !offset) return fail(GI_ERR_INVALID_ARGUMENT, "NULL argument");
+  // the allocation's base (cudaIpcGetMemHandle names whole allocations; a torch tensor may
+  // sit inside a larger caching-allocator block): the driver's cuMemGetAddressRange, through
+  // the runtime's entry-point query so that the library does not link libcuda
+  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(GI_ERR_CUDA, "cuMemGetAddressRange entry point not found");
+    get_range = (GetRange)fn;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, (CUdeviceptr)dptr) != CUDA_SUCCESS)
+    return fail(GI_ERR_INVALID_ARGUMENT, "dptr is not device memory of this process");
+  cudaIpcMemHandle_t h;
+  GI_CUDA(cudaIpcGetMemHandle(&h, (void*)base), "cudaIpcGetMemHandle");
+  memcpy(handle, &h, sizeof(h));
+  *offset = (uint64_t)((CUdeviceptr)dptr - base);
+  return GI_OK;
+}
+
+gi_status gi_ipc_open_handle(const void* handle, uint64_t offset, int32_t device, void** dptr) {
+  if (!handle || !dptr) return fail(GI_ERR_INVALID_ARGUMENT, "NULL argument");
+  DeviceGuard dg(device);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  GI_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  *dptr = (char*)base + offset;
+  return GI_OK;
+}
+
+gi_status gi_ipc_close_handle(void* dptr, uint64_t offset, int32_t device) {
+  if (!dptr) return fail(GI_ERR_INVALID_ARGUMENT, "NULL argument");
+  DeviceGuard dg(device);
+  GI_CUDA(cudaIpcCloseMemHandle((char*)dptr - offset), "cudaIpcCloseMemHandle");
+  return GI_OK;
 }
 
 gi_status gi_sssp_batch(const gi_graph* g, const int32_t* srcs, int32_t nsrc, uint32_t delta,

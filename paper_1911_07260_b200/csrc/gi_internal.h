@@ -124,6 +124,10 @@ struct KArgs {
   uint32_t dyn_claim;   // ROUND phases claim frontier chunks dynamically (skewed degrees) vs equal slices
   const uint32_t* h;    // A*: per-vertex heuristic (priority = dist + h); nullptr = 0 (SSSP / PPSP)
   uint32_t* src_next;   // batch: claims so far (source index = ngroups + claim)
+  uint32_t* const* peers;  // gi_sssp_batch_peers: [npeers] row bases of every rank's result
+                           // matrix (device-accessible: local, P2P or IPC-mapped); nullptr = none
+  int32_t npeers;
+  uint32_t peer_vec;    // 16-byte copies (n % 4 == 0 and every base 16-byte aligned)
 };
 
 // k-core (gi_kcore.cu): control block, statistics and arguments.

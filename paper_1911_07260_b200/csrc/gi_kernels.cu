@@ -1496,6 +1496,25 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
       if (__syncthreads_or(bad) && tid == 0) atomicOr(&a.qstats[si].overflow, 1u);
     }
 
+    // ---- fused gather (gi_sssp_batch_peers): the finished row is written straight into
+    // every other rank's result matrix (peer memory over NVLink), by this group's CTAs,
+    // while the other groups keep computing — no separate all-gather after the batch ----
+    if (a.npeers > 0) {
+      for (int32_t pi = 0; pi < a.npeers; ++pi) {
+        uint32_t* dst = a.peers[pi];
+        if (dst == a.dist) continue;  // the rank's own matrix: computed in place
+        dst += (size_t)si * (size_t)n;
+        if (a.peer_vec) {
+          const uint4* s4 = reinterpret_cast<const uint4*>(dist);
+          uint4* d4 = reinterpret_cast<uint4*>(dst);
+          for (int64_t i = (int64_t)rank * kBlock + tid; i < n / 4; i += (int64_t)G * kBlock) d4[i] = __ldcg(s4 + i);
+        } else {
+          for (int64_t i = (int64_t)rank * kBlock + tid; i < n; i += (int64_t)G * kBlock) dst[i] = ld_dist(dist + i);
+        }
+      }
+      __threadfence_system();
+    }
+
     // ---- statistics ----
     const unsigned long long tv = block_sum(tnv, s);
     const unsigned long long te = block_sum(tne, s);

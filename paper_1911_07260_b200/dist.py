@@ -3,8 +3,16 @@ independent sources are split across GPUs, with the graph replicated per GPU and
 gathered over NCCL/NVLink. A single-source query runs on one GPU.").
 
 One process per GPU (torchrun). Every rank holds a replica of the graph (generated
-deterministically, so no broadcast is needed), runs ``gi_sssp_batch`` on its contiguous
-block of sources, and the uint32 rows are all-gathered — the only data-path collective.
+deterministically, so no broadcast is needed) and computes a contiguous block of sources.
+
+Two ways to assemble the [k, n] result on every rank:
+- ``sssp_batch_fused_gather`` (the product path): every rank's result matrix is mapped into
+  every other rank (CUDA IPC handles exchanged once over the process group), and the
+  kernel itself writes each finished row into all of them over NVLink while its other CTA
+  groups keep computing (``gi_sssp_batch_peers``). No collective moves data; one barrier
+  marks completion.
+- ``sssp_batch_multi_gpu``: ``gi_sssp_batch`` then an NCCL all-gather of the rows (the
+  baseline the fused path replaces; also the gloo-testable reference for the sharding).
 """
 from __future__ import annotations
 
@@ -79,3 +87,62 @@ def sssp_batch_multi_gpu(G, srcs, delta: int, compute=None, **opts):
         dist.all_gather(parts, local.contiguous())
         gathered = torch.cat(parts, 0)
     return unpad_rows(gathered, k, world)
+
+
+def peer_row_addresses(bases, lo: int, n: int, itemsize: int = 4):
+    """Device address of row `lo` in each rank's [k, n] matrix (base addresses `bases`)."""
+    return [int(b) + lo * n * itemsize for b in bases]
+
+
+def exchange_handles(out, rank: int, world: int, device: int, all_gather_object=None, ipc=None):
+    """Map every rank's result matrix into this process. Returns (bases, opened) where
+    bases[r] is the device address of rank r's matrix as seen from this rank and opened
+    lists (address, offset) pairs to close after the final barrier."""
+    if ipc is None:
+        from . import gi as ipc
+    if all_gather_object is None:
+        import torch.distributed as dist
+        all_gather_object = dist.all_gather_object
+    mine = ipc.ipc_handle(out)
+    allh = [None] * world
+    all_gather_object(allh, mine)
+    bases, opened = [], []
+    for r in range(world):
+        if r == rank:
+            bases.append(int(out.data_ptr()))
+        else:
+            h, off = allh[r]
+            addr = ipc.ipc_open(h, off, device)
+            bases.append(addr)
+            opened.append((addr, off))
+    return bases, opened
+
+
+def sssp_batch_fused_gather(G, srcs, delta: int, out=None, **opts):
+    """All ranks call this with the same ``srcs``; returns the [k, n] int32 tensor of
+    distances (uint32 bit patterns) on every rank, assembled by the kernels' own peer
+    stores (``gi_sssp_batch_peers``)."""
+    import torch
+    import torch.distributed as dist
+    from . import gi
+
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    srcs = np.asarray(srcs, dtype=np.int32)
+    k = srcs.shape[0]
+    n = G.n
+    if out is None:
+        out = torch.empty((k, n), dtype=torch.int32, device=f"cuda:{G.device}")
+    if world == 1:
+        bases, opened = [int(out.data_ptr())], []
+    else:
+        bases, opened = exchange_handles(out, rank, world, G.device)
+    lo, hi = shard_bounds(k, rank, world)
+    if hi > lo:
+        gi.gi_sssp_batch_peers(G, srcs[lo:hi], delta, peer_row_addresses(bases, lo, n), rank,
+                               gi.make_options(**opts) if opts else None)
+    if world > 1:
+        dist.barrier()  # every rank's kernel has completed: all rows are in every matrix
+        for addr, off in opened:
+            gi.ipc_close(addr, off, G.device)
+    return out

@@ -28,7 +28,8 @@ STATUS = {0: "GI_OK", 1: "GI_ERR_INVALID_ARGUMENT", 2: "GI_ERR_OUT_OF_RANGE", 3:
 EXPORTS = ["gi_graph_create", "gi_graph_destroy", "gi_graph_info", "gi_sssp_delta", "gi_sssp_batch",
            "gi_options_default", "gi_sssp_delta_ex", "gi_sssp_batch_ex", "gi_last_error",
            "gi_status_string", "gi_version", "gi_ppsp_delta", "gi_ppsp_delta_ex", "gi_astar_delta",
-           "gi_astar_delta_ex", "gi_kcore", "gi_kcore_ex"]
+           "gi_astar_delta_ex", "gi_kcore", "gi_kcore_ex", "gi_sssp_batch_peers", "gi_ipc_get_handle",
+           "gi_ipc_open_handle", "gi_ipc_close_handle"]
 
 
 class GiError(RuntimeError):
@@ -75,6 +76,11 @@ _lib.gi_options_default.argtypes = [ctypes.POINTER(gi_options)]
 _lib.gi_options_default.restype = None
 _lib.gi_sssp_delta_ex.argtypes = [_vp, _i32, _u32, ctypes.POINTER(gi_options), _vp, ctypes.POINTER(gi_stats)]
 _lib.gi_sssp_batch_ex.argtypes = [_vp, _vp, _i32, _u32, ctypes.POINTER(gi_options), _vp, ctypes.POINTER(gi_stats)]
+_lib.gi_sssp_batch_peers.argtypes = [_vp, _vp, _i32, _u32, ctypes.POINTER(gi_options), ctypes.POINTER(_vp), _i32,
+                                     _i32, ctypes.POINTER(gi_stats)]
+_lib.gi_ipc_get_handle.argtypes = [_vp, _vp, ctypes.POINTER(ctypes.c_uint64)]
+_lib.gi_ipc_open_handle.argtypes = [_vp, ctypes.c_uint64, _i32, ctypes.POINTER(_vp)]
+_lib.gi_ipc_close_handle.argtypes = [_vp, ctypes.c_uint64, _i32]
 _lib.gi_ppsp_delta.argtypes = [_vp, _i32, _i32, _u32, _vp]
 _lib.gi_ppsp_delta_ex.argtypes = [_vp, _i32, _i32, _u32, ctypes.POINTER(gi_options), _vp, ctypes.POINTER(gi_stats)]
 _lib.gi_astar_delta.argtypes = [_vp, _i32, _i32, _u32, _vp, _vp]
@@ -87,7 +93,8 @@ _lib.gi_status_string.argtypes = [ctypes.c_int]
 _lib.gi_status_string.restype = ctypes.c_char_p
 _lib.gi_version.restype = _i32
 for _f in ("gi_graph_create", "gi_graph_info", "gi_sssp_delta", "gi_sssp_batch", "gi_sssp_delta_ex",
-           "gi_sssp_batch_ex", "gi_ppsp_delta", "gi_ppsp_delta_ex", "gi_astar_delta", "gi_astar_delta_ex", "gi_kcore", "gi_kcore_ex"):
+           "gi_sssp_batch_ex", "gi_ppsp_delta", "gi_ppsp_delta_ex", "gi_astar_delta", "gi_astar_delta_ex", "gi_kcore",
+           "gi_kcore_ex", "gi_sssp_batch_peers", "gi_ipc_get_handle", "gi_ipc_open_handle", "gi_ipc_close_handle"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 
@@ -196,6 +203,38 @@ def gi_sssp_batch(g: Graph, srcs, delta: int, dist_out, options: gi_options | No
     _check(_lib.gi_sssp_batch_ex(g.handle, _ptr(srcs), k, int(delta),
                                  ctypes.byref(options) if options else None, _ptr(dist_out), st))
     return st
+
+
+def gi_sssp_batch_peers(g: Graph, srcs, delta: int, peer_rows, self_index: int,
+                        options: gi_options | None = None, want_stats: bool = True):
+    """C-ABI gi_sssp_batch_peers. peer_rows: device addresses (ints) of this block's first
+    row inside every rank's result matrix; rows are computed in peer_rows[self_index]."""
+    k = int(srcs.shape[0])
+    st = (gi_stats * max(k, 1))() if want_stats else None
+    arr = (_vp * len(peer_rows))(*[int(p) for p in peer_rows])
+    _check(_lib.gi_sssp_batch_peers(g.handle, _ptr(srcs), k, int(delta), ctypes.byref(options) if options else None,
+                                    arr, len(peer_rows), int(self_index), st))
+    return st
+
+
+def ipc_handle(t) -> tuple[bytes, int]:
+    """(64-byte IPC handle of the allocation holding tensor t, byte offset of t in it)."""
+    h = (ctypes.c_uint8 * 64)()
+    off = ctypes.c_uint64()
+    _check(_lib.gi_ipc_get_handle(_vp(t.data_ptr()), h, ctypes.byref(off)))
+    return bytes(h), off.value
+
+
+def ipc_open(handle: bytes, offset: int, device: int) -> int:
+    """Map another process's allocation; returns the device address of base + offset."""
+    h = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    p = _vp()
+    _check(_lib.gi_ipc_open_handle(h, int(offset), int(device), ctypes.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(addr: int, offset: int, device: int) -> None:
+    _check(_lib.gi_ipc_close_handle(_vp(addr), int(offset), int(device)))
 
 
 def sssp(g: Graph, src: int, delta: int, out=None, **opts):

@@ -436,3 +436,75 @@ def test_kcore_matches_oracle(gi, config_graph):
         c3, st3 = gi.kcore(G3)
         assert np.array_equal(gi.as_uint32(c3), ref3)
         assert st3["edges_relaxed"] == g3.m  # every vertex is peeled once: each CSR entry is scanned once
+
+
+def test_batch_peers_fused_gather_one_process(gi, config_graph):
+    """gi_sssp_batch_peers (north_star multi-GPU batch) emulated in one
+    process: two 'ranks' each compute a block of sources into their own matrix, and the
+    kernel writes every finished row into the other matrix too. Both matrices must equal
+    the oracle row for row (n % 4 == 0: 16-byte copies; n % 4 != 0: element copies)."""
+    import torch
+    for g in (config_graph(1), gen.uniform_random(1001, 6000, 1, 100, 3)):
+        G = gi.Graph.from_csr(g)
+        srcs = gen.sources(g.n, 9, 11).astype(np.int32)
+        ref, _ = oracle.dijkstra_many(g, srcs)[:2]
+        mats = [torch.full((9, g.n), 7, dtype=torch.int32, device="cuda") for _ in range(2)]
+        bases = [m.data_ptr() for m in mats]
+        from paper_1911_07260_b200.dist import peer_row_addresses, shard_bounds
+        for r in range(2):
+            lo, hi = shard_bounds(9, r, 2)
+            gi.gi_sssp_batch_peers(G, srcs[lo:hi], 50 if g.n == 1001 else 1000,
+                                   peer_row_addresses(bases, lo, g.n), r)
+        torch.cuda.synchronize()
+        for m in mats:
+            assert np.array_equal(gi.as_uint32(m), ref)
+        with pytest.raises(gi.GiError):
+            gi.gi_sssp_batch_peers(G, srcs[:2], 10, bases, 2)  # self out of range
+        with pytest.raises(gi.GiError):
+            gi.gi_sssp_batch_peers(G, srcs[:2], 10, [bases[0], 0], 0)  # NULL peer row
+
+
+def _peers_worker(rank, world, port, q):
+    import socket  # noqa: F401
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_1911_07260_b200 import gi as m
+    from paper_1911_07260_b200.dist import sssp_batch_fused_gather
+    g = gen.config_graph(1)
+    G = m.Graph.from_csr(g)
+    srcs = gen.sources(g.n, 10, 5).astype(np.int32)
+    full = sssp_batch_fused_gather(G, srcs, 1000)
+    torch.cuda.synchronize()
+    q.put((rank, m.as_uint32(full)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_batch_peers_ipc_two_processes(gi):
+    """The fused gather across processes (CUDA IPC handles exchanged over a gloo group):
+    two ranks on this one GPU — their kernels do not wait on each other, each only writes
+    its finished rows into the other's matrix — and both end with all 10 rows."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_peers_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    g = gen.config_graph(1)
+    srcs = gen.sources(g.n, 10, 5).astype(np.int32)
+    ref, _ = oracle.dijkstra_many(g, srcs)[:2]
+    for r in (0, 1):
+        assert np.array_equal(res[r], ref), r

@@ -14,10 +14,16 @@ ap.add_argument("--threshold", type=int, default=0)
 ap.add_argument("--max-ctas", type=int, default=0)
 ap.add_argument("--pre-read", type=int, default=0)
 ap.add_argument("--drain", default="auto")
+ap.add_argument("--kcore", action="store_true", help="run k-core instead of SSSP")
 a = ap.parse_args()
 g = gen.config_graph(a.config) if a.config else gen.path(20000)
 G = gi.Graph.from_csr(g)
 src = gen.config_source(a.config, g) if a.config else 0
+if a.kcore:
+    for i in range(a.reps):
+        core, st = gi.kcore(G)
+        print(i, "kcore", {k: st[k] for k in ("gpu_ms", "buckets", "rounds", "fused_subrounds", "spills")})
+    sys.exit(0)
 if a.config == 5:  # the 64-source batch
     srcs = gen.config_sources(5, g, 64)
     for i in range(a.reps):
