@@ -303,7 +303,9 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   // 512 otherwise (the latency-bound chains of road graphs); gi_options.cta_threads overrides
   if (opt.cta_threads != 0 && opt.cta_threads != 512 && opt.cta_threads != 1024)
     return fail(GI_ERR_INVALID_ARGUMENT, "cta_threads must be 0, 512 or 1024");
-  const int wide = opt.cta_threads ? (opt.cta_threads == 1024) : (g->max_deg > 32 ? 1 : 0);
+  // (a batch of >= 8 sources is throughput-bound: 1024 threads there too — config 5,
+  // 64 sources: 207 ms against 225 ms with 512)
+  const int wide = opt.cta_threads ? (opt.cta_threads == 1024) : (g->max_deg > 32 || (batch && nsrc >= 8) ? 1 : 0);
   const int bps = g->bps[wide][kind];
   int total = g->sm_count * bps;
   // group sizing: single source -> one group of every CTA (capped by max_ctas);
