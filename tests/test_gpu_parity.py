@@ -508,3 +508,37 @@ def test_batch_peers_ipc_two_processes(gi):
     ref, _ = oracle.dijkstra_many(g, srcs)[:2]
     for r in (0, 1):
         assert np.array_equal(res[r], ref), r
+
+
+def test_concurrent_host_threads_one_graph(gi, config_graph):
+    """SURVEY §8(b) semantics: the graph is immutable and each call takes its own workspace
+    (and stream), so queries from several host threads on one graph may overlap — their
+    persistent kernels are cooperative launches, each co-resident as a whole. Every result
+    must still be bit-exact."""
+    import threading
+    g = config_graph(1)
+    G = gi.Graph.from_csr(g)
+    srcs = [0, 777, 31337, 65535, 4242, 12]
+    refs = {s: oracle.dijkstra(g, s)[0] for s in srcs}
+    errors = []
+
+    def worker(i):
+        try:
+            for rep in range(3):
+                s = srcs[(i + rep) % len(srcs)]
+                d, _ = run(gi, G, s, 1000, fusion=bool((i + rep) % 2))
+                if not np.array_equal(d, refs[s]):
+                    errors.append((i, rep, s))
+            out, _ = gi.sssp_batch(G, np.array(srcs[:3], np.int32), 1000)
+            if not np.array_equal(gi.as_uint32(out), np.stack([refs[s] for s in srcs[:3]])):
+                errors.append((i, "batch"))
+        except Exception as e:  # noqa: BLE001
+            errors.append((i, repr(e)))
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=120)
+    assert not any(t.is_alive() for t in ts), "a query did not finish"
+    assert not errors, errors
