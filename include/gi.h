@@ -93,21 +93,24 @@ typedef struct {
   uint32_t struct_size;      /* = sizeof(gi_options) (ABI check) */
   int32_t fusion;            /* 1: bucket fusion (default); 0: one group-wide barrier per relax round */
   uint32_t fusion_threshold; /* T: a CTA-local current-bucket bin of size >= T spills to the global
-                                frontier (PAPER.md:539 strict '<'); 0 = library default */
+                                frontier (PAPER.md:539 strict '<'); 0 = library default; values
+                                above the bin capacity (2048 at 512 threads, 4096 at 1024) are
+                                clamped to it */
   int32_t max_ctas;          /* cap on persistent CTAs per query group (0 = all co-resident) */
   uint32_t hub_min;          /* out-degree >= hub_min: the vertex's edges are split over every CTA of
-                                the group in the next phase (0 = default 4096; values < 1024 are
-                                raised to 1024) */
+                                the group in the next phase (0 = default 1024; values < 256 are
+                                raised to 256) */
   uint32_t drain;            /* fused drain of the CTA-local bucket: 0 = default (bsp), 1 = bsp (one
                                 CTA barrier per sub-round), 2 = async (barrier-free work ring;
                                 GI_ERR_UNSUPPORTED if some out-degree > 8); ignored without fusion */
-  int32_t group_ctas;        /* batch only: CTAs per concurrent query group (0 = auto) */
+  int32_t group_ctas;        /* batch only: CTAs per concurrent query group (0 = auto: one group per
+                                source, >= 2 CTAs each, capped by free memory for workspaces) */
   int32_t pre_read;          /* read dist[v] before atomicMin: 0 = auto (on when max out-degree > 32),
                                 1 = on, 2 = off */
   void* cuda_stream;         /* cudaStream_t to run on (NULL = library stream); calls still
                                 synchronise that stream before returning */
   int32_t cta_threads;       /* threads per persistent CTA: 0 = auto (1024 when the max out-degree
-                                is > 32, else 512), 512 or 1024 */
+                                is > 32 or for a batch of >= 8 sources, else 512), 512 or 1024 */
   int32_t reserved2;         /* must be 0 */
 } gi_options;
 

@@ -329,7 +329,9 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
       const int64_t hubcap = std::min<int64_t>(2 * (g->m / kMinHubMin) + 64, 0x7FFFFFFF);
       const size_t per = (size_t)(16 * g->n + 16 * nw) + 2 * (size_t)hubcap * sizeof(HubEnt) + sizeof(Ctl);
       size_t free_b = 0, total_b = 0;
-      if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+      // (cudaMemGetInfo costs milliseconds: asked only when new workspaces are needed)
+      const int want = std::min(total / G, nsrc);
+      if (want > w->cap_groups && cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
         const int maxg = w->cap_groups + std::max<int64_t>(1, (int64_t)(free_b / 2 / per));
         if (total / G > maxg) G = (total + maxg - 1) / maxg;
       }
@@ -410,8 +412,14 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   a.div = make_fastdiv(delta);
   a.hub_min = opt.hub_min ? std::max(opt.hub_min, kMinHubMin) : kDefaultHubMin;
   a.hubcap = w->hubcap;
-  a.T = opt.fusion_threshold ? opt.fusion_threshold : (g->max_deg > 32 ? kDefaultTSkewed : kDefaultT);
-  if (a.T > (uint32_t)kBinCap) a.T = kBinCap;
+  // threshold: a throughput-bound batch (>= 8 sources, small groups) keeps whole bins local
+  // up to the bin capacity (every spill costs a group round trip through the global frontier;
+  // config 5: T = 2048 183 ms against 207 ms at 1024, and 160 ms with T = 4096 in the
+  // 1024-thread kernel's bins); single queries use the measured defaults
+  const bool throughput = batch && nsrc >= 8;
+  a.T = opt.fusion_threshold ? opt.fusion_threshold
+                             : (g->max_deg > 32 ? kDefaultTSkewed : throughput ? (uint32_t)kBinCapW[wide] : kDefaultT);
+  if (a.T > (uint32_t)kBinCapW[wide]) a.T = kBinCapW[wide];
   if (kind == KIND_FUSED_ASYNC && a.T > kRingSafe) a.T = kRingSafe;
   // pre-read dist[v] before the atomic: pays off when hubs attract many redundant
   // relaxations (skewed degrees), costs one L2 round trip per level otherwise

@@ -14,7 +14,12 @@ constexpr uint32_t kInf = 0xFFFFFFFFu;
 #endif
 constexpr int kBlock = GI_BLOCK;     // threads per persistent CTA
 constexpr int kMinBlocksPerSm = GI_MINB;
-constexpr int kBinCap = 2048;        // CTA-local current-bucket bin of uint2 {v, d}; two (ping-pong) per CTA
+// CTA-local current-bucket bin of uint2 {v, d}; two (ping-pong) per CTA. By CTA width (512,
+// 1024): the 1024-thread kernel also runs the throughput-bound batches, whose bins are big
+// (config 5: 4096 against 2048 cut spills 3,647 -> 58 and 183 -> 160 ms; single queries
+// unchanged).
+constexpr int kBinCapW[2] = {2048, 4096};
+constexpr int kBinCap = kBinCapW[GI_BLOCK >= 1024 ? 1 : 0];
 constexpr int kBigCap = 2048;        // CTA-local list of high-degree vertices (deg > 8) per bin
 constexpr uint32_t kDefaultT = 1024; // fusion threshold default (vertices per CTA bin), max out-degree <= 32
 constexpr uint32_t kDefaultTSkewed = 256;  // ... and on skewed graphs (max out-degree > 32); DESIGN.md §10

@@ -13,7 +13,10 @@ g = gen.config_graph(cfg)
 src = gen.config_source(cfg, g)
 srcs = gen.config_sources(5, g, 64).astype(np.int32) if cfg == 5 else None
 out = torch.empty((64 if cfg == 5 else 1) * g.n, dtype=torch.int32, device="cuda")
-for so in sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ.get("AB_DIR", "ab"), "libgi_*.so"))):
+libs = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ.get("AB_DIR", "ab"), "libgi_*.so")))
+if os.environ.get("AB_ONLY"):  # one library per process: no second-instance placement effect
+    libs = [x for x in libs if os.path.basename(x) == f"libgi_{os.environ['AB_ONLY']}.so"]
+for so in libs:
     lib = ctypes.CDLL(so)
     vp = ctypes.c_void_p
     lib.gi_graph_create.argtypes = [ctypes.c_int64, ctypes.c_int64, vp, vp, vp, ctypes.c_int, ctypes.POINTER(vp)]
