@@ -68,6 +68,9 @@ struct Workspace {
   uint32_t* d_stage = nullptr;  // staging for host dist_out
   size_t stagecap = 0;
   uint32_t* d_src_next = nullptr;  // batch source claim counter
+  int32_t* h_srcs = nullptr;     // pinned staging: sources (H2D) and statistics (D2H), so the
+  QStats* h_qstats = nullptr;    // per-call copies are asynchronous (no pageable staging)
+  int hcap_q = 0;
   uint32_t** d_peers = nullptr;  // gi_sssp_batch_peers: device copy of the peer row bases
   int peercap = 0;
   uint32_t* d_h = nullptr;      // staging for a host A* heuristic
@@ -86,6 +89,8 @@ struct Workspace {
     if (d_stage) cudaFree(d_stage);
     if (d_h) cudaFree(d_h);
     if (d_peers) cudaFree(d_peers);
+    if (h_srcs) cudaFreeHost(h_srcs);
+    if (h_qstats) cudaFreeHost(h_qstats);
     if (d_src_next) cudaFree(d_src_next);
     if (kc_prio) cudaFree(kc_prio);
     if (kc_ctl) cudaFree(kc_ctl);
@@ -392,7 +397,18 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
       d_h = w->d_h;
     }
   }
-  if ((e = cudaMemcpyAsync(w->d_srcs, hsrc.data(), sizeof(int32_t) * nsrc, cudaMemcpyHostToDevice, st)))
+  if (w->hcap_q < nsrc) {
+    if (w->h_srcs) cudaFreeHost(w->h_srcs);
+    if (w->h_qstats) cudaFreeHost(w->h_qstats);
+    w->h_srcs = nullptr;
+    w->h_qstats = nullptr;
+    w->hcap_q = 0;
+    if ((e = cudaMallocHost(&w->h_srcs, sizeof(int32_t) * nsrc)) != cudaSuccess) return bail(e, "alloc pinned srcs");
+    if ((e = cudaMallocHost(&w->h_qstats, sizeof(QStats) * nsrc)) != cudaSuccess) return bail(e, "alloc pinned stats");
+    w->hcap_q = nsrc;
+  }
+  memcpy(w->h_srcs, hsrc.data(), sizeof(int32_t) * nsrc);
+  if ((e = cudaMemcpyAsync(w->d_srcs, w->h_srcs, sizeof(int32_t) * nsrc, cudaMemcpyHostToDevice, st)))
     return bail(e, "copy srcs");
   if ((e = cudaMemsetAsync(w->d_qstats, 0, sizeof(QStats) * nsrc, st))) return bail(e, "memset qstats");
   if (!w->d_src_next && (e = cudaMalloc(&w->d_src_next, sizeof(uint32_t)))) return bail(e, "alloc claim counter");
@@ -453,8 +469,8 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   if ((e = wide ? v1024::launch_sssp(a, kind, G * ngroups, st) : v512::launch_sssp(a, kind, G * ngroups, st)))
     return bail(e, "launch sssp_persistent");
   if ((e = cudaEventRecord(w->ev1, st))) return bail(e, "event");
-  std::vector<QStats> hq(nsrc);
-  if ((e = cudaMemcpyAsync(hq.data(), w->d_qstats, sizeof(QStats) * nsrc, cudaMemcpyDeviceToHost, st)))
+  QStats* hq = w->h_qstats;
+  if ((e = cudaMemcpyAsync(hq, w->d_qstats, sizeof(QStats) * nsrc, cudaMemcpyDeviceToHost, st)))
     return bail(e, "copy stats");
   if (ppsp) {
     if ((e = cudaMemcpyAsync(dist_out, d_dist + target, 4, dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
@@ -467,13 +483,12 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   if ((e = cudaStreamSynchronize(st))) return bail(e, "sssp kernel");
   float ms = 0.f;
   cudaEventElapsedTime(&ms, w->ev0, w->ev1);
-  ws_release(g, w, true);
-
   bool ovf = false;
-  for (int i = 0; i < nsrc; ++i) {
+  for (int i = 0; i < nsrc; ++i) {  // hq is the workspace's pinned buffer: read before release
     if (hq[i].overflow) ovf = true;
     if (stats) fill_stats(&stats[i], hq[i], ms, G, ngroups, base_kind(kind), wide ? 1024 : 512);
   }
+  ws_release(g, w, true);
   if (ovf) return fail(GI_ERR_OVERFLOW, "a reachable vertex has distance >= UINT32_MAX");
   return GI_OK;
 }
