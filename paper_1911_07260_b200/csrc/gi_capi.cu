@@ -836,6 +836,7 @@ gi_status gi_kcore_ex(const gi_graph* cg_, const gi_options* opt_in, uint32_t* c
     stats->empty_extractions = hs.empty;
     stats->fused_subrounds = hs.subrounds;
     stats->spills = hs.spills;
+    stats->critical_subrounds = hs.critical;
     stats->gpu_ms = ms;
     stats->ctas = grid;
     stats->threads_per_cta = 512;

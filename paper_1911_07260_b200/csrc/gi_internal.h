@@ -1,5 +1,6 @@
 // gi_internal.h — structures shared by the sm_100a kernels and the host engine.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -143,13 +144,16 @@ struct alignas(128) KcCtl {
   uint32_t qclaim[3];   // ROUND: next unclaimed frontier position, by phase mod 3
   uint32_t xfin[3];     // vertices finished by an extraction, by extraction mod 3
   uint32_t hcount[3];   // group hub-list sizes, by phase mod 3
-  uint32_t pad0[14];
+  uint32_t maxsub[3];   // max fused sub-rounds of any CTA, by phase mod 3 (critical-path stat)
+  uint32_t pad0[11];
   uint32_t bar;         // group barrier word, own 128 B line
   uint32_t pad1[31];
 };
 
+static_assert(offsetof(KcCtl, bar) == 128, "the k-core barrier word owns its 128-byte line");
+
 struct KcStats {
-  unsigned long long buckets, rounds, phases, vertices, edges, empty, subrounds, spills;
+  unsigned long long buckets, rounds, phases, vertices, edges, empty, subrounds, spills, critical;
 };
 
 struct KcArgs {

@@ -52,6 +52,8 @@ struct KcShared {
   uint32_t bincnt[3];           // local bin fills, rotating by drain iteration
   unsigned long long total;
   unsigned long long red[kKcBlock / 32];
+  uint32_t woff[kKcBlock / 32];  // extraction: per-warp offsets of the kept entries
+  uint32_t pbase;                // extraction: this CTA's slot in the next pile
 };
 
 struct KcSmem {
@@ -288,6 +290,7 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
   KcCtx c;
   c.nfin = 0; c.nedge = 0;
   unsigned long long buckets = 0, rounds = 0, phases = 0, empty = 0, subrounds = 0, spills = 0;
+  unsigned long long critical = 0, sub0 = 0;  // sum over phases of the busiest CTA's sub-rounds
   uint32_t p = 0, j = 0, k = 0, prev = KC_DONE;
   for (;;) {
     if (tid == 0) {
@@ -296,6 +299,7 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
       if (prev == KC_EXTRACT) {
         if (__ldcg(&ctl->xfin[j % 3])) ++buckets; else ++empty;
       }
+      if (p > 0 && rank == 0) critical += __ldcg(&ctl->maxsub[(p - 1) % 3]);
       const uint32_t qn = __ldcg(&ctl->qcount[p % 3]);
       const uint32_t hn = __ldcg(&ctl->hcount[p % 3]);
       const uint32_t pc = __ldcg(&ctl->pcount[j % 3]);
@@ -318,6 +322,7 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
       ctl->qcount[(p + 2) % 3] = 0;
       ctl->hcount[(p + 2) % 3] = 0;
       ctl->qclaim[(p + 1) % 3] = 0;  // last used in phase p-2, which every CTA has left
+      ctl->maxsub[(p + 2) % 3] = 0;  // read above (rank 0 only), rewritten from phase p+2 on
       if (mode == KC_EXTRACT) {
         ctl->pcount[(j + 1) % 3] = 0; ctl->kmin[(j + 1) % 3] = kUnset; ctl->xfin[(j + 1) % 3] = 0;
       } else {
@@ -356,6 +361,7 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
           cc[x] = v[x] >= 0 ? ld_cg(a.core + v[x]) : 0u;
           pr[x] = v[x] >= 0 ? ld_cg(a.prio + v[x]) : 0u;
         }
+        uint32_t keepm = 0;
 #pragma unroll
         for (int x = 0; x < X; ++x) {
           const bool live = v[x] >= 0 && cc[x] == kUnset;  // finished entries are dropped
@@ -364,10 +370,37 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
           const bool fin = live && pr[x] <= k && atomicCAS(a.core + v[x], kUnset, k) == kUnset;
           const bool keep = live && pr[x] > k;
           if (fin) { ++c.nfin; ++nx; }
-          if (keep) c.my_kmin = min(c.my_kmin, pr[x]);
+          if (keep) { c.my_kmin = min(c.my_kmin, pr[x]); keepm |= 1u << x; }
           kc_push(c, fin, v[x]);
-          kc_append(keep, v[x], pile_live, pcount_live);
         }
+        // kept entries -> the next pile with ONE global atomic per CTA per iteration: every
+        // CTA appends to the same counter, and per-warp atomics (one per 32 entries)
+        // serialised on it (config 2 keeps ~16 M entries per extraction)
+        uint32_t mk[X], pre[X], wtot = 0;
+#pragma unroll
+        for (int x = 0; x < X; ++x) {
+          mk[x] = __ballot_sync(0xffffffffu, (keepm >> x) & 1u);
+          pre[x] = wtot;
+          wtot += __popc(mk[x]);
+        }
+        if (lane == 0) s.woff[tid >> 5] = wtot;
+        __syncthreads();
+        if (tid == 0) {
+          uint32_t run = 0;
+          for (int w = 0; w < kKcBlock / 32; ++w) {
+            const uint32_t t = s.woff[w];
+            s.woff[w] = run;
+            run += t;
+          }
+          s.pbase = run ? atomicAdd(pcount_live, run) : 0u;
+        }
+        __syncthreads();
+        const uint32_t wb = s.pbase + s.woff[tid >> 5];
+        const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+        for (int x = 0; x < X; ++x)
+          if ((keepm >> x) & 1u) pile_live[wb + pre[x] + __popc(mk[x] & lt)] = v[x];
+        __syncthreads();  // s.woff / s.pbase are rewritten next iteration
       }
       nx = __reduce_add_sync(0xffffffffu, nx);
       if (lane == 0 && nx) atomicAdd(&ctl->xfin[j % 3], nx);
@@ -436,6 +469,10 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
       kc_relax_entries(a, s, sm, c, nin);  // ends with a barrier
     }
 
+    if (tid == 0 && subrounds != sub0) {
+      atomicMax(&ctl->maxsub[p % 3], (uint32_t)(subrounds - sub0));
+      sub0 = subrounds;
+    }
     // next k: the exact minimum priority of the unfinished vertices (kept entries and
     // every non-crossing decrement), warp min -> smem -> one global atomic per CTA
     const uint32_t km = __reduce_min_sync(0xffffffffu, c.my_kmin);
@@ -457,6 +494,7 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
     if (spills) atomicAdd(&a.stats->spills, spills);
     if (rank == 0) {
       a.stats->buckets = buckets; a.stats->rounds = rounds; a.stats->phases = phases + 1; a.stats->empty = empty;
+      a.stats->critical = critical;
     }
   }
 }

@@ -22,7 +22,8 @@ src = gen.config_source(a.config, g) if a.config else 0
 if a.kcore:
     for i in range(a.reps):
         core, st = gi.kcore(G)
-        print(i, "kcore", {k: st[k] for k in ("gpu_ms", "buckets", "rounds", "fused_subrounds", "spills")})
+        print(i, "kcore", {k: st[k] for k in ("gpu_ms", "buckets", "rounds", "grid_syncs", "fused_subrounds",
+                                              "critical_subrounds", "spills")})
     sys.exit(0)
 if a.config == 5:  # the 64-source batch
     srcs = gen.config_sources(5, g, 64)
