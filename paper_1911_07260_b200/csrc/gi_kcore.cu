@@ -41,7 +41,10 @@ namespace cg = cooperative_groups;
 constexpr int kKcBlock = 512;
 constexpr int kKcEdges = 8;     // consecutive edges per thread per iteration
 constexpr int kKcChunk = 2048;  // frontier vertices staged per claim / per local bin (max)
-constexpr uint32_t kKcT = 1024; // bucket fusion threshold: a local bin of >= T vertices spills
+#ifndef GI_KCT
+#define GI_KCT 1024
+#endif
+constexpr uint32_t kKcT = GI_KCT; // bucket fusion threshold: a local bin of >= T vertices spills
 constexpr uint32_t kKcHub = 1024;  // out-degree >= this: edges split over every CTA in the next round
 constexpr uint32_t kUnset = 0xFFFFFFFFu;
 
