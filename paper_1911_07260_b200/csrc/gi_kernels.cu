@@ -89,6 +89,9 @@ constexpr uint32_t kClaimsPerCta = GI_CLAIMS;  // ROUND: ~claims per CTA per pha
 constexpr uint32_t kMaxClaim = GI_MAXCLAIM;
   // drain: spill a bin's big list above this
 
+#ifndef GI_LANE_PUSH
+#define GI_LANE_PUSH 1
+#endif
 #ifdef GI_TRACE
 // Debug builds only: cycles between trace points, accumulated by CTA 0 / thread 0 in
 // shared memory (so that tracing adds ~no latency) and flushed at kernel exit.
@@ -419,7 +422,22 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
   uint32_t ovm = FUSED ? 0u : curm;  // current-bucket pushes bound for the global frontier
-  if constexpr (FUSED) {
+  if constexpr (FUSED && GI_LANE_PUSH) {
+    // one shared atomic per pushing lane: no ballot -> warp atomic -> shuffle chain on the
+    // critical path of a level (a bin sub-round pushes a handful of vertices per warp)
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if ((curm >> k) & 1u) {
+        const uint32_t pos = atomicAdd(c.outcnt, 1u);
+        if (pos < (uint32_t)kBinCap) {
+          if (!GI_X_NOPF) prefetch_own(c.slots + 8 * (size_t)e[k].x);
+          c.out[pos] = make_uint2(e[k].x, nd[k]);
+        } else {
+          ovm |= 1u << k;
+        }
+      }
+    }
+  } else if constexpr (FUSED) {
     uint32_t mk[K], pre[K], tot = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
