@@ -41,6 +41,9 @@ namespace cg = cooperative_groups;
 constexpr int kKcBlock = 512;
 constexpr int kKcEdges = 8;     // consecutive edges per thread per iteration
 constexpr int kKcChunk = 2048;  // frontier vertices staged per claim / per local bin (max)
+#ifndef GI_KC_LANE_PUSH
+#define GI_KC_LANE_PUSH 1
+#endif
 #ifndef GI_KCT
 #define GI_KCT 1024
 #endif
@@ -97,6 +100,16 @@ __device__ __forceinline__ void kc_append(bool want, int32_t v, int32_t* list, u
 // fusion: drained in this phase, no group barrier) or, when the bin is full, the global
 // frontier (the next group-wide round). Called by all 32 lanes.
 __device__ __forceinline__ void kc_push(KcCtx& c, bool want, int32_t v) {
+  if (GI_KC_LANE_PUSH) {  // one shared atomic per pushing lane (as SSSP's bin pushes)
+    bool spill = false;
+    if (want) {
+      const uint32_t pos = atomicAdd(c.outcnt, 1u);
+      spill = pos >= (uint32_t)kKcChunk;
+      if (!spill) c.out[pos] = v;
+    }
+    kc_append(spill, v, c.q_next, c.qcount_next);
+    return;
+  }
   const uint32_t m = __ballot_sync(0xffffffffu, want);
   if (!m) return;
   const uint32_t lane = threadIdx.x & 31;
