@@ -78,6 +78,16 @@ def test_error_paths_without_gpu(gi):
     assert lib.gi_sssp_delta(None, 0, 1, d.ctypes.data) == 1
     assert lib.gi_graph_info(None, None, None, None) == 1
     lib.gi_graph_destroy(None)  # NULL-safe
+    # the fused-gather batch and the IPC helpers: argument errors before any device work
+    peers = (ctypes.c_void_p * 2)(None, None)
+    assert lib.gi_sssp_batch_peers(None, None, 0, 1, None, peers, 2, 0, None) == 1  # NULL peer rows
+    assert lib.gi_sssp_batch_peers(None, None, 0, 1, None, peers, 0, 0, None) == 1  # npeers < 1
+    assert lib.gi_sssp_batch_peers(None, None, 0, 1, None, peers, 2, 2, None) == 1  # self out of range
+    hbuf = (ctypes.c_uint8 * 64)()
+    off64 = ctypes.c_uint64()
+    assert lib.gi_ipc_get_handle(None, hbuf, ctypes.byref(off64)) == 1
+    assert lib.gi_ipc_open_handle(None, 0, 0, None) == 1
+    assert lib.gi_ipc_close_handle(None, 0, 0) == 1
     import torch
     if not torch.cuda.is_available():
         rc = lib.gi_graph_create(1, 1, off.ctypes.data, cols.ctypes.data, w.ctypes.data, 0, ctypes.byref(h))
