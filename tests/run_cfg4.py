@@ -2,7 +2,7 @@
 generate (host, gen/), upload, Δ-stepping at Δ=2 (fused and unfused), then parity:
 the C certificate over every edge (C0∧C1∧C2 <=> exact for w >= 1) and the
 full CPU Dijkstra oracle compared element by element. Prints one JSON line.
-usage: python tools/run_cfg4.py [--no-oracle] [--reps 3]"""
+usage: python tests/run_cfg4.py [--no-oracle] [--reps 3]"""
 import argparse
 import json
 import os
