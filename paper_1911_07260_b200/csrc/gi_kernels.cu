@@ -89,6 +89,9 @@ constexpr uint32_t kClaimsPerCta = GI_CLAIMS;  // ROUND: ~claims per CTA per pha
 constexpr uint32_t kMaxClaim = GI_MAXCLAIM;
   // drain: spill a bin's big list above this
 
+#ifndef GI_LANE_FAR
+#define GI_LANE_FAR 1
+#endif
 #ifndef GI_LANE_PUSH
 #define GI_LANE_PUSH 1
 #endif
@@ -477,7 +480,20 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
       if (((ovm >> k) & 1u) && !(ob[k] & (1u << (e[k].x & 31)))) newm |= 1u << k;
     warp_append(newm, vv, c.q_next, c.qcount_next, c.slots);
   }
-  {
+  if (LD && GI_LANE_FAR) {
+    // low-degree graphs: far pushes are few per warp; one shared atomic per pushing lane on
+    // the warp's segment counter, and the rare overflow goes straight to the global pile
+    const uint32_t warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if ((farm >> k) & 1u) {
+        c.my_fmin = min(c.my_fmin, bk[k]);
+        const uint32_t pos = atomicAdd(&c.s->wfar[warp], 1u);
+        if (pos < (uint32_t)kFarSeg) c.farstage[warp * kFarSeg + pos] = (int32_t)e[k].x;
+        else push_far_global(c, (int32_t)e[k].x);
+      }
+    }
+  } else {
     uint32_t mk[K], pre[K], tot = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -1461,7 +1477,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           bulk_append(nf, [&](uint32_t i) { return fs[i]; }, c.farbits, c.far_live, c.fcount_live, nullptr);
         } else {  // each warp flushes its own segment
           const uint32_t w = tid >> 5;
-          warp_flush_far(c, c.farstage + w * kFarSeg, s.wfar[w]);
+          warp_flush_far(c, c.farstage + w * kFarSeg, min(s.wfar[w], (uint32_t)kFarSeg));
         }
         uint32_t fm = __reduce_min_sync(0xffffffffu, c.my_fmin);
         if ((tid & 31) == 0 && fm != kInf) atomicMin(&s.fmin, fm);
