@@ -466,7 +466,14 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
       }
     }
   }
-  if (__any_sync(0xffffffffu, ovm != 0)) {  // dedup (qbits) with every atomic in flight, one append per warp
+  if (FUSED && LD && GI_LANE_FAR) {
+    // a full bin (rare on low-degree graphs): per-lane global pushes, no warp vote on the path
+    if (ovm) {
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if ((ovm >> k) & 1u) push_global(c, (int32_t)e[k].x);
+    }
+  } else if (__any_sync(0xffffffffu, ovm != 0)) {  // dedup (qbits) with every atomic in flight, one append per warp
     uint32_t ob[K];
     int32_t vv[K];
 #pragma unroll
