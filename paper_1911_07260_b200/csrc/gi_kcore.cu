@@ -100,14 +100,22 @@ __device__ __forceinline__ void kc_append(bool want, int32_t v, int32_t* list, u
 // fusion: drained in this phase, no group barrier) or, when the bin is full, the global
 // frontier (the next group-wide round). Called by all 32 lanes.
 __device__ __forceinline__ void kc_push(KcCtx& c, bool want, int32_t v) {
-  if (GI_KC_LANE_PUSH) {  // one shared atomic per pushing lane (as SSSP's bin pushes)
-    bool spill = false;
+  if (GI_KC_LANE_PUSH) {
+    // one shared atomic per pushing lane (as SSSP's bin pushes), and a full bin spills per
+    // lane too: no warp-collective operation after the decrements (a lane would wait for
+    // the warp's slowest atomic before pushing)
     if (want) {
       const uint32_t pos = atomicAdd(c.outcnt, 1u);
-      spill = pos >= (uint32_t)kKcChunk;
-      if (!spill) c.out[pos] = v;
+      if (pos < (uint32_t)kKcChunk) {
+        c.out[pos] = v;
+      } else {
+        cg::coalesced_group g = cg::coalesced_threads();
+        uint32_t base = 0;
+        if (g.thread_rank() == 0) base = atomicAdd(c.qcount_next, g.size());
+        base = g.shfl(base, 0);
+        c.q_next[base + g.thread_rank()] = v;
+      }
     }
-    kc_append(spill, v, c.q_next, c.qcount_next);
     return;
   }
   const uint32_t m = __ballot_sync(0xffffffffu, want);
