@@ -23,6 +23,15 @@ for graph, s in ((g, 100), (r, gen.max_degree_vertex(r))):
         h = gen.grid_heuristic(64, 64, 7, 1)
         assert gi.astar(G, s, 7, 50, h)[0] == int(ref[7])
     out, _ = gi.sssp_batch(G, np.array([s, 0, 5], np.int32), 50)
+    many = np.arange(10, dtype=np.int32)  # >= 8 sources: the throughput configuration (1024 threads, big bins)
+    outm, _ = gi.sssp_batch(G, many, 50)
+    import torch
+    mats = [torch.zeros((3, graph.n), dtype=torch.int32, device="cuda") for _ in range(2)]
+    for rr, (lo, hi) in enumerate(((0, 2), (2, 3))):  # the fused gather, two ranks in one process
+        gi.gi_sssp_batch_peers(G, np.array([s, 0, 5], np.int32)[lo:hi], 50,
+                               [m.data_ptr() + lo * graph.n * 4 for m in mats], rr)
+    torch.cuda.synchronize()
+    assert all(np.array_equal(gi.as_uint32(m), gi.as_uint32(out)) for m in mats)
     assert gi.ppsp(G, s, 3, 50)[0] == int(ref[3])
     core, _ = gi.kcore(G)
     assert np.array_equal(gi.as_uint32(core), oracle.kcore(graph))
