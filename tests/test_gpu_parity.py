@@ -542,3 +542,17 @@ def test_concurrent_host_threads_one_graph(gi, config_graph):
         t.join(timeout=120)
     assert not any(t.is_alive() for t in ts), "a query did not finish"
     assert not errors, errors
+
+
+def test_single_cta_overflow_paths(gi):
+    """One or two CTAs on a 512x512 grid: a sub-round pushes more vertices than a bin holds
+    (the per-lane full-bin fallback to the global frontier) and a warp stages more far-pile
+    entries in one phase than its segment holds (the per-lane fallback to the global pile).
+    Distances must still be bit-exact."""
+    g = gen.grid(512, 512, 1, 100, 21, p_del=0.05, p_diag=0.02)
+    G = gi.Graph.from_csr(g)
+    ref, _ = oracle.dijkstra(g, 0)
+    for o, delta in ((dict(max_ctas=1, threshold=2048), 10**9), (dict(max_ctas=1), 64),
+                     (dict(max_ctas=2, threshold=2048), 16), (dict(max_ctas=1, cta_threads=1024), 10**9)):
+        d, _ = run(gi, G, 0, delta, **o)
+        assert np.array_equal(d, ref), (o, delta)
