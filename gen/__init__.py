@@ -228,6 +228,38 @@ CONFIG_DELTAS = {
 
 
 def config_graph(cfg: int) -> CSR:
+    """The config's canonical graph. With GI_GEN_CACHE=<dir> set (measurement tools only),
+    the CSR is kept there as .npy files and memory-mapped on later calls."""
+    cache = os.environ.get("GI_GEN_CACHE")
+    if cache:
+        base = os.path.join(cache, f"cfg{2 if cfg == 5 else cfg}")
+        names = ("offsets", "cols", "w")
+        if all(os.path.exists(f"{base}_{k}.npy") for k in names):
+            arrs = [np.load(f"{base}_{k}.npy", mmap_mode="r") for k in names]
+            g = _config_graph(cfg, meta_only=True)
+            return CSR(arrs[0], arrs[1], arrs[2], g.name, g.meta)
+        g = _config_graph(cfg)
+        os.makedirs(cache, exist_ok=True)
+        for k in names:
+            np.save(f"{base}_{k}.npy", getattr(g, k))
+        return g
+    return _config_graph(cfg)
+
+
+_CONFIG_META = {
+    1: ("cfg1_grid256", dict(kind="grid", rows=256, cols=256, w_lo=1, w_hi=1000, seed=1, p_del=0.0, p_diag=0.0)),
+    2: ("cfg2_road4096", dict(kind="grid", rows=4096, cols=4096, w_lo=1, w_hi=10000, seed=2, p_del=0.05,
+                              p_diag=0.01)),
+    3: ("cfg3_rmat22", dict(kind="rmat", scale=22, edge_factor=16, w_lo=1, w_hi=22, seed=3)),
+    4: ("cfg4_rmat26", dict(kind="rmat", scale=26, edge_factor=16, w_lo=1, w_hi=26, seed=4)),
+}
+
+
+def _config_graph(cfg: int, meta_only: bool = False) -> CSR:
+    if meta_only:
+        name, meta = _CONFIG_META[2 if cfg == 5 else cfg]
+        e = np.zeros(0, np.int32)
+        return CSR(np.zeros(1, np.int64), e, e.view(np.uint32), name, dict(meta))
     if cfg == 1:
         return grid(256, 256, 1, 1000, 1, name="cfg1_grid256")
     if cfg in (2, 5):

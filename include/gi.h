@@ -111,7 +111,10 @@ typedef struct {
                                 synchronise that stream before returning */
   int32_t cta_threads;       /* threads per persistent CTA: 0 = auto (1024 when the max out-degree
                                 is > 32 or for a batch of >= 8 sources, else 512), 512 or 1024 */
-  int32_t reserved2;         /* must be 0 */
+  int32_t expand;            /* ROUND phases on skewed graphs: collect every frontier vertex of
+                                out-degree > 8 into one group list and relax the concatenation of
+                                their edges split evenly over all warps (edge-balanced, kernel (b)):
+                                0 = auto (on when the max out-degree is > 32), 1 = on, 2 = off */
 } gi_options;
 
 /* Counters of one query (SURVEY §8(a) "Counter definitions"). */
@@ -219,6 +222,25 @@ gi_status gi_astar_delta_ex(const gi_graph* g, int32_t src, int32_t dst, uint32_
  * edges_relaxed, gpu_ms; kernel_kind = 3. */
 gi_status gi_kcore(const gi_graph* g, uint32_t* core_out);
 gi_status gi_kcore_ex(const gi_graph* g, const gi_options* opt, uint32_t* core_out, gi_stats* stats);
+
+/* ---- measurement (bench.py; not part of a query) -------------------------------- */
+
+/* Latency floors of the dependent chains, measured on `device` (SURVEY.md §8(d) "Which
+ * roofline bounds the path": sync floor = grid_syncs x t_sync + launches x t_launch; chain
+ * floor = dependent levels x t_hop). t_sync: one group barrier of the persistent kernels
+ * (one CTA per SM, the barrier the fused drain avoids); t_hop: one
+ * dependent relaxation hop — an atomicMin on a random 4-byte word of a 64 MB array whose
+ * old value names the next word, with that vertex's 64-byte slot (1 GB array) loaded beside
+ * it, one chain per SM; t_launch: an empty kernel replayed from a CUDA graph. `iters`
+ * barriers / 4 x iters hops are timed with CUDA events. Allocates ~1.1 GB for the call. */
+typedef struct {
+  float t_sync_us;
+  float t_hop_us;
+  float t_launch_us;
+  float sm_clock_mhz; /* cudaDevAttrClockRate (the maximum clock, not the one under load) */
+  int32_t ctas;       /* CTAs in the barrier probe (one per SM) */
+} gi_floors;
+gi_status gi_probe_floors(int32_t device, int32_t iters, gi_floors* out);
 
 /* Thread-local description of the last non-OK status returned on this thread. */
 const char* gi_last_error(void);

@@ -60,11 +60,13 @@ def _L():
         _lib = ctypes.CDLL(build())
         vp, i64 = ctypes.c_void_p, ctypes.c_int64
         _lib.oracle_dijkstra.argtypes = [i64, vp, vp, vp, ctypes.c_int32, vp]
+        _lib.oracle_dijkstra_budget.argtypes = [i64, vp, vp, vp, ctypes.c_int32, vp, ctypes.c_double,
+                                                ctypes.POINTER(i64), ctypes.POINTER(i64)]
         _lib.oracle_bellman_ford.argtypes = [i64, vp, vp, vp, ctypes.c_int32, vp]
         _lib.oracle_transpose.argtypes = [i64, i64, vp, vp, vp, vp, vp, vp]
         _lib.oracle_certificate.argtypes = [i64, vp, vp, vp, vp, vp, vp, ctypes.c_int32, vp, vp]
         _lib.oracle_kcore.argtypes = [i64, vp, vp, vp]
-        for f in ("oracle_dijkstra", "oracle_bellman_ford", "oracle_transpose", "oracle_certificate",
+        for f in ("oracle_dijkstra", "oracle_dijkstra_budget", "oracle_bellman_ford", "oracle_transpose", "oracle_certificate",
                   "oracle_kcore"):
             getattr(_lib, f).restype = ctypes.c_int
     return _lib
@@ -86,6 +88,18 @@ def dijkstra(g, src: int):
     if rc < 0:
         raise ValueError(f"oracle_dijkstra rc={rc}")
     return dist, rc
+
+
+def dijkstra_budget(g, src: int, budget_s: float):
+    """Timing only (bench.py's bounded CPU baseline): the same Dijkstra, stopped after
+    budget_s seconds of wall time. Returns (vertices settled, out-edges scanned, status)."""
+    off, col, w = _arrs(g)
+    dist = np.empty(g.n, np.uint32)
+    settled, scanned = ctypes.c_int64(), ctypes.c_int64()
+    rc = _L().oracle_dijkstra_budget(g.n, off.ctypes.data, col.ctypes.data, w.ctypes.data, int(src),
+                                     dist.ctypes.data, float(budget_s) * 1e3, ctypes.byref(settled),
+                                     ctypes.byref(scanned))
+    return int(settled.value), int(scanned.value), rc
 
 
 def bellman_ford(g, src: int):

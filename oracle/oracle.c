@@ -29,9 +29,11 @@
  * source, hand-worked examples (tests/golden/), closed forms (Manhattan grid,
  * path), scipy.sparse.csgraph.dijkstra, and the certificate below.
  */
+#define _POSIX_C_SOURCE 199309L /* clock_gettime (timing budget only) */
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #define ORACLE_OK 0
 #define ORACLE_OVERFLOW 1
@@ -74,12 +76,24 @@ static void sift_down(heap_t* h, int64_t i) {
   }
 }
 
+static double now_ms(void) {
+  struct timespec t;
+  clock_gettime(CLOCK_MONOTONIC, &t);
+  return (double)t.tv_sec * 1e3 + (double)t.tv_nsec * 1e-6;
+}
+
 /* Dijkstra: D[v]=inf, D[s]=0; repeatedly extract the minimum-D vertex u and, for
  * each out-edge (u,v,w) in CSR order, lower D[v] to D[u]+w if smaller
  * (decrease-key). Output dist[v] = D[v] if finite (< UINT32_MAX), UINT32_MAX if
- * unreached; a finite D[v] >= UINT32_MAX returns ORACLE_OVERFLOW. */
-int oracle_dijkstra(int64_t n, const int64_t* off, const int32_t* col, const uint32_t* w,
-                    int32_t src, uint32_t* dist) {
+ * unreached; a finite D[v] >= UINT32_MAX returns ORACLE_OVERFLOW.
+ *
+ * budget_ms > 0 (timing only: bench.py's bounded cpu_baseline / reference sample) stops
+ * the loop after that much wall time; the vertices settled so far are final, the rest of
+ * dist is not. *settled / *scanned (nullable) receive the extracted vertices and the
+ * out-edges examined. The arithmetic is the same with or without a budget. */
+int oracle_dijkstra_budget(int64_t n, const int64_t* off, const int32_t* col, const uint32_t* w,
+                           int32_t src, uint32_t* dist, double budget_ms, int64_t* settled,
+                           int64_t* scanned) {
   if (n < 1 || src < 0 || src >= n || !off || !dist) return ORACLE_BAD_INPUT;
   heap_t h;
   h.size = 0;
@@ -93,13 +107,18 @@ int oracle_dijkstra(int64_t n, const int64_t* off, const int32_t* col, const uin
 
   h.key[src] = 0;
   h.heap[0] = src; h.pos[src] = 0; h.size = 1;
+  const double t0 = budget_ms > 0 ? now_ms() : 0.0;
+  int64_t pops = 0, edges = 0;
   while (h.size > 0) {
+    if (budget_ms > 0 && (pops & 1023) == 0 && pops > 0 && now_ms() - t0 > budget_ms) break;
+    ++pops;
     int32_t u = h.heap[0];
     heap_swap(&h, 0, h.size - 1);
     h.size--; h.pos[u] = -1;
     sift_down(&h, 0);
     done[u] = 1;
     uint64_t du = h.key[u];
+    edges += off[u + 1] - off[u];
     for (int64_t e = off[u]; e < off[u + 1]; ++e) {
       int32_t v = col[e];
       uint64_t nd = du + (uint64_t)w[e];
@@ -117,7 +136,14 @@ int oracle_dijkstra(int64_t n, const int64_t* off, const int32_t* col, const uin
     else dist[v] = (uint32_t)h.key[v];
   }
   free(h.heap); free(h.pos); free(h.key); free(done);
+  if (settled) *settled = pops;
+  if (scanned) *scanned = edges;
   return rc;
+}
+
+int oracle_dijkstra(int64_t n, const int64_t* off, const int32_t* col, const uint32_t* w,
+                    int32_t src, uint32_t* dist) {
+  return oracle_dijkstra_budget(n, off, col, w, src, dist, 0.0, NULL, NULL);
 }
 
 /* Brute-force Bellman-Ford (tiny graphs only; checks Dijkstra): n-1 full passes

@@ -111,6 +111,9 @@ struct gi_graph {
   uint2* d_slots = nullptr;  // ELL adjacency slots, 64 B per vertex
   void* d_arena = nullptr;   // one allocation holding offsets, edges and slots (2 MB-aligned parts)
   uint32_t max_deg = 0;
+  int64_t n_big = 0;             // vertices of out-degree > 8 (skewed graphs: expand list capacity)
+  uint32_t* d_pedges = nullptr;  // packed edges (w << colbits | col), skewed graphs whose weights fit
+  uint32_t colbits = 0;
   int sm_count = 0;
   int bps[2][KIND_COUNT] = {};  // co-resident CTAs per SM, by width (512, 1024) and KernelKind
   int bps_kcore = 0;
@@ -122,6 +125,7 @@ struct gi_graph {
   // device is the graph's (DeviceGuard) wherever this runs
   ~gi_graph() {
     pool.clear();
+    if (d_pedges) cudaFree(d_pedges);
     if (d_arena) {
       cudaFree(d_arena);
     } else {
@@ -154,6 +158,14 @@ gi_status dmalloc(T** p, size_t count, std::vector<void*>* track, const char* wh
   return GI_OK;
 }
 
+// Group hub-list capacity: every hub (deg >= 256) twice over, and on skewed graphs (expand)
+// every vertex of degree > 8 once more; entries past the capacity are relaxed CTA-locally.
+uint32_t hub_capacity(const gi_graph* g) {
+  int64_t cap = 2 * (g->m / kMinHubMin) + 64;
+  if (g->max_deg > 32) cap = std::max<int64_t>(cap, g->n_big + 2 * (g->m / kMinHubMin) + 64);
+  return (uint32_t)std::min<int64_t>(cap, 0x7FFFFFFF);
+}
+
 // Make a workspace with >= k groups, >= nsrc stats slots.
 gi_status ws_prepare(gi_graph* g, Workspace* w, int k, int nsrc) {
   const int64_t n = g->n;
@@ -161,9 +173,11 @@ gi_status ws_prepare(gi_graph* g, Workspace* w, int k, int nsrc) {
   w->n = n;
   // a vertex with deg >= kMinHubMin can appear at most m / kMinHubMin times ... per distinct
   // vertex; twice that covers re-queued entries, the rest fall back to CTA-local processing
-  w->hubcap = (uint32_t)std::min<int64_t>(2 * (g->m / kMinHubMin) + 64, 0x7FFFFFFF);
+  w->hubcap = hub_capacity(g);
   if (!w->stream) {
-    GI_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    // a BLOCKING stream: work on it is ordered with the legacy default stream, where torch
+    // (and most callers) queue the kernels that produce the inputs and consume dist_out
+    GI_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamDefault), "cudaStreamCreate");
     GI_CUDA(cudaEventCreate(&w->ev0), "cudaEventCreate");
     GI_CUDA(cudaEventCreate(&w->ev1), "cudaEventCreate");
   }
@@ -182,6 +196,12 @@ gi_status ws_prepare(gi_graph* g, Workspace* w, int k, int nsrc) {
       if ((s = dmalloc(&gw.ctl, 1, &w->allocs, "alloc ctl"))) return s;
       if ((s = dmalloc(&gw.hub[0], (size_t)w->hubcap, &w->allocs, "alloc hub list"))) return s;
       if ((s = dmalloc(&gw.hub[1], (size_t)w->hubcap, &w->allocs, "alloc hub list"))) return s;
+      gw.xpre = nullptr;
+      gw.xtot = nullptr;
+      if (g->max_deg > 32) {  // expand (skewed graphs)
+        if ((s = dmalloc(&gw.xpre, (size_t)w->hubcap, &w->allocs, "alloc expand prefix"))) return s;
+        if ((s = dmalloc(&gw.xtot, (size_t)kMaxGroupCtas, &w->allocs, "alloc expand totals"))) return s;
+      }
       // bitmaps start (and, after every completed query, end) all-zero
       GI_CUDA(cudaMemsetAsync(gw.farbits, 0, nwords * 4, w->stream), "memset");
       GI_CUDA(cudaMemsetAsync(gw.qbits[0], 0, nwords * 4, w->stream), "memset");
@@ -292,6 +312,7 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
 
   const bool fused = opt.fusion != 0;
   if (opt.drain > 2) return fail(GI_ERR_INVALID_ARGUMENT, "drain must be 0 (auto), 1 (bsp) or 2 (async)");
+  if (opt.expand < 0 || opt.expand > 2) return fail(GI_ERR_INVALID_ARGUMENT, "expand must be 0 (auto), 1 (on) or 2 (off)");
   if (heur && fused && opt.drain == 2) return fail(GI_ERR_UNSUPPORTED, "A* runs with the bsp drain (drain 0/1)");
   if (fused && opt.drain == 2 && g->max_deg > kAsyncMaxDeg)
     return fail(GI_ERR_UNSUPPORTED, "async drain needs max out-degree <= %u (graph has %u)", kAsyncMaxDeg,
@@ -331,8 +352,9 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
       // 5 (64 sources): 2 CTAs x 64 groups 228 ms, 16 x 9 258 ms, 3 x 49 266 ms.
       G = std::max(2, total / nsrc);
       const int64_t nw = (g->n + 31) / 32;
-      const int64_t hubcap = std::min<int64_t>(2 * (g->m / kMinHubMin) + 64, 0x7FFFFFFF);
-      const size_t per = (size_t)(16 * g->n + 16 * nw) + 2 * (size_t)hubcap * sizeof(HubEnt) + sizeof(Ctl);
+      const int64_t hubcap = hub_capacity(g);
+      const size_t per = (size_t)(16 * g->n + 16 * nw) + 2 * (size_t)hubcap * sizeof(HubEnt) +
+                         (g->max_deg > 32 ? (size_t)hubcap * 8 : 0) + sizeof(Ctl);
       size_t free_b = 0, total_b = 0;
       // (cudaMemGetInfo costs milliseconds: asked only when new workspaces are needed)
       const int want = std::min(total / G, nsrc);
@@ -436,12 +458,16 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   a.T = opt.fusion_threshold ? opt.fusion_threshold
                              : (g->max_deg > 32 ? kDefaultTSkewed : throughput ? (uint32_t)kBinCapW[wide] : kDefaultT);
   if (a.T > (uint32_t)kBinCapW[wide]) a.T = kBinCapW[wide];
-  if (kind == KIND_FUSED_ASYNC && a.T > kRingSafe) a.T = kRingSafe;
+  if (kind == KIND_FUSED_ASYNC && a.T > kRingSafeW[wide]) a.T = kRingSafeW[wide];
   // pre-read dist[v] before the atomic: pays off when hubs attract many redundant
   // relaxations (skewed degrees), costs one L2 round trip per level otherwise
   a.pre_read = opt.pre_read == 1 ? 1u : opt.pre_read == 2 ? 0u : (g->max_deg > 32 ? 1u : 0u);
   a.target = target;
   a.dyn_claim = g->max_deg > 32 ? 1u : 0u;
+  // expand needs the group list's prefix workspace (skewed graphs) and fits groups of <= 1024 CTAs
+  a.expand = (g->max_deg > 32 && opt.expand != 2 && G <= kMaxGroupCtas) ? 1u : 0u;
+  a.pedges = g->d_pedges;
+  a.colbits = g->colbits;
   if ((e = cudaMemsetAsync(w->d_src_next, 0, sizeof(uint32_t), st))) return bail(e, "init claim counter");
   a.src_next = w->d_src_next;  // claims count from 0; sources 0..ngroups-1 are taken statically
   a.h = d_h;
@@ -554,8 +580,8 @@ gi_status gi_graph_create(int64_t n, int64_t m, const int64_t* row_offsets, cons
       return fail(GI_ERR_CUDA, "persistent kernel variant %d cannot be resident", k);
   }
 
-  cudaStream_t st;
-  GI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  cudaStream_t st;  // blocking: ordered with the legacy default stream (device input arrays)
+  GI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamDefault), "stream");
   struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } sg{st};
 
   uint32_t* d_bad = nullptr;
@@ -623,6 +649,32 @@ gi_status gi_graph_create(int64_t n, int64_t m, const int64_t* row_offsets, cons
     GI_CUDA(launch_max_degree(g->d_off, n, d_maxdeg, st), "max degree");
     GI_CUDA(cudaMemcpyAsync(&g->max_deg, d_maxdeg, 4, cudaMemcpyDeviceToHost, st), "copy max degree");
     GI_CUDA(cudaStreamSynchronize(st), "graph build");
+    if (g->max_deg > 32) {
+      // skewed graph: the expand list capacity, and packed edges when the weights fit the
+      // bits a column id leaves free (config 4: 26-bit ids, weights < 26 < 2^6)
+      unsigned long long* d_cnt = nullptr;
+      GI_CUDA(cudaMalloc(&d_cnt, 16), "alloc");
+      FreeGuard fcnt{d_cnt};
+      GI_CUDA(cudaMemsetAsync(d_cnt, 0, 16, st), "memset");
+      GI_CUDA(launch_count_big(g->d_off, n, d_cnt, st), "count high-degree vertices");
+      uint32_t* d_mw = reinterpret_cast<uint32_t*>(d_cnt + 1);
+      GI_CUDA(launch_max_weight(g->d_edges, m, d_mw, st), "max weight");
+      unsigned long long hb[2] = {0, 0};
+      GI_CUDA(cudaMemcpyAsync(hb, d_cnt, 16, cudaMemcpyDeviceToHost, st), "copy counts");
+      GI_CUDA(cudaStreamSynchronize(st), "graph build");
+      g->n_big = (int64_t)hb[0];
+      const uint32_t max_w = (uint32_t)hb[1];
+      uint32_t colbits = 1;
+      while (colbits < 31 && (1ll << colbits) < n) ++colbits;
+      const char* pk = getenv("GI_PACK");
+      const bool want_pack = !(pk && pk[0] == '0');
+      if (want_pack && m > 0 && ((uint64_t)max_w >> (32 - colbits)) == 0) {
+        GI_CUDA(cudaMalloc(&g->d_pedges, sizeof(uint32_t) * (size_t)m), "alloc packed edges");
+        g->colbits = colbits;
+        GI_CUDA(launch_pack_edges(g->d_edges, g->d_pedges, m, colbits, st), "pack edges");
+        GI_CUDA(cudaStreamSynchronize(st), "graph build");
+      }
+    }
   }
   if (bad) {  // ~gi_graph frees the device memory
     return fail(GI_ERR_INVALID_GRAPH, "offsets not a valid CSR (offsets[0]=0, non-decreasing, offsets[n]=m) "

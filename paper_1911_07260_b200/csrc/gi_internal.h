@@ -35,7 +35,13 @@ constexpr uint32_t kDefaultHubMin = 1024;  // default out-degree for the group-w
 constexpr uint32_t kMinHubMin = 256;       // smallest accepted hub_min (bounds the hub-list size)
 constexpr int kRingLog = 11;
 constexpr int kRing = 1 << kRingLog;       // async drain: CTA-local work ring (entries of 16 B header + 64 B slot)
-constexpr uint32_t kRingSafe = kRing - 16 * 32 - 64;  // admission limit (see the ring protocol)
+// Ring admission limit (see the ring protocol in gi_kernels.cu): concurrent pushers overshoot
+// by < one entry per thread (kBlock) and claimed-but-unread entries are < 4 per warp, so a
+// limit of kRing - kBlock - 4 * warps keeps every unread entry inside the ring. By CTA width
+// (512, 1024): 1472 and 896.
+constexpr uint32_t ring_safe(int block) { return (uint32_t)(kRing - block - 4 * (block / 32)); }
+constexpr uint32_t kRingSafeW[2] = {ring_safe(512), ring_safe(1024)};
+constexpr uint32_t kRingSafe = ring_safe(kBlock);
 constexpr uint32_t kAsyncMaxDeg = kSlotEdges;  // async drain needs every adjacency inline in its ELL slot
 
 // Persistent-kernel variants.
@@ -99,8 +105,12 @@ struct GroupWs {
   int32_t* far[2];    // [n] far pile, double-buffered across extractions
   int32_t* q[2];      // [n] global frontier, double-buffered across phases
   struct HubEnt* hub[2];  // [hubcap] group hub lists (deg >= hub_min), by phase parity
+  unsigned long long* xpre;  // [hubcap] expand: exclusive degree prefix of each entry within its CTA slice
+  unsigned long long* xtot;  // [kMaxGroupCtas] expand: edge total of each CTA's slice of the list
   Ctl* ctl;
 };
+
+constexpr int kMaxGroupCtas = 1024;  // expand: largest group (CTAs) the slice totals are sized for
 
 // A high-degree vertex queued for relaxation by every CTA of the group.
 struct HubEnt {
@@ -108,6 +118,7 @@ struct HubEnt {
   uint32_t deg;
   uint32_t du;
 };
+static_assert(sizeof(HubEnt) == 16, "expand loads a list entry as one 16-byte vector");
 
 struct KArgs {
   const uint2* slots;   // [n][8] ELL adjacency slots (64 B per vertex)
@@ -134,6 +145,11 @@ struct KArgs {
                            // matrix (device-accessible: local, P2P or IPC-mapped); nullptr = none
   int32_t npeers;
   uint32_t peer_vec;    // 16-byte copies (n % 4 == 0 and every base 16-byte aligned)
+  // expand (skewed graphs): a ROUND phase collects every high-degree frontier vertex into the
+  // group list and relaxes the concatenation of their edges split evenly over all warps
+  uint32_t expand;
+  const uint32_t* pedges;  // [m] packed edges (w << colbits | col) or nullptr (use `edges`)
+  uint32_t colbits;        // packed: bits of the column id
 };
 
 // k-core (gi_kcore.cu): control block, statistics and arguments.
@@ -187,6 +203,11 @@ cudaError_t launch_interleave(const int32_t* cols, const uint32_t* w, uint2* edg
 cudaError_t launch_build_slots(const int64_t* off, const uint2* edges, uint2* slots, int64_t n,
                                cudaStream_t st);
 cudaError_t launch_max_degree(const int64_t* off, int64_t n, uint32_t* max_deg, cudaStream_t st);
+// skewed-graph layout: vertices of out-degree > 8 (expand list capacity), max weight, and
+// the packed edge array (w << colbits | col) when every weight fits the spare bits
+cudaError_t launch_count_big(const int64_t* off, int64_t n, unsigned long long* count, cudaStream_t st);
+cudaError_t launch_max_weight(const uint2* edges, int64_t m, uint32_t* max_w, cudaStream_t st);
+cudaError_t launch_pack_edges(const uint2* edges, uint32_t* packed, int64_t m, uint32_t colbits, cudaStream_t st);
 cudaError_t launch_validate_offsets(const int64_t* off, int64_t n, int64_t m, uint32_t* bad_flag,
                                     cudaStream_t st);
 cudaError_t launch_kcore(const KcArgs& a, int grid, cudaStream_t st);  // gi_kcore.cu

@@ -49,6 +49,8 @@
 
 #include <cooperative_groups.h>
 
+#include <atomic>
+
 namespace cg = cooperative_groups;
 
 namespace gi {
@@ -147,12 +149,63 @@ using dev::fence_acq_rel;
 using dev::ld_relaxed;
 
 __device__ __forceinline__ void red_min(uint32_t* p, uint32_t v) {
+#if GI_X_DIST_EL
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("red.relaxed.gpu.global.min.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+#else
   asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#endif
 }
 
 // dist[] is written by atomics inside this kernel: read it coherently from L2,
 // never through the non-coherent/L1 path (SURVEY §7 hard part 1).
 __device__ __forceinline__ uint32_t ld_dist(const uint32_t* p) { return __ldcg(p); }
+
+// L2 eviction-priority policies (createpolicy; the policy travels with the access).
+__device__ __forceinline__ uint64_t pol_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+#ifndef GI_X_DIST_EL
+#define GI_X_DIST_EL 0
+#endif
+#ifndef GI_X_EDGE_EF
+#define GI_X_EDGE_EF 0
+#endif
+// relaxation-target reads / writes of dist (skewed graphs: the hot targets should stay in L2)
+__device__ __forceinline__ uint32_t ld_dist_tgt(const uint32_t* p) {
+#if GI_X_DIST_EL
+  uint32_t v;
+  asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_evict_last()));
+  return v;
+#else
+  return __ldcg(p);
+#endif
+}
+// packed edges (w << colbits | col), streamed
+__device__ __forceinline__ uint32_t ld_pedge(const uint32_t* p) {
+  uint32_t x;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(x) : "l"(p), "l"(pol_evict_first()));
+  return x;
+}
+// streamed CSR edges: read once per relaxation pass
+__device__ __forceinline__ uint2 ld_edge(const uint2* p) {
+#if GI_X_EDGE_EF
+  uint2 x;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+               : "=r"(x.x), "=r"(x.y) : "l"(p), "l"(pol_evict_first()));
+  return x;
+#else
+  return __ldg(p);
+#endif
+}
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
@@ -213,6 +266,8 @@ struct Shared {
   uint32_t done;            // processed entries + finished feeding warps - warps (termination)
   uint32_t maxdep;          // max depth (sub-round equivalent) processed this phase
   uint32_t spilled;         // some push overflowed the ring threshold this phase
+  uint32_t xhn;             // expand: entries of the group list after collection
+  unsigned long long xS[kMaxGroupCtas + 1];  // expand: exclusive prefix of the CTA slice totals
 };
 
 // Everything a relaxation needs, held in registers for one phase.
@@ -378,7 +433,7 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
     // dedup bits (far pile) or the staleness probe (bins) absorb; the thread holding the
     // final minimum always pushes (whoever wrote it first saw a larger value).
 #pragma unroll
-    for (int k = 0; k < K; ++k) old[k] = (ok & (1u << k)) ? ld_dist(c.dist + e[k].x) : 0u;
+    for (int k = 0; k < K; ++k) old[k] = (ok & (1u << k)) ? ld_dist_tgt(c.dist + e[k].x) : 0u;
 #pragma unroll
     for (int k = 0; k < K; ++k)
       if (!(nd[k] < old[k])) ok &= ~(1u << k);
@@ -706,7 +761,7 @@ __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32
             rel = be.beg - (int64_t)nxt;
             nxt = lo + 1 < nb ? c.pre[lo + 1] : total;
           }
-          e[u] = __ldg(c.edges + rel + (int64_t)k);
+          e[u] = ld_edge(c.edges + rel + (int64_t)k);
           du[u] = be.du;
           valid |= 1u << u;
         }
@@ -724,6 +779,172 @@ __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32
     TRACE(17);
   }
   TRACE(13);
+}
+
+// ---------------------------------------------------------------------------------
+// Expand (skewed graphs, ROUND phases): every frontier vertex of out-degree > 8 found this
+// phase (and every hub queued by the previous phase's drains) is an entry {beg, deg, du} of
+// the group list X. The concatenation of their edge lists — E edges — is split into W equal
+// contiguous ranges, one per warp of the group, so that a hub of a million edges and ten
+// thousand vertices of degree 20 cost the same per warp (edge-balanced relaxation, kernel
+// (b)). Two steps after the phase's collection barrier:
+//   expand_scan  — each CTA takes a contiguous slice of X and writes the exclusive degree
+//                  prefix of every entry WITHIN its slice (xpre) and the slice total (xtot);
+//   expand_relax — after a second barrier, global position of entry i of slice r is
+//                  S[r] + xpre[i] (S = prefix of the slice totals, built in shared memory by
+//                  every CTA). A warp finds the entry holding its first position (binary
+//                  search over S, then a 32-ary search over xpre), keeps a window of 32
+//                  consecutive entries in its lanes (entry end positions relative to the
+//                  range start) and maps each row of 32 consecutive positions to entries
+//                  with one ballot, one OR-reduction and a popcount: lane k reads edge
+//                  (position - entry start + entry beg) — consecutive lanes read consecutive
+//                  edges of the same list (coalesced).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ void expand_scan(const HubEnt* X, unsigned long long* xpre, unsigned long long* xtot,
+                                            uint32_t hn, uint32_t G, uint32_t rank, Shared& s) {
+  const uint32_t lo = (uint32_t)(((uint64_t)hn * rank) / G), hi = (uint32_t)(((uint64_t)hn * (rank + 1)) / G);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long carry = 0;
+  for (uint32_t base = lo; base < hi; base += 4 * kBlock) {
+    unsigned long long loc[4], sum = 0;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const uint32_t i = base + 4 * threadIdx.x + x;
+      loc[x] = sum;
+      sum += i < hi ? __ldcg(&X[i].deg) : 0u;
+    }
+    unsigned long long incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += t;
+    }
+    if (lane == 31) s.red[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const unsigned long long w = lane < kBlock / 32 ? s.red[lane] : 0ull;
+      unsigned long long wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= (uint32_t)o) wi += t;
+      }
+      if (lane < kBlock / 32) s.red[lane] = wi - w;
+      if (lane == kBlock / 32 - 1) s.total = wi;
+    }
+    __syncthreads();
+    const unsigned long long off = carry + s.red[warp] + incl - sum;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const uint32_t i = base + 4 * threadIdx.x + x;
+      if (i < hi) xpre[i] = off + loc[x];
+    }
+    carry += s.total;
+    __syncthreads();  // s.red / s.total are rewritten by the next chunk
+  }
+  if (threadIdx.x == 0) xtot[rank] = carry;
+}
+
+// One warp's window of list entries jb .. jb+31: lane k holds entry jb+k's end position
+// relative to the warp's range start (clamped to [0, len]), beg - start (edge index of a
+// position = off + position) and du.
+struct XWin {
+  uint32_t endr;
+  int64_t off;
+  uint32_t du;
+};
+
+__device__ __forceinline__ XWin expand_window(const HubEnt* X, const unsigned long long* xpre, uint32_t hn,
+                                              uint32_t G, const unsigned long long* S, uint32_t jb,
+                                              unsigned long long a, uint32_t len) {
+  const uint32_t idx = jb + (threadIdx.x & 31);
+  XWin w;
+  w.endr = len; w.off = 0; w.du = 0;
+  if (idx < hn) {
+    // written by other CTAs before the group barrier: L2-coherent loads
+    const uint4 he = __ldcg(reinterpret_cast<const uint4*>(X + idx));  // {beg lo, beg hi, deg, du}
+    const int64_t beg = (int64_t)(((uint64_t)he.y << 32) | he.x);
+    const uint32_t r = (uint32_t)((((uint64_t)idx + 1) * G - 1) / hn);  // slice of idx
+    const unsigned long long start = S[r] + __ldcg(xpre + idx);
+    const unsigned long long end = start + he.z;
+    w.endr = end <= a ? 0u : (uint32_t)min(end - a, (unsigned long long)len);
+    w.off = beg - (int64_t)start;
+    w.du = he.w;
+  }
+  return w;
+}
+
+template <bool FUSED>
+__device__ __forceinline__ void expand_relax(Ctx& c, const HubEnt* X, const unsigned long long* xpre, uint32_t hn,
+                                             uint32_t G, const unsigned long long* S, unsigned long long a,
+                                             unsigned long long b, const uint32_t* pedges, uint32_t colbits,
+                                             uint32_t& ne) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t len = (uint32_t)(b - a);
+  // slice r holding position a: the largest r with S[r] <= a (S[G] = E > a)
+  uint32_t rlo = 0, rhi = G;
+  while (rhi - rlo > 1) {
+    const uint32_t mid = (rlo + rhi) >> 1;
+    if (S[mid] <= a) rlo = mid; else rhi = mid;
+  }
+  // entry within the slice: the largest i with xpre[i] <= a - S[r] (32-ary search)
+  const unsigned long long t = a - S[rlo];
+  uint32_t ilo = (uint32_t)(((uint64_t)hn * rlo) / G), ihi = (uint32_t)(((uint64_t)hn * (rlo + 1)) / G);
+  while (ihi - ilo > 32) {
+    const uint32_t step = (ihi - ilo + 31) / 32;
+    const uint32_t idx = ilo + lane * step;
+    const bool pr = idx < ihi && __ldcg(xpre + idx) <= t;
+    const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, pr));
+    ilo += (cnt - 1) * step;
+    ihi = min(ilo + step, ihi);
+  }
+  {
+    const uint32_t idx = ilo + lane;
+    const bool pr = idx < ihi && __ldcg(xpre + idx) <= t;
+    ilo += __popc(__ballot_sync(0xffffffffu, pr)) - 1;
+  }
+  uint32_t jb = ilo;
+  XWin w = expand_window(X, xpre, hn, G, S, jb, a, len);
+  const uint32_t lanemask = (2u << lane) - 2u;  // bits 1..lane (lane 31: 0xFFFFFFFE)
+  const uint32_t cmask = colbits >= 32 ? 0xFFFFFFFFu : (1u << colbits) - 1u;
+  constexpr int K = kBigK;
+  for (uint32_t it0 = 0; it0 < len; it0 += 32 * K) {
+    uint2 e[K];
+    uint32_t du[K];
+    uint32_t valid = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      e[k] = make_uint2(0, 0);
+      du[k] = 0;
+      const uint32_t r0 = it0 + 32 * k;
+      if (r0 >= len) continue;  // warp-uniform
+      // the window must hold every entry of this row: refill at the entry holding r0
+      const uint32_t last = __shfl_sync(0xffffffffu, w.endr, 31);
+      if (last < min(r0 + 32, len)) {
+        jb += __popc(__ballot_sync(0xffffffffu, w.endr <= r0));
+        w = expand_window(X, xpre, hn, G, S, jb, a, len);
+      }
+      const uint32_t c0 = __popc(__ballot_sync(0xffffffffu, w.endr <= r0));  // entry of r0, relative
+      const uint32_t x = w.endr - r0;
+      const uint32_t heads = __reduce_or_sync(0xffffffffu, (x - 1u < 31u) ? (1u << x) : 0u);
+      const uint32_t slot = c0 + __popc(heads & lanemask);
+      const int64_t off = __shfl_sync(0xffffffffu, w.off, slot);
+      const uint32_t d = __shfl_sync(0xffffffffu, w.du, slot);
+      if (r0 + lane < len) {
+        const int64_t ei = off + (int64_t)(a + r0 + lane);
+        if (pedges) {
+          const uint32_t pe = ld_pedge(pedges + ei);
+          e[k] = make_uint2(pe & cmask, pe >> colbits);
+        } else {
+          e[k] = ld_edge(c.edges + ei);
+        }
+        du[k] = d;
+        valid |= 1u << k;
+      }
+    }
+    relax_batch<FUSED, K>(c, e, du, valid);
+    ne += __popc(valid);
+  }
 }
 
 // Relax every entry of a CTA-local bin (stage A, then stage B when high-degree
@@ -1366,11 +1587,18 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           scanned += hi - lo;
         }
       } else {
-        // hubs queued in the previous phase: every CTA relaxes its 1/G slice of every
-        // hub's edges (stage B over the slices), so a hub costs ~deg/G per CTA
         const uint32_t hn = s.hn;
-        const HubEnt* hub_in = (p & 1) ? ws.hub[1] : ws.hub[0];
-        for (uint32_t h0 = 0; h0 < hn; h0 += kBigCap) {
+        HubEnt* hub_in = (p & 1) ? ws.hub[1] : ws.hub[0];
+        if (a.expand) {
+          // expand: this phase's high-degree frontier vertices join the hubs queued by the
+          // previous phase in the group list, relaxed edge-balanced after the collection
+          c.hub_min = kSlotEdges + 1;
+          c.hub_next = hub_in;
+          c.hcount_next = &ctl->hcount[p % 3];
+        }
+        // hubs queued in the previous phase (no expand): every CTA relaxes its 1/G slice of
+        // every hub's edges (stage B over the slices), so a hub costs ~deg/G per CTA
+        for (uint32_t h0 = 0; h0 < (a.expand ? 0u : hn); h0 += kBigCap) {
           const uint32_t nh = min((uint32_t)kBigCap, hn - h0);
           for (uint32_t i = tid; i < nh; i += kBlock) {
             const HubEnt he = hub_in[h0 + i];
@@ -1445,6 +1673,43 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           }
         }
         __syncthreads();
+        if (a.expand) {
+          c.hub_min = a.hub_min;
+          c.hub_next = (p & 1) ? ws.hub[0] : ws.hub[1];
+          c.hcount_next = &ctl->hcount[(p + 1) % 3];
+          group_barrier(ctl, G);  // the group list is complete
+          ++phases;
+          if (tid == 0) s.xhn = min(__ldcg(&ctl->hcount[p % 3]), a.hubcap);
+          __syncthreads();
+          const uint32_t xn = s.xhn;
+          if (xn) {
+            expand_scan(hub_in, ws.xpre, ws.xtot, xn, G, rank, s);
+            group_barrier(ctl, G);  // slice prefixes and totals are final
+            ++phases;
+            if (tid < 32) {  // S[r] = sum of the slice totals before r
+              unsigned long long carry = 0;
+              if (tid == 0) s.xS[0] = 0;
+              for (uint32_t b0 = 0; b0 < G; b0 += 32) {
+                const uint32_t r = b0 + tid;
+                unsigned long long v = r < G ? __ldcg(ws.xtot + r) : 0ull;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                  const unsigned long long t = __shfl_up_sync(0xffffffffu, v, o);
+                  if (tid >= (uint32_t)o) v += t;
+                }
+                if (r < G) s.xS[r + 1] = carry + v;
+                carry += __shfl_sync(0xffffffffu, v, 31);
+              }
+            }
+            __syncthreads();
+            const unsigned long long E = s.xS[G];
+            const uint64_t W = (uint64_t)G * (kBlock / 32), wg = (uint64_t)rank * (kBlock / 32) + (tid >> 5);
+            const unsigned long long a0 = E * wg / W, b0 = E * (wg + 1) / W;
+            if (a0 < b0) expand_relax<FUSED>(c, hub_in, ws.xpre, xn, G, s.xS, a0, b0, a.pedges, a.colbits, ne);
+            TRACE(18);
+            __syncthreads();
+          }
+        }
       }
 
       if constexpr (FUSED && !ASYNC) {
@@ -1631,6 +1896,30 @@ __global__ void max_degree_kernel(const int64_t* __restrict__ off, int64_t n, ui
   if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
 }
 
+__global__ void count_big_kernel(const int64_t* __restrict__ off, int64_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    c += (off[v + 1] - off[v]) > kSlotEdges;
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+__global__ void max_weight_kernel(const uint2* __restrict__ edges, int64_t m, uint32_t* out) {
+  uint32_t mx = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    mx = max(mx, edges[i].y);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
+__global__ void pack_edges_kernel(const uint2* __restrict__ edges, uint32_t* __restrict__ packed, int64_t m,
+                                  uint32_t colbits) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint2 e = edges[i];
+    packed[i] = (e.y << colbits) | e.x;
+  }
+}
+
 __global__ void validate_offsets_kernel(const int64_t* __restrict__ off, int64_t n, int64_t m,
                                         uint32_t* bad) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -1663,13 +1952,18 @@ static const void* kernel_fn(int kind) {
   }
 }
 
-static bool g_attr_set[KIND_COUNT] = {};
+// The dynamic shared-memory attribute belongs to the kernel's per-context function object:
+// cached per (device, kind), so that a graph on a second device sets it there too.
+static std::atomic<uint64_t> g_attr_set[KIND_COUNT];
 
 static cudaError_t set_attrs(int kind) {
-  if (g_attr_set[kind]) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kernel_fn(kind), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       smem_bytes(kind));
-  if (e == cudaSuccess) g_attr_set[kind] = true;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = dev < 64 ? 1ull << dev : 0ull;
+  if (bit && (g_attr_set[kind].load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel_fn(kind), cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(kind));
+  if (e == cudaSuccess && bit) g_attr_set[kind].fetch_or(bit, std::memory_order_acq_rel);
   return e;
 }
 
@@ -1736,6 +2030,23 @@ cudaError_t launch_build_slots(const int64_t* off, const uint2* edges, uint2* sl
 
 cudaError_t launch_max_degree(const int64_t* off, int64_t n, uint32_t* max_deg, cudaStream_t st) {
   max_degree_kernel<<<grid_for(n), 256, 0, st>>>(off, n, max_deg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_count_big(const int64_t* off, int64_t n, unsigned long long* count, cudaStream_t st) {
+  count_big_kernel<<<grid_for(n), 256, 0, st>>>(off, n, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_max_weight(const uint2* edges, int64_t m, uint32_t* max_w, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  max_weight_kernel<<<grid_for(m), 256, 0, st>>>(edges, m, max_w);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_edges(const uint2* edges, uint32_t* packed, int64_t m, uint32_t colbits, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  pack_edges_kernel<<<grid_for(m), 256, 0, st>>>(edges, packed, m, colbits);
   return cudaGetLastError();
 }
 

@@ -29,7 +29,7 @@ EXPORTS = ["gi_graph_create", "gi_graph_destroy", "gi_graph_info", "gi_sssp_delt
            "gi_options_default", "gi_sssp_delta_ex", "gi_sssp_batch_ex", "gi_last_error",
            "gi_status_string", "gi_version", "gi_ppsp_delta", "gi_ppsp_delta_ex", "gi_astar_delta",
            "gi_astar_delta_ex", "gi_kcore", "gi_kcore_ex", "gi_sssp_batch_peers", "gi_ipc_get_handle",
-           "gi_ipc_open_handle", "gi_ipc_close_handle"]
+           "gi_ipc_open_handle", "gi_ipc_close_handle", "gi_probe_floors"]
 
 
 class GiError(RuntimeError):
@@ -48,7 +48,7 @@ class gi_options(ctypes.Structure):
                 ("fusion_threshold", ctypes.c_uint32), ("max_ctas", ctypes.c_int32),
                 ("hub_min", ctypes.c_uint32), ("drain", ctypes.c_uint32),
                 ("group_ctas", ctypes.c_int32), ("pre_read", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p),
-                ("cta_threads", ctypes.c_int32), ("reserved2", ctypes.c_int32)]
+                ("cta_threads", ctypes.c_int32), ("expand", ctypes.c_int32)]
 
 
 class gi_stats(ctypes.Structure):
@@ -60,6 +60,14 @@ class gi_stats(ctypes.Structure):
                 ("gpu_ms", ctypes.c_float), ("ctas", ctypes.c_int32),
                 ("threads_per_cta", ctypes.c_int32), ("groups", ctypes.c_int32),
                 ("kernel_kind", ctypes.c_int32)]
+
+    def to_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class gi_floors(ctypes.Structure):
+    _fields_ = [("t_sync_us", ctypes.c_float), ("t_hop_us", ctypes.c_float), ("t_launch_us", ctypes.c_float),
+                ("sm_clock_mhz", ctypes.c_float), ("ctas", ctypes.c_int32)]
 
     def to_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -88,13 +96,15 @@ _lib.gi_kcore.argtypes = [_vp, _vp]
 _lib.gi_kcore_ex.argtypes = [_vp, ctypes.POINTER(gi_options), _vp, ctypes.POINTER(gi_stats)]
 _lib.gi_astar_delta_ex.argtypes = [_vp, _i32, _i32, _u32, _vp, ctypes.POINTER(gi_options), _vp,
                                    ctypes.POINTER(gi_stats)]
+_lib.gi_probe_floors.argtypes = [_i32, _i32, ctypes.POINTER(gi_floors)]
 _lib.gi_last_error.restype = ctypes.c_char_p
 _lib.gi_status_string.argtypes = [ctypes.c_int]
 _lib.gi_status_string.restype = ctypes.c_char_p
 _lib.gi_version.restype = _i32
 for _f in ("gi_graph_create", "gi_graph_info", "gi_sssp_delta", "gi_sssp_batch", "gi_sssp_delta_ex",
            "gi_sssp_batch_ex", "gi_ppsp_delta", "gi_ppsp_delta_ex", "gi_astar_delta", "gi_astar_delta_ex", "gi_kcore",
-           "gi_kcore_ex", "gi_sssp_batch_peers", "gi_ipc_get_handle", "gi_ipc_open_handle", "gi_ipc_close_handle"):
+           "gi_kcore_ex", "gi_sssp_batch_peers", "gi_ipc_get_handle", "gi_ipc_open_handle", "gi_ipc_close_handle",
+           "gi_probe_floors"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 
@@ -129,8 +139,107 @@ def _ptr(x):
     raise TypeError(type(x))
 
 
+def _is_torch(x):
+    return hasattr(x, "data_ptr") and hasattr(x, "dtype") and not isinstance(x, np.ndarray)
+
+
+def _as_index_array(x, dtype, what):
+    """Validate / coerce an index array to a contiguous `dtype` (np.int32 or np.int64) array or
+    tensor of the same kind; values must fit the target type. Lists become numpy arrays."""
+    import torch
+    if _is_torch(x):
+        want = torch.int32 if dtype == np.int32 else torch.int64
+        if x.dtype == want:
+            return x.contiguous()
+        if x.dtype in (torch.int8, torch.int16, torch.int32, torch.int64, torch.uint8):
+            info = np.iinfo(dtype)
+            if x.numel() and (int(x.min()) < info.min or int(x.max()) > info.max):
+                raise ValueError(f"{what}: values do not fit {np.dtype(dtype).name}")
+            return x.to(want).contiguous()
+        raise TypeError(f"{what}: integer tensor required, got {x.dtype}")
+    a = np.asarray(x)
+    if a.dtype.kind not in "iu":
+        raise TypeError(f"{what}: integer array required, got {a.dtype}")
+    if a.dtype != dtype:
+        info = np.iinfo(dtype)
+        if a.size and (int(a.min()) < info.min or int(a.max()) > info.max):
+            raise ValueError(f"{what}: values do not fit {np.dtype(dtype).name}")
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _as_u32_bits(x, what):
+    """uint32 data (weights, heuristics): numpy uint32 (int32 reinterpreted; other integer
+    dtypes range-checked and converted) or a 4-byte integer torch tensor (int32 holds the bits)."""
+    import torch
+    if _is_torch(x):
+        if x.dtype in (torch.int32, getattr(torch, "uint32", torch.int32)):
+            return x.contiguous()
+        if x.dtype in (torch.int64, torch.int16, torch.uint8, torch.int8):
+            if x.numel() and (int(x.min()) < 0 or int(x.max()) > 0xFFFFFFFF):
+                raise ValueError(f"{what}: values outside [0, 2^32)")
+            return _u32_tensor(x)
+        raise TypeError(f"{what}: 32-bit integer tensor required, got {x.dtype}")
+    a = np.asarray(x)
+    if a.dtype == np.uint32:
+        return np.ascontiguousarray(a)
+    if a.dtype == np.int32:
+        return np.ascontiguousarray(a).view(np.uint32)
+    if a.dtype.kind not in "iu":
+        raise TypeError(f"{what}: integer array required, got {a.dtype}")
+    if a.size and (int(a.min()) < 0 or int(a.max()) > 0xFFFFFFFF):
+        raise ValueError(f"{what}: values outside [0, 2^32)")
+    return np.ascontiguousarray(a, dtype=np.uint32)
+
+
+def _u32_tensor(x):
+    """integer tensor with values in [0, 2^32) -> int32 tensor holding the uint32 bits."""
+    import torch
+    y = x.to(torch.int64)
+    y = torch.where(y >= 2 ** 31, y - 2 ** 32, y)
+    return y.to(torch.int32).contiguous()
+
+
+def _check_out(x, count, what):
+    """A result buffer: 4-byte elements, contiguous, exactly `count` of them."""
+    if _is_torch(x):
+        if x.element_size() != 4 or x.dtype.is_floating_point:
+            raise TypeError(f"{what}: int32/uint32 tensor required, got {x.dtype}")
+        if not x.is_contiguous():
+            raise ValueError(f"{what}: tensor must be contiguous")
+        if x.numel() != count:
+            raise ValueError(f"{what}: {x.numel()} elements, need {count}")
+        return
+    if not isinstance(x, np.ndarray):
+        raise TypeError(f"{what}: numpy array or torch tensor required")
+    if x.dtype not in (np.uint32, np.int32):
+        raise TypeError(f"{what}: uint32/int32 array required, got {x.dtype}")
+    if not x.flags["C_CONTIGUOUS"] or not x.flags["WRITEABLE"]:
+        raise ValueError(f"{what}: array must be C-contiguous and writeable")
+    if x.size != count:
+        raise ValueError(f"{what}: {x.size} elements, need {count}")
+
+
+def _default_stream(options, *tensors):
+    """Options with cuda_stream = torch's current stream of the tensors' device when the
+    caller gave none and some argument is a CUDA tensor, so that the query is ordered after
+    the torch work that produced its inputs and before the work that reads its output."""
+    dev = None
+    for t in tensors:
+        if _is_torch(t) and t.is_cuda:
+            dev = t.device
+            break
+    if dev is None:
+        return options
+    if options is None:
+        options = make_options()
+    if not options.cuda_stream:
+        import torch
+        options.cuda_stream = torch.cuda.current_stream(dev).cuda_stream
+    return options
+
+
 def make_options(fusion=True, threshold=0, max_ctas=0, group_ctas=0, pre_read=0, hub_min=0,
-                 drain=0, stream=None, cta_threads=0) -> gi_options:
+                 drain=0, stream=None, cta_threads=0, expand=0) -> gi_options:
     o = gi_options()
     _lib.gi_options_default(ctypes.byref(o))
     o.fusion = 1 if fusion else 0
@@ -141,6 +250,7 @@ def make_options(fusion=True, threshold=0, max_ctas=0, group_ctas=0, pre_read=0,
     o.hub_min = hub_min
     o.drain = {"auto": 0, "bsp": 1, "async": 2}.get(drain, drain)
     o.cta_threads = cta_threads
+    o.expand = {"auto": 0, "on": 1, "off": 2}.get(expand, expand)
     if stream is not None:
         o.cuda_stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     return o
@@ -151,10 +261,13 @@ class Graph:
     (host or CUDA) — int64 offsets[n+1], int32 cols[m], uint32/int32 weights[m]."""
 
     def __init__(self, offsets, cols, weights, device: int = 0):
+        offsets = _as_index_array(offsets, np.int64, "offsets")
+        cols = _as_index_array(cols, np.int32, "cols")
+        weights = _as_u32_bits(weights, "weights")
         n = int(offsets.shape[0]) - 1
         m = int(cols.shape[0])
-        if isinstance(weights, np.ndarray) and weights.dtype != np.uint32:
-            weights = weights.astype(np.uint32)
+        if int(weights.shape[0]) != m:
+            raise ValueError(f"weights: {int(weights.shape[0])} elements, cols has {m}")
         h = _vp()
         _check(_lib.gi_graph_create(n, m, _ptr(offsets), _ptr(cols) if m else None,
                                     _ptr(weights) if m else None, device, ctypes.byref(h)))
@@ -189,6 +302,8 @@ class Graph:
 def gi_sssp_delta(g: Graph, src: int, delta: int, dist_out, options: gi_options | None = None,
                   want_stats: bool = True):
     """C-ABI gi_sssp_delta_ex. dist_out: torch int32/uint32 CUDA tensor [n] or numpy uint32 [n]."""
+    _check_out(dist_out, g.n, "dist_out")
+    options = _default_stream(options, dist_out)
     st = gi_stats() if want_stats else None
     _check(_lib.gi_sssp_delta_ex(g.handle, int(src), int(delta), ctypes.byref(options) if options else None,
                                  _ptr(dist_out), ctypes.byref(st) if st is not None else None))
@@ -198,7 +313,10 @@ def gi_sssp_delta(g: Graph, src: int, delta: int, dist_out, options: gi_options 
 def gi_sssp_batch(g: Graph, srcs, delta: int, dist_out, options: gi_options | None = None,
                   want_stats: bool = True):
     """C-ABI gi_sssp_batch_ex. srcs: int32 array/tensor [k]; dist_out [k, n]."""
+    srcs = _as_index_array(srcs, np.int32, "srcs")
     k = int(srcs.shape[0])
+    _check_out(dist_out, k * g.n, "dist_out")
+    options = _default_stream(options, dist_out, srcs)
     st = (gi_stats * max(k, 1))() if want_stats else None
     _check(_lib.gi_sssp_batch_ex(g.handle, _ptr(srcs), k, int(delta),
                                  ctypes.byref(options) if options else None, _ptr(dist_out), st))
@@ -209,7 +327,12 @@ def gi_sssp_batch_peers(g: Graph, srcs, delta: int, peer_rows, self_index: int,
                         options: gi_options | None = None, want_stats: bool = True):
     """C-ABI gi_sssp_batch_peers. peer_rows: device addresses (ints) of this block's first
     row inside every rank's result matrix; rows are computed in peer_rows[self_index]."""
+    srcs = _as_index_array(srcs, np.int32, "srcs")
     k = int(srcs.shape[0])
+    if options is None or not options.cuda_stream:
+        import torch
+        options = options if options is not None else make_options()
+        options.cuda_stream = torch.cuda.current_stream(g.device).cuda_stream
     st = (gi_stats * max(k, 1))() if want_stats else None
     arr = (_vp * len(peer_rows))(*[int(p) for p in peer_rows])
     _check(_lib.gi_sssp_batch_peers(g.handle, _ptr(srcs), k, int(delta), ctypes.byref(options) if options else None,
@@ -249,8 +372,7 @@ def sssp(g: Graph, src: int, delta: int, out=None, **opts):
 
 def sssp_batch(g: Graph, srcs, delta: int, out=None, **opts):
     import torch
-    if not hasattr(srcs, "data_ptr") and not isinstance(srcs, np.ndarray):
-        srcs = np.asarray(srcs, dtype=np.int32)
+    srcs = _as_index_array(srcs, np.int32, "srcs")
     k = int(srcs.shape[0])
     if out is None:
         out = torch.empty((k, g.n), dtype=torch.int32, device=f"cuda:{g.device}")
@@ -261,6 +383,8 @@ def sssp_batch(g: Graph, srcs, delta: int, out=None, **opts):
 def gi_ppsp_delta(g: Graph, src: int, dst: int, delta: int, dist_st, options: gi_options | None = None,
                   want_stats: bool = True):
     """C-ABI gi_ppsp_delta_ex. dist_st: one-element uint32 (or int32) array/tensor."""
+    _check_out(dist_st, 1, "dist_st")
+    options = _default_stream(options, dist_st)
     st = gi_stats() if want_stats else None
     _check(_lib.gi_ppsp_delta_ex(g.handle, int(src), int(dst), int(delta),
                                  ctypes.byref(options) if options else None, _ptr(dist_st),
@@ -279,6 +403,11 @@ def ppsp(g: Graph, src: int, dst: int, delta: int, **opts):
 def gi_astar_delta(g: Graph, src: int, dst: int, delta: int, h, dist_st, options: gi_options | None = None,
                    want_stats: bool = True):
     """C-ABI gi_astar_delta_ex. h: uint32 (or int32 bits) [n] array/tensor, host or device."""
+    h = _as_u32_bits(h, "h")
+    if int(h.shape[0]) != g.n:
+        raise ValueError(f"h: {int(h.shape[0])} elements, need {g.n}")
+    _check_out(dist_st, 1, "dist_st")
+    options = _default_stream(options, dist_st, h)
     st = gi_stats() if want_stats else None
     _check(_lib.gi_astar_delta_ex(g.handle, int(src), int(dst), int(delta), _ptr(h),
                                   ctypes.byref(options) if options else None, _ptr(dist_st),
@@ -288,8 +417,6 @@ def gi_astar_delta(g: Graph, src: int, dst: int, delta: int, h, dist_st, options
 
 def astar(g: Graph, src: int, dst: int, delta: int, h, **opts):
     """A* (Δ-stepping on the priority dist + h, PPSP stop). Returns (distance, stats dict)."""
-    if isinstance(h, np.ndarray) and h.dtype != np.uint32:
-        h = h.astype(np.uint32)
     out = np.zeros(1, np.uint32)
     st = gi_astar_delta(g, src, dst, delta, h, out, make_options(**opts) if opts else None)
     return int(out[0]), st.to_dict()
@@ -297,6 +424,8 @@ def astar(g: Graph, src: int, dst: int, delta: int, h, **opts):
 
 def gi_kcore(g: Graph, core_out, options: gi_options | None = None, want_stats: bool = True):
     """C-ABI gi_kcore_ex. core_out: uint32/int32 [n], host or device."""
+    _check_out(core_out, g.n, "core_out")
+    options = _default_stream(options, core_out)
     st = gi_stats() if want_stats else None
     _check(_lib.gi_kcore_ex(g.handle, ctypes.byref(options) if options else None, _ptr(core_out),
                             ctypes.byref(st) if st is not None else None))
@@ -311,6 +440,13 @@ def kcore(g: Graph, out=None, **opts):
         out = torch.empty(g.n, dtype=torch.int32, device=f"cuda:{g.device}")
     st = gi_kcore(g, out, make_options(**opts) if opts else None)
     return out, st.to_dict()
+
+
+def probe_floors(device: int = 0, iters: int = 2000) -> dict:
+    """C-ABI gi_probe_floors: t_sync / t_hop / t_launch (µs) measured on `device`."""
+    f = gi_floors()
+    _check(_lib.gi_probe_floors(int(device), int(iters), ctypes.byref(f)))
+    return f.to_dict()
 
 
 def as_uint32(t) -> np.ndarray:

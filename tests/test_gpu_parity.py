@@ -273,6 +273,36 @@ def test_hubs_and_mixed_degrees(gi):
             assert np.array_equal(d, ref), (s, o, delta)
 
 
+def test_expand_edge_balanced(gi):
+    """Expand (skewed graphs): ROUND phases collect every frontier vertex of degree > 8 into
+    one group list and split the concatenation of their edges evenly over all warps. Random
+    power-law-like graphs; packed (weights fit the spare bits) and unpacked edges; groups of
+    1..7 CTAs and the whole grid; expand forced on / off; fusion on / off; several Δ."""
+    rng = np.random.default_rng(41)
+    for t in range(6):
+        n = int(rng.integers(2_000, 60_000))
+        # degrees: a few hubs, a body of medium vertices, many tiny ones (max degree > 32)
+        deg = np.minimum(rng.zipf(1.7, size=n), n - 1)
+        deg[rng.integers(0, n, 3)] = rng.integers(2_000, max(2_001, n // 2), 3)
+        wmax = int(rng.choice([3, 30, 1 << 20]))  # 1 << 20: too wide to pack beside the ids
+        edges = [(u, int(v), int(w)) for u in range(n) for v, w in
+                 zip(rng.integers(0, n, deg[u]), rng.integers(0, wmax, deg[u]))]
+        g = gen.from_edges(n, edges)
+        G = gi.Graph.from_csr(g)
+        s = int(np.argmax(deg)) if t % 2 == 0 else int(rng.integers(0, n))
+        ref, _ = oracle.dijkstra(g, s)
+        for o, delta in ((dict(), 1), (dict(), 7), (dict(expand="off"), 7), (dict(expand="on", fusion=False), 3),
+                         (dict(max_ctas=1), 5), (dict(max_ctas=2, threshold=1), 2), (dict(max_ctas=7), 1 << 30),
+                         (dict(fusion=False, max_ctas=3), 1), (dict(pre_read=2), 4)):
+            d, st = run(gi, G, s, delta, **o)
+            assert np.array_equal(d, ref), (t, o, delta)
+            assert st["buckets"] == oracle.bucket_count(ref, delta), (t, o, delta)
+        srcs = rng.integers(0, n, 5).astype(np.int32)
+        out, _ = gi.sssp_batch(G, srcs, 4)
+        refs, _, _ = oracle.dijkstra_many(g, srcs)
+        assert np.array_equal(gi.as_uint32(out), refs), t
+
+
 @pytest.mark.slow
 @pytest.mark.skipif(os.environ.get("GI_SKIP_CFG4") == "1",
                     reason="config 4 (RMAT-26, 2.1 B edges): ~2 min and ~25 GB of host RAM (GI_SKIP_CFG4=1)")

@@ -243,3 +243,16 @@ def test_kcore_matches_definition_bruteforce():
     und = list(zip(src.tolist(), g.cols.tolist()))
     s = _sym(64, und)
     assert np.array_equal(oracle.kcore(s), oracle.kcore_bruteforce(s))
+
+
+def test_dijkstra_budget_is_the_same_loop():
+    """The bounded-sample entry point (bench.py's CPU baseline) with no budget settles every
+    reached vertex once and scans exactly their out-edges; its distances equal dijkstra's."""
+    g = gen.grid(40, 40, 1, 100, 3, p_del=0.2)
+    ref, _ = oracle.dijkstra(g, 5)
+    settled, scanned, rc = oracle.dijkstra_budget(g, 5, 0.0)
+    reached = ref != oracle.INF
+    assert rc == 0 and settled == int(reached.sum())
+    assert scanned == int(np.diff(g.offsets)[reached].sum())
+    s2, e2, _ = oracle.dijkstra_budget(g, 5, 1e-9)  # a budget stops early but never before one pop
+    assert 1 <= s2 <= settled and e2 <= scanned

@@ -1,0 +1,32 @@
+"""Config-4 gather ceiling (tools/gather_probe.cu): G edges/s of cols -> dist[col] reads.
+usage: GI_GEN_CACHE=/tmp/gcache python tools/gather_probe.py"""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import gen
+
+so = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ab", "libprobe.so")
+lib = ctypes.CDLL(so)
+lib.probe_gather.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                             ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+g = gen.config_graph(int(os.environ.get("CFG", "4")))
+cols = torch.from_numpy(np.array(g.cols)).cuda()
+m = g.m
+dist = torch.zeros(g.n, dtype=torch.int32, device="cuda")
+sink = torch.zeros(4, dtype=torch.int32, device="cuda")
+st = torch.cuda.current_stream()
+for mode, name in ((2, "edge stream only"), (0, "dist ld.cg"), (1, "dist ld.ca (L1)"), (3, "dist ld.cg evict_last")):
+    for blocks, threads in ((148 * 2, 1024), (148 * 8, 256), (148 * 16, 128)):
+        ts = []
+        for r in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            rc = lib.probe_gather(mode, cols.data_ptr(), m, dist.data_ptr(), sink.data_ptr(), blocks, threads,
+                                  ctypes.c_void_p(st.cuda_stream))
+            assert rc == 0, rc
+            e1.record(st)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        t = min(ts[1:])
+        print(f"{name:24s} grid {blocks}x{threads}: {t:.3f} ms  {m / t / 1e6:.1f} G edges/s", flush=True)

@@ -11,7 +11,7 @@ import numpy as np  # noqa: E402
 
 import gen  # noqa: E402
 
-so = "/tmp/libgi_trace.so"
+so = os.environ.get("TRACE_SO", "/tmp/libgi_trace.so")
 CS = os.path.join(ROOT, "paper_1911_07260_b200/csrc")
 if not os.path.exists(so) or os.environ.get("REBUILD"):
     nv = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-DGI_TRACE", "-Xcompiler",
@@ -77,7 +77,7 @@ clk = 1.965e3  # cycles per µs at the max SM clock
 names = {0: "bsp drain loop top", 2: "slot load", 3: "relax", 4: "rest", 5: "decision", 6: "feed (async) / extract",
          7: "phase work end", 8: "far flush + fmin", 9: "group barrier", 11: "drain (async, CTA 0)",
          12: "stage B scan", 13: "stage B edge loop", 14: "ROUND claim+staging", 15: "hub slices (after B)",
-         16: "B iter: search + edge-load issue", 17: "B iter: relax_batch (waits)"}
+         16: "B iter: search + edge-load issue", 17: "B iter: relax_batch (waits)", 18: "expand (scan barrier -> relax done)"}
 tot = 0
 for k in range(32):
     c = int(buf[32 + k])
