@@ -73,6 +73,7 @@ struct Workspace {
   int hcap_q = 0;
   uint32_t** d_peers = nullptr;  // gi_sssp_batch_peers: device copy of the peer row bases
   int peercap = 0;
+  uint32_t* h_pending = nullptr;  // pinned: KState.pending of a split query, read between segments
   uint32_t* d_h = nullptr;      // staging for a host A* heuristic
   size_t hcap = 0;
   uint32_t* kc_prio = nullptr;  // k-core: priorities [n]
@@ -91,6 +92,7 @@ struct Workspace {
     if (d_peers) cudaFree(d_peers);
     if (h_srcs) cudaFreeHost(h_srcs);
     if (h_qstats) cudaFreeHost(h_qstats);
+    if (h_pending) cudaFreeHost(h_pending);
     if (d_src_next) cudaFree(d_src_next);
     if (kc_prio) cudaFree(kc_prio);
     if (kc_ctl) cudaFree(kc_ctl);
@@ -110,9 +112,11 @@ struct gi_graph {
   uint2* d_edges = nullptr;
   uint2* d_slots = nullptr;  // ELL adjacency slots, 64 B per vertex
   void* d_arena = nullptr;   // one allocation holding offsets, edges and slots (2 MB-aligned parts)
+
   uint32_t max_deg = 0;
   int64_t n_big = 0;             // vertices of out-degree > 8 (skewed graphs: expand list capacity)
   uint32_t* d_pedges = nullptr;  // packed edges (w << colbits | col), skewed graphs whose weights fit
+
   uint32_t colbits = 0;
   int sm_count = 0;
   int bps[2][KIND_COUNT] = {};  // co-resident CTAs per SM, by width (512, 1024) and KernelKind
@@ -198,6 +202,8 @@ gi_status ws_prepare(gi_graph* g, Workspace* w, int k, int nsrc) {
       if ((s = dmalloc(&gw.hub[1], (size_t)w->hubcap, &w->allocs, "alloc hub list"))) return s;
       gw.xpre = nullptr;
       gw.xtot = nullptr;
+      if ((s = dmalloc(&gw.kst, 1, &w->allocs, "alloc expand state"))) return s;
+      GI_CUDA(cudaMemsetAsync(gw.kst, 0, sizeof(KState), w->stream), "memset");
       if (g->max_deg > 32) {  // expand (skewed graphs)
         if ((s = dmalloc(&gw.xpre, (size_t)w->hubcap, &w->allocs, "alloc expand prefix"))) return s;
         if ((s = dmalloc(&gw.xtot, (size_t)kMaxGroupCtas, &w->allocs, "alloc expand totals"))) return s;
@@ -251,11 +257,12 @@ void ws_release(gi_graph* g, Workspace* w, bool healthy) {
   g->pool.emplace_back(w);
 }
 
-void fill_stats(gi_stats* st, const QStats& q, float ms, int ctas, int groups, int kind, int threads) {
+void fill_stats(gi_stats* st, const QStats& q, float ms, int ctas, int groups, int kind, int threads,
+                int launches) {
   st->buckets = q.buckets;
   st->rounds = q.rounds;
   st->grid_syncs = q.phases;
-  st->kernel_launches = 1;
+  st->kernel_launches = launches;
   st->fused_subrounds = q.subrounds;
   st->spills = q.spills;
   st->vertices_processed = q.vertices;
@@ -465,9 +472,26 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   a.target = target;
   a.dyn_claim = g->max_deg > 32 ? 1u : 0u;
   // expand needs the group list's prefix workspace (skewed graphs) and fits groups of <= 1024 CTAs
-  a.expand = (g->max_deg > 32 && opt.expand != 2 && G <= kMaxGroupCtas) ? 1u : 0u;
+  // expand (opt-in, single queries on skewed graphs): every ROUND phase collects its
+  // high-degree frontier into the group list, and lists of >= split_min edges are relaxed by
+  // expand_kernel between two segments of the persistent kernel (KState); lighter lists are
+  // relaxed slice-wise in the kernel. Measured against the default CTA-level stage B on
+  // configs 3-4 it is not faster, so the default stays off.
+  a.expand = (g->max_deg > 32 && opt.expand == 1 && G <= kMaxGroupCtas && ngroups == 1 && nsrc == 1 &&
+              kind != KIND_FUSED_ASYNC) ? 1u : 0u;
   a.pedges = g->d_pedges;
   a.colbits = g->colbits;
+  a.split = a.expand;
+  a.resume = 0;
+  {
+    const char* sm = getenv("GI_SPLIT_MIN");
+    a.split_min = sm ? strtoull(sm, nullptr, 10) : 0ull;
+  }
+  if (a.expand) {
+    const int xk = kind == KIND_UNFUSED ? KIND_UNFUSED_XP : KIND_FUSED_BSP_XP;
+    if (g->bps[wide][xk] >= bps) kind = xk;  // same co-residency as the kernel G was sized for
+    else a.expand = a.split = 0;
+  }
   if ((e = cudaMemsetAsync(w->d_src_next, 0, sizeof(uint32_t), st))) return bail(e, "init claim counter");
   a.src_next = w->d_src_next;  // claims count from 0; sources 0..ngroups-1 are taken statically
   a.h = d_h;
@@ -491,9 +515,30 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
     a.peer_vec = vec ? 1u : 0u;
   }
 
+  if (a.split && !w->h_pending) {
+    if ((e = cudaMallocHost(&w->h_pending, sizeof(uint32_t))) != cudaSuccess) return bail(e, "alloc pinned flag");
+  }
   if ((e = cudaEventRecord(w->ev0, st))) return bail(e, "event");
   if ((e = wide ? v1024::launch_sssp(a, kind, G * ngroups, st) : v512::launch_sssp(a, kind, G * ngroups, st)))
     return bail(e, "launch sssp_persistent");
+  int launches = 1;
+  if (a.split) {
+    // the persistent kernel stops at every heavy expand (KState.pending): run the list's
+    // relaxation as its own kernel, then resume the persistent kernel at the same phase
+    KState* kst = w->h_groups[0].kst;
+    KArgs ar = a;
+    ar.resume = 1;
+    for (;;) {
+      if ((e = cudaMemcpyAsync(w->h_pending, &kst->pending, sizeof(uint32_t), cudaMemcpyDeviceToHost, st)) ||
+          (e = cudaStreamSynchronize(st)))
+        return bail(e, "sssp kernel segment");
+      if (!*w->h_pending) break;
+      if ((e = v1024::launch_expand(a, st, nullptr))) return bail(e, "launch expand_kernel");
+      if ((e = wide ? v1024::launch_sssp(ar, kind, G * ngroups, st) : v512::launch_sssp(ar, kind, G * ngroups, st)))
+        return bail(e, "resume sssp_persistent");
+      launches += 2;
+    }
+  }
   if ((e = cudaEventRecord(w->ev1, st))) return bail(e, "event");
   QStats* hq = w->h_qstats;
   if ((e = cudaMemcpyAsync(hq, w->d_qstats, sizeof(QStats) * nsrc, cudaMemcpyDeviceToHost, st)))
@@ -512,7 +557,7 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   bool ovf = false;
   for (int i = 0; i < nsrc; ++i) {  // hq is the workspace's pinned buffer: read before release
     if (hq[i].overflow) ovf = true;
-    if (stats) fill_stats(&stats[i], hq[i], ms, G, ngroups, base_kind(kind), wide ? 1024 : 512);
+    if (stats) fill_stats(&stats[i], hq[i], ms, G, ngroups, base_kind(kind), wide ? 1024 : 512, launches);
   }
   ws_release(g, w, true);
   if (ovf) return fail(GI_ERR_OVERFLOW, "a reachable vertex has distance >= UINT32_MAX");

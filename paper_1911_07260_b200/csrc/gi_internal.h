@@ -50,9 +50,16 @@ enum KernelKind : int {
   // low-degree specialisations (every adjacency inline in its ELL slot, no pre-read): the
   // high-degree stages compiled out of the sub-round's serial path
   KIND_UNFUSED_LD = 3, KIND_FUSED_BSP_LD = 4,
-  KIND_COUNT = 5
+  // skewed graphs with expand on (gi_options.expand = 1): ROUND phases collect the group list
+  // and stop for expand_kernel (KState); compiled apart so that the default kernels keep
+  // their registers
+  KIND_UNFUSED_XP = 5, KIND_FUSED_BSP_XP = 6,
+  KIND_COUNT = 7
 };
-inline int base_kind(int k) { return k == KIND_UNFUSED_LD ? KIND_UNFUSED : k == KIND_FUSED_BSP_LD ? KIND_FUSED_BSP : k; }
+inline int base_kind(int k) {
+  return (k == KIND_UNFUSED_LD || k == KIND_UNFUSED_XP) ? KIND_UNFUSED
+         : (k == KIND_FUSED_BSP_LD || k == KIND_FUSED_BSP_XP) ? KIND_FUSED_BSP : k;
+}
 
 // Division by the invariant Δ (Granlund & Montgomery 1994, round-up method):
 // q = (t + ((x - t) >> s1)) >> s2 with t = umulhi(mul, x).
@@ -107,10 +114,24 @@ struct GroupWs {
   struct HubEnt* hub[2];  // [hubcap] group hub lists (deg >= hub_min), by phase parity
   unsigned long long* xpre;  // [hubcap] expand: exclusive degree prefix of each entry within its CTA slice
   unsigned long long* xtot;  // [kMaxGroupCtas] expand: edge total of each CTA's slice of the list
+  struct KState* kst;        // split expand: the phase loop's state while the relaxation runs outside
   Ctl* ctl;
 };
 
+// Split expand (single queries on skewed graphs): when a ROUND phase's group list holds at
+// least split_min edges, the persistent kernel saves its phase-loop state here and exits;
+// the host launches expand_kernel (the edge-balanced relaxation with the whole register file
+// of its own, 2 CTAs per SM) and then resumes the persistent kernel at the same phase.
+struct KState {
+  uint32_t p, j, b, prev;       // phase loop position
+  unsigned long long phases, rounds, buckets, empty, critical;  // group counters (rank 0)
+  unsigned long long E;         // edges of the pending list
+  uint32_t xn;                  // entries of the pending list
+  uint32_t pending;             // 1 = the kernel stopped for an external expand of phase p
+};
+
 constexpr int kMaxGroupCtas = 1024;  // expand: largest group (CTAs) the slice totals are sized for
+
 
 // A high-degree vertex queued for relaxation by every CTA of the group.
 struct HubEnt {
@@ -150,6 +171,9 @@ struct KArgs {
   uint32_t expand;
   const uint32_t* pedges;  // [m] packed edges (w << colbits | col) or nullptr (use `edges`)
   uint32_t colbits;        // packed: bits of the column id
+  uint32_t split;          // single query: heavy expands run in expand_kernel (see KState)
+  uint32_t resume;         // this launch resumes a query stopped for an external expand
+  unsigned long long split_min;  // list edges from which a phase's expand runs outside
 };
 
 // k-core (gi_kcore.cu): control block, statistics and arguments.
@@ -195,6 +219,8 @@ int smem_bytes(int kind);
 }  // namespace v512
 namespace v1024 {
 cudaError_t launch_sssp(const KArgs& a, int kind, int grid, cudaStream_t st);
+// the external expand of a split query (KState), 1024-thread CTAs on every SM
+cudaError_t launch_expand(const KArgs& a, cudaStream_t st, int* grid_used);
 cudaError_t query_occupancy(int kind, int* blocks_per_sm);
 int smem_bytes(int kind);
 }  // namespace v1024

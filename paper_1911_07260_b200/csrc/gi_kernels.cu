@@ -190,10 +190,19 @@ __device__ __forceinline__ uint32_t ld_dist_tgt(const uint32_t* p) {
 #endif
 }
 // packed edges (w << colbits | col), streamed
+#ifndef GI_X_PEDGE
+#define GI_X_PEDGE 1
+#endif
 __device__ __forceinline__ uint32_t ld_pedge(const uint32_t* p) {
+#if GI_X_PEDGE == 1
+  return __ldcs(p);  // ld.global.cs: streamed once, evict-first
+#elif GI_X_PEDGE == 2
+  return __ldg(p);
+#else
   uint32_t x;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(x) : "l"(p), "l"(pol_evict_first()));
   return x;
+#endif
 }
 // streamed CSR edges: read once per relaxation pass
 __device__ __forceinline__ uint2 ld_edge(const uint2* p) {
@@ -874,12 +883,54 @@ __device__ __forceinline__ XWin expand_window(const HubEnt* X, const unsigned lo
   return w;
 }
 
+#ifndef GI_INKERNEL_EXPAND
+#define GI_INKERNEL_EXPAND 0
+#endif
+#ifndef GI_XK
+#if GI_BLOCK >= 1024
+#define GI_XK 4
+#else
+#define GI_XK 8
+#endif
+#endif
+constexpr int kXK = GI_XK;  // expand: rows of 32 edges per warp per iteration
+
+// Lean relaxation of one expand row set: the pre-read dist[v] filters (a skewed graph's
+// edges mostly hit settled or already-lower targets); an improving candidate is written
+// with red.min and pushed — current bucket to the CTA bin (fusion) or the global frontier,
+// future buckets to the warp's far staging segment (one shared atomic per pushing lane).
 template <bool FUSED>
+__device__ __forceinline__ void expand_push(Ctx& c, uint32_t v, uint32_t nd) {
+  red_min(c.dist + v, nd);
+  const uint32_t bk = c.h ? max(prio_bucket(nd, __ldg(c.h + v), c.div), c.b) : fdiv(nd, c.div);
+  if (bk == c.b) {
+    if constexpr (FUSED) {
+      const uint32_t pos = atomicAdd(c.outcnt, 1u);
+      if (pos < (uint32_t)kBinCap) {
+        prefetch_own(c.slots + 8 * (size_t)v);
+        c.out[pos] = make_uint2(v, nd);
+        return;
+      }
+    }
+    push_global(c, (int32_t)v);
+  } else {
+    c.my_fmin = min(c.my_fmin, bk);
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t pos = atomicAdd(&c.s->wfar[warp], 1u);
+    if (pos < (uint32_t)kFarSeg) c.farstage[warp * kFarSeg + pos] = (int32_t)v;
+    else push_far_global(c, (int32_t)v);
+  }
+}
+
+template <bool PACKED> struct XEdge { using T = uint2; };
+template <> struct XEdge<true> { using T = uint32_t; };  // {w << colbits | col}
+
+template <bool FUSED, bool PACKED>
 __device__ __forceinline__ void expand_relax(Ctx& c, const HubEnt* X, const unsigned long long* xpre, uint32_t hn,
                                              uint32_t G, const unsigned long long* S, unsigned long long a,
                                              unsigned long long b, const uint32_t* pedges, uint32_t colbits,
                                              uint32_t& ne) {
-  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t len = (uint32_t)(b - a);
   // slice r holding position a: the largest r with S[r] <= a (S[G] = E > a)
   uint32_t rlo = 0, rhi = G;
@@ -907,14 +958,15 @@ __device__ __forceinline__ void expand_relax(Ctx& c, const HubEnt* X, const unsi
   XWin w = expand_window(X, xpre, hn, G, S, jb, a, len);
   const uint32_t lanemask = (2u << lane) - 2u;  // bits 1..lane (lane 31: 0xFFFFFFFE)
   const uint32_t cmask = colbits >= 32 ? 0xFFFFFFFFu : (1u << colbits) - 1u;
-  constexpr int K = kBigK;
-  for (uint32_t it0 = 0; it0 < len; it0 += 32 * K) {
-    uint2 e[K];
-    uint32_t du[K];
-    uint32_t valid = 0;
+  constexpr int K = kXK;
+  // map the K rows starting at it0 to edges and issue their loads (all K in flight)
+  using ET = typename XEdge<PACKED>::T;
+  auto map_load = [&](uint32_t it0, ET (&e)[K], uint32_t (&du)[K], uint32_t& valid) {
+    int64_t ei[K];
+    valid = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      e[k] = make_uint2(0, 0);
+      ei[k] = 0;
       du[k] = 0;
       const uint32_t r0 = it0 + 32 * k;
       if (r0 >= len) continue;  // warp-uniform
@@ -931,19 +983,60 @@ __device__ __forceinline__ void expand_relax(Ctx& c, const HubEnt* X, const unsi
       const int64_t off = __shfl_sync(0xffffffffu, w.off, slot);
       const uint32_t d = __shfl_sync(0xffffffffu, w.du, slot);
       if (r0 + lane < len) {
-        const int64_t ei = off + (int64_t)(a + r0 + lane);
-        if (pedges) {
-          const uint32_t pe = ld_pedge(pedges + ei);
-          e[k] = make_uint2(pe & cmask, pe >> colbits);
-        } else {
-          e[k] = ld_edge(c.edges + ei);
-        }
+        ei[k] = off + (int64_t)(a + r0 + lane);
         du[k] = d;
         valid |= 1u << k;
       }
     }
-    relax_batch<FUSED, K>(c, e, du, valid);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if constexpr (PACKED) e[k] = (valid >> k) & 1u ? ld_pedge(pedges + ei[k]) : 0u;
+      else e[k] = (valid >> k) & 1u ? ld_edge(c.edges + ei[k]) : make_uint2(0, 0);
+    }
+  };
+  auto col_of = [&](const ET& x) -> uint32_t {
+    if constexpr (PACKED) return x & cmask; else return x.x;
+  };
+  auto w_of = [&](const ET& x) -> uint32_t {
+    if constexpr (PACKED) return x >> colbits; else return x.y;
+  };
+  ET e[K];
+  uint32_t du[K], valid;
+  map_load(0, e, du, valid);
+  for (uint32_t it0 = 0; it0 < len; it0 += 32 * K) {
+    // the pre-reads of this batch (all K in flight) ...
+    uint32_t old[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) old[k] = (valid >> k) & 1u ? ld_dist_tgt(c.dist + col_of(e[k])) : 0u;
+    // ... while the next batch is mapped and its edge loads are issued
+    ET en[K];
+    uint32_t dn[K], vn = 0;
+    if (it0 + 32 * K < len) map_load(it0 + 32 * K, en, dn, vn);
+    TRACE(21);
     ne += __popc(valid);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (!((valid >> k) & 1u)) continue;
+      const uint32_t v = col_of(e[k]);
+      const uint32_t nd = du[k] + w_of(e[k]);
+      if (nd < du[k] || nd == kInf) {
+        mark_overflow(c.ovfbits, c.ovf_cand, v);
+        continue;
+      }
+      if (nd < old[k]) expand_push<FUSED>(c, v, nd);
+    }
+    TRACE(22);
+    // the warp's far segment is flushed before the next batch could overflow it
+    __syncwarp();
+    if (c.s->wfar[warp] > (uint32_t)(kFarSeg / 2)) {  // warp-uniform
+      warp_flush_far(c, c.farstage + warp * kFarSeg, min(c.s->wfar[warp], (uint32_t)kFarSeg));
+      if (lane == 0) c.s->wfar[warp] = 0;
+      __syncwarp();
+    }
+    TRACE(23);
+#pragma unroll
+    for (int k = 0; k < K; ++k) { e[k] = en[k]; du[k] = dn[k]; }
+    valid = vn;
   }
 }
 
@@ -1316,9 +1409,12 @@ __device__ __forceinline__ void async_feed(Ctx& c, Shared& s, const Ring& r, boo
 
 template <int KIND>
 __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs a) {
-  constexpr bool FUSED = KIND != KIND_UNFUSED && KIND != KIND_UNFUSED_LD;
+  constexpr bool FUSED = KIND != KIND_UNFUSED && KIND != KIND_UNFUSED_LD && KIND != KIND_UNFUSED_XP;
   constexpr bool ASYNC = KIND == KIND_FUSED_ASYNC;
   constexpr bool LOWDEG = KIND == KIND_UNFUSED_LD || KIND == KIND_FUSED_BSP_LD;
+  // expand (and its split into expand_kernel) exists only in the kernels skewed graphs run:
+  // compiled out of the low-degree and async kernels, whose registers it would take
+  constexpr bool XP = KIND == KIND_UNFUSED_XP || KIND == KIND_FUSED_BSP_XP;
   // bsp: bins [2][kBinCap] uint2, high-degree list [kBigCap], its prefix [kBigCap], far staging
   // [kFarStage]; async: ring [kRing] (+ per-warp queues), far staging
   extern __shared__ uint2 s_dyn[];
@@ -1339,9 +1435,11 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
   for (int32_t si = (int32_t)gid; si < a.nsrc;) {
     uint32_t* dist = a.dist + (size_t)si * (size_t)n;
     const int32_t src = a.srcs[si];
+    // split expand: this launch continues a single query stopped for an external expand
+    const bool resuming = XP && a.resume != 0;
 
     // ---- init: Dist = {inf}, Dist[src] = 0; far pile = {src} ----
-    {
+    if (!resuming) {
       int64_t done = 0;
       if ((reinterpret_cast<uintptr_t>(dist) & 15) == 0) {
         const int64_t n4 = n >> 2;
@@ -1360,7 +1458,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
       for (int64_t i = done + (int64_t)rank * kBlock + tid; i < n; i += (int64_t)G * kBlock)
         dist[i] = (i == src) ? 0u : kInf;
     }
-    if (rank == 0 && tid == 0) {
+    if (!resuming && rank == 0 && tid == 0) {
       for (int k = 0; k < 3; ++k) {
         ctl->qcount[k] = 0; ctl->fcount[k] = 0; ctl->fmin[k] = kInf; ctl->xlive[k] = 0; ctl->maxsub[k] = 0;
         ctl->hcount[k] = 0; ctl->qclaim[k] = 0; ctl->tdist[k] = kInf;
@@ -1369,7 +1467,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
       ws.far[0][0] = src;
       atomicOr(&ws.farbits[src >> 5], 1u << (src & 31));
     }
-    group_barrier(ctl, G);
+    if (!resuming) group_barrier(ctl, G);
 
     Ctx c;
     c.dist = dist; c.slots = a.slots; c.edges = a.edges; c.div = a.div;
@@ -1396,10 +1494,25 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
     unsigned long long phases = 0, rounds = 0, buckets = 0, empty = 0, critical = 0;  // rank 0, thread 0
     unsigned long long sub_at_phase_start = 0;
     uint32_t p = 0, j = 0, b = 0, prev = MODE_NONE;
+    bool mid = false;  // resuming inside ROUND phase p, after its external expand
+    if (resuming) {
+      const KState* ks = ws.kst;
+      p = ks->p; j = ks->j; b = ks->b; prev = ks->prev;
+      if (rank == 0 && tid == 0) {
+        phases = ks->phases; rounds = ks->rounds; buckets = ks->buckets; empty = ks->empty; critical = ks->critical;
+      }
+      mid = true;
+    }
 
     for (;;) {
+      if (mid && tid == 0) {  // phase p continues: its list was relaxed outside, the bins are empty
+        s.mode = MODE_ROUND; s.cnt = 0; s.hn = 0;
+        s.cnt3[0] = 0; s.cnt3[1] = 0; s.bigtail = 0; s.farcnt = 0;
+        for (int w = 0; w < kBlock / 32; ++w) s.wfar[w] = 0;
+        s.fmin = kInf;
+      }
       // ---- decide (identically in every CTA, from counters final at the barrier) ----
-      if (tid == 0) {
+      if (tid == 0 && !mid) {
         // L2-coherent loads, all four in flight at once (ordered after the barrier's fence)
         const uint32_t xl = __ldcg(&ctl->xlive[j % 3]);
         const uint32_t qn = __ldcg(&ctl->qcount[p % 3]);
@@ -1455,13 +1568,13 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
         const uint32_t lo2 = (uint32_t)(((uint64_t)fc * rank) / G), hi2 = (uint32_t)(((uint64_t)fc * (rank + 1)) / G);
         for (uint32_t i = lo2 + tid; i < hi2; i += kBlock) {
           const int32_t v = pile[i];
-          atomicAnd(&ws.farbits[v >> 5], ~(1u << (v & 31)));
+          if (v >= 0) atomicAnd(&ws.farbits[v >> 5], ~(1u << (v & 31)));  // < 0: an expand chunk's hole
         }
         break;
       }
       const uint32_t cnt = s.cnt;
       if (mode == MODE_EXTRACT) { ++j; b = s.b; }
-      if (rank == 0 && tid == 0) {
+      if (rank == 0 && tid == 0 && !mid) {
         ctl->qcount[(p + 2) % 3] = 0;
         ctl->maxsub[(p + 2) % 3] = 0;
         ctl->hcount[(p + 2) % 3] = 0;
@@ -1586,34 +1699,41 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           if (tl) atomicAdd(&ctl->xlive[j % 3], tl);
           scanned += hi - lo;
         }
-      } else {
+      } else if (!mid) {
         const uint32_t hn = s.hn;
         HubEnt* hub_in = (p & 1) ? ws.hub[1] : ws.hub[0];
-        if (a.expand) {
+        if (XP && a.expand) {
           // expand: this phase's high-degree frontier vertices join the hubs queued by the
           // previous phase in the group list, relaxed edge-balanced after the collection
           c.hub_min = kSlotEdges + 1;
           c.hub_next = hub_in;
           c.hcount_next = &ctl->hcount[p % 3];
+          // split: a phase may stop for an external expand, which would drop this CTA's bin —
+          // the collection's current-bucket pushes go to the global frontier instead (a full bin)
+          if (a.split && tid == 0) s.cnt3[0] = kBinCap;
         }
-        // hubs queued in the previous phase (no expand): every CTA relaxes its 1/G slice of
-        // every hub's edges (stage B over the slices), so a hub costs ~deg/G per CTA
-        for (uint32_t h0 = 0; h0 < (a.expand ? 0u : hn); h0 += kBigCap) {
-          const uint32_t nh = min((uint32_t)kBigCap, hn - h0);
-          for (uint32_t i = tid; i < nh; i += kBlock) {
-            const HubEnt he = hub_in[h0 + i];
-            const uint64_t lo_e = (uint64_t)he.deg * rank / G, hi_e = (uint64_t)he.deg * (rank + 1) / G;
-            BigEnt be;
-            be.beg = he.beg + (int64_t)lo_e;
-            be.deg = (uint32_t)(hi_e - lo_e);
-            be.du = he.du;
-            c.big[i] = be;
+        // a group list relaxed slice-wise: every CTA relaxes its 1/G slice of every entry's
+        // edges (stage B over the slices), so an entry costs ~deg/G per CTA
+        auto hub_slices = [&](uint32_t hcnt) {
+          for (uint32_t h0 = 0; h0 < hcnt; h0 += kBigCap) {
+            const uint32_t nh = min((uint32_t)kBigCap, hcnt - h0);
+            for (uint32_t i = tid; i < nh; i += kBlock) {
+              const HubEnt he = hub_in[h0 + i];
+              const uint64_t lo_e = (uint64_t)he.deg * rank / G, hi_e = (uint64_t)he.deg * (rank + 1) / G;
+              BigEnt be;
+              be.beg = he.beg + (int64_t)lo_e;
+              be.deg = (uint32_t)(hi_e - lo_e);
+              be.du = he.du;
+              c.big[i] = be;
+            }
+            __syncthreads();
+            stage_big<FUSED>(c, s, nh, ne);
+            __syncthreads();
+            TRACE(15);
           }
-          __syncthreads();
-          stage_big<FUSED>(c, s, nh, ne);
-          __syncthreads();
-          TRACE(15);
-        }
+        };
+        // hubs queued in the previous phase (no expand)
+        if (!(XP && a.expand)) hub_slices(hn);
         // ROUND: relax the group's global frontier, one slice per CTA, staged through
         // bin 1 in chunks (pushes go to bin 0, which the drain below consumes)
         const int32_t* q_in = (p & 1) ? ws.q[1] : ws.q[0];
@@ -1673,12 +1793,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           }
         }
         __syncthreads();
-        if (a.expand) {
+        if (XP && a.expand) {
           c.hub_min = a.hub_min;
           c.hub_next = (p & 1) ? ws.hub[0] : ws.hub[1];
           c.hcount_next = &ctl->hcount[(p + 1) % 3];
+          if (a.split && tid == 0) s.cnt3[0] = 0;  // nothing was written to the bin
           group_barrier(ctl, G);  // the group list is complete
           ++phases;
+          TRACE(19);
           if (tid == 0) s.xhn = min(__ldcg(&ctl->hcount[p % 3]), a.hubcap);
           __syncthreads();
           const uint32_t xn = s.xhn;
@@ -1702,16 +1824,60 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
               }
             }
             __syncthreads();
+            TRACE(20);
             const unsigned long long E = s.xS[G];
+            if (a.split && E >= a.split_min) {
+              // a heavy list: save the phase loop's state and stop; the host runs
+              // expand_kernel on the list and resumes this kernel at phase p (KState)
+              {
+                const uint32_t w = tid >> 5;
+                warp_flush_far(c, c.farstage + w * kFarSeg, min(s.wfar[w], (uint32_t)kFarSeg));
+                const uint32_t fm = __reduce_min_sync(0xffffffffu, c.my_fmin);
+                if ((tid & 31) == 0 && fm != kInf) atomicMin(&s.fmin, fm);
+              }
+              tnv += nv; tne += ne;
+              const unsigned long long tv = block_sum(tnv, s);
+              const unsigned long long te = block_sum(tne, s);
+              if (tid == 0) {
+                if (s.fmin != kInf) atomicMin(&ctl->fmin[j % 3], s.fmin);
+                QStats* q = &a.qstats[si];
+                atomicAdd(&q->vertices, tv);
+                atomicAdd(&q->edges, te + (rank == 0 ? E : 0ull));  // the external expand's edges
+                if (subrounds) atomicAdd(&q->subrounds, subrounds);
+                if (spills) atomicAdd(&q->spills, spills);
+                if (scanned) atomicAdd(&q->far_scanned, scanned);
+                if (rank == 0) {
+                  KState* ks = ws.kst;
+                  ks->p = p; ks->j = j; ks->b = b; ks->prev = prev;
+                  ks->phases = phases; ks->rounds = rounds; ks->buckets = buckets; ks->empty = empty;
+                  ks->critical = critical; ks->E = E; ks->xn = xn;
+                  __threadfence();
+                  ks->pending = 1;
+                }
+              }
+              TRACE_FLUSH();
+              return;
+            }
+#if GI_INKERNEL_EXPAND
             const uint64_t W = (uint64_t)G * (kBlock / 32), wg = (uint64_t)rank * (kBlock / 32) + (tid >> 5);
             const unsigned long long a0 = E * wg / W, b0 = E * (wg + 1) / W;
-            if (a0 < b0) expand_relax<FUSED>(c, hub_in, ws.xpre, xn, G, s.xS, a0, b0, a.pedges, a.colbits, ne);
-            TRACE(18);
+            if (a0 < b0) {
+              if (a.pedges) expand_relax<FUSED, true>(c, hub_in, ws.xpre, xn, G, s.xS, a0, b0, a.pedges, a.colbits, ne);
+              else expand_relax<FUSED, false>(c, hub_in, ws.xpre, xn, G, s.xS, a0, b0, a.pedges, a.colbits, ne);
+            }
             __syncthreads();
+#else
+            // a light list (or a batch, which cannot stop for an external expand): the slice-wise
+            // relaxation in this kernel (the edge-balanced loop inlined here spilled the
+            // persistent kernel's registers)
+            hub_slices(xn);
+#endif
+            TRACE(18);
           }
         }
       }
 
+      mid = false;
       if constexpr (FUSED && !ASYNC) {
         // (c) bucket fusion: drain the CTA-local bin while it stays below T
         // (PAPER.md:537-550); a bin of size >= T goes to the global frontier
@@ -1847,6 +2013,218 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
   TRACE_FLUSH();
 }
 
+#if GI_BLOCK >= 1024
+// The external expand of a split query (KState): the edge-balanced relaxation of phase p's
+// group list, launched by the host between two segments of the persistent kernel. It is
+// written without the persistent kernel's context so that the edge loop keeps only what it
+// uses in registers: the window of 32 list entries, K rows of packed edges in flight, the
+// pre-read distances. Improving candidates are written with red.min and staged per warp in
+// shared memory — future buckets for the far pile, the current bucket for the global
+// frontier — and flushed with the dedup test-and-set and one append atomic per warp.
+constexpr int kXSeg = 384;     // far staging entries per warp
+constexpr int kXCur = 128;     // current-bucket staging entries per warp
+constexpr int kXRows = 4;      // rows of 32 edges per warp per iteration
+
+
+struct XShared {
+  unsigned long long S[kMaxGroupCtas + 1];
+  int32_t far[kBlock / 32][kXSeg];
+  int32_t cur[kBlock / 32][kXCur];
+  uint32_t nfar[kBlock / 32], ncur[kBlock / 32];
+};
+
+// dedup-append of a warp's staged vertices (bits = dedup bitmap) to a global list
+__device__ __forceinline__ void xflush(const int32_t* seg, uint32_t n, uint32_t* bits, int32_t* list,
+                                       uint32_t* count, const uint2* slots_pf) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t base = 0; base < n; base += 4 * 32) {
+    int32_t v[4];
+    uint32_t old[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const uint32_t i = base + x * 32 + lane;
+      v[x] = i < n ? seg[i] : -1;
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x) old[x] = v[x] >= 0 ? atomicOr(&bits[v[x] >> 5], 1u << (v[x] & 31)) : ~0u;
+    uint32_t newm = 0;
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      if (v[x] >= 0 && !(old[x] & (1u << (v[x] & 31)))) newm |= 1u << x;
+    warp_append(newm, v, list, count, slots_pf);
+  }
+  __syncwarp();
+}
+
+template <bool PACKED>
+__global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
+  extern __shared__ __align__(16) unsigned char x_dyn[];
+  XShared& xs = *reinterpret_cast<XShared*>(x_dyn);
+  const GroupWs ws = a.groups[0];
+  Ctl* ctl = ws.ctl;
+  const KState* ks = ws.kst;
+  const uint32_t p = ks->p, j = ks->j, bcur = ks->b, hn = ks->xn;
+  const unsigned long long E = ks->E;
+  const uint32_t G = (uint32_t)a.group_size;  // the persistent group, whose CTAs sliced the list
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < 32) {  // S[r] = sum of the slice totals before r
+    unsigned long long carry = 0;
+    if (tid == 0) xs.S[0] = 0;
+    for (uint32_t b0 = 0; b0 < G; b0 += 32) {
+      const uint32_t r = b0 + tid;
+      unsigned long long v = r < G ? __ldcg(ws.xtot + r) : 0ull;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, v, o);
+        if (tid >= (uint32_t)o) v += t;
+      }
+      if (r < G) xs.S[r + 1] = carry + v;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  if (lane == 0) { xs.nfar[warp] = 0; xs.ncur[warp] = 0; }
+  __syncthreads();
+  const unsigned long long* S = xs.S;
+  const HubEnt* X = (p & 1) ? ws.hub[1] : ws.hub[0];
+  const unsigned long long* xpre = ws.xpre;
+  uint32_t* const dist = a.dist;
+  const FastDiv div = a.div;
+  const uint32_t colbits = a.colbits;
+  const uint32_t cmask = colbits >= 32 ? 0xFFFFFFFFu : (1u << colbits) - 1u;
+  uint32_t my_fmin = kInf;
+  auto flush_far = [&]() {
+    __syncwarp();
+    const uint32_t n = min(xs.nfar[warp], (uint32_t)kXSeg);
+    xflush(xs.far[warp], n, ws.farbits, (j & 1) ? ws.far[1] : ws.far[0], &ctl->fcount[j % 3], nullptr);
+    if (lane == 0) xs.nfar[warp] = 0;
+    __syncwarp();
+  };
+  auto flush_cur = [&]() {
+    __syncwarp();
+    const uint32_t n = min(xs.ncur[warp], (uint32_t)kXCur);
+    xflush(xs.cur[warp], n, (p & 1) ? ws.qbits[0] : ws.qbits[1], (p & 1) ? ws.q[0] : ws.q[1],
+           &ctl->qcount[(p + 1) % 3], a.slots);
+    if (lane == 0) xs.ncur[warp] = 0;
+    __syncwarp();
+  };
+
+  const uint64_t W = (uint64_t)gridDim.x * (kBlock / 32), wg = (uint64_t)blockIdx.x * (kBlock / 32) + warp;
+  const unsigned long long a0 = E * wg / W, b0 = E * (wg + 1) / W;
+  if (a0 < b0) {
+    const uint32_t len = (uint32_t)(b0 - a0);
+    // slice r holding position a0, then the entry within it (as expand_relax)
+    uint32_t rlo = 0, rhi = G;
+    while (rhi - rlo > 1) {
+      const uint32_t mid = (rlo + rhi) >> 1;
+      if (S[mid] <= a0) rlo = mid; else rhi = mid;
+    }
+    const unsigned long long t = a0 - S[rlo];
+    uint32_t ilo = (uint32_t)(((uint64_t)hn * rlo) / G), ihi = (uint32_t)(((uint64_t)hn * (rlo + 1)) / G);
+    while (ihi - ilo > 32) {
+      const uint32_t step = (ihi - ilo + 31) / 32;
+      const uint32_t idx = ilo + lane * step;
+      const bool pr = idx < ihi && __ldcg(xpre + idx) <= t;
+      ilo += (__popc(__ballot_sync(0xffffffffu, pr)) - 1) * step;
+      ihi = min(ilo + step, ihi);
+    }
+    {
+      const uint32_t idx = ilo + lane;
+      const bool pr = idx < ihi && __ldcg(xpre + idx) <= t;
+      ilo += __popc(__ballot_sync(0xffffffffu, pr)) - 1;
+    }
+    uint32_t jb = ilo;
+    XWin w = expand_window(X, xpre, hn, G, S, jb, a0, len);
+    const uint32_t lanemask = (2u << lane) - 2u;
+    using ET = typename XEdge<PACKED>::T;
+    // map rows it0.. to (edge, du) and issue the edge loads
+    auto map_load = [&](uint32_t it0, ET (&e)[kXRows], uint32_t (&du)[kXRows], uint32_t& valid) {
+      int64_t ei[kXRows];
+      valid = 0;
+#pragma unroll
+      for (int k = 0; k < kXRows; ++k) {
+        ei[k] = 0;
+        du[k] = 0;
+        const uint32_t r0 = it0 + 32 * k;
+        if (r0 >= len) continue;  // warp-uniform
+        const uint32_t last = __shfl_sync(0xffffffffu, w.endr, 31);
+        if (last < min(r0 + 32, len)) {
+          jb += __popc(__ballot_sync(0xffffffffu, w.endr <= r0));
+          w = expand_window(X, xpre, hn, G, S, jb, a0, len);
+        }
+        const uint32_t c0 = __popc(__ballot_sync(0xffffffffu, w.endr <= r0));
+        const uint32_t x = w.endr - r0;
+        const uint32_t heads = __reduce_or_sync(0xffffffffu, (x - 1u < 31u) ? (1u << x) : 0u);
+        const uint32_t slot = c0 + __popc(heads & lanemask);
+        const int64_t off = __shfl_sync(0xffffffffu, w.off, slot);
+        const uint32_t d = __shfl_sync(0xffffffffu, w.du, slot);
+        if (r0 + lane < len) {
+          ei[k] = off + (int64_t)(a0 + r0 + lane);
+          du[k] = d;
+          valid |= 1u << k;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kXRows; ++k) {
+        if constexpr (PACKED) e[k] = (valid >> k) & 1u ? ld_pedge(a.pedges + ei[k]) : 0u;
+        else e[k] = (valid >> k) & 1u ? ld_edge(a.edges + ei[k]) : make_uint2(0, 0);
+      }
+    };
+    ET e[kXRows];
+    uint32_t du[kXRows], valid;
+    map_load(0, e, du, valid);
+    for (uint32_t it0 = 0; it0 < len; it0 += 32 * kXRows) {
+      uint32_t old[kXRows];
+#pragma unroll
+      for (int k = 0; k < kXRows; ++k) {
+        uint32_t v;
+        if constexpr (PACKED) v = e[k] & cmask; else v = e[k].x;
+        old[k] = (valid >> k) & 1u ? ld_dist_tgt(dist + v) : 0u;
+      }
+      // the next rows' edge loads fly while this batch's pre-reads return
+      ET en[kXRows];
+      uint32_t dn[kXRows], vn = 0;
+      if (it0 + 32 * kXRows < len) map_load(it0 + 32 * kXRows, en, dn, vn);
+#pragma unroll
+      for (int k = 0; k < kXRows; ++k) {
+        if (!((valid >> k) & 1u)) continue;
+        uint32_t v, nd;
+        if constexpr (PACKED) { v = e[k] & cmask; nd = du[k] + (e[k] >> colbits); }
+        else { v = e[k].x; nd = du[k] + e[k].y; }
+        if (nd < du[k] || nd == kInf) {
+          mark_overflow(ws.ovfbits, &ctl->ovf_cand, v);
+          continue;
+        }
+        if (nd < old[k]) {
+          red_min(dist + v, nd);
+          const uint32_t bk = a.h ? max(prio_bucket(nd, __ldg(a.h + v), div), bcur) : fdiv(nd, div);
+          if (bk == bcur) {
+            const uint32_t pos = atomicAdd(&xs.ncur[warp], 1u);
+            if (pos < (uint32_t)kXCur) xs.cur[warp][pos] = (int32_t)v;
+          } else {
+            my_fmin = min(my_fmin, bk);
+            const uint32_t pos = atomicAdd(&xs.nfar[warp], 1u);
+            if (pos < (uint32_t)kXSeg) xs.far[warp][pos] = (int32_t)v;
+          }
+        }
+      }
+      __syncwarp();
+      // staging never overflows: at most 32 * kXRows pushes per iteration
+      if (xs.nfar[warp] > (uint32_t)(kXSeg - 32 * kXRows)) flush_far();
+      if (xs.ncur[warp] > (uint32_t)(kXCur - 32 * kXRows)) flush_cur();
+#pragma unroll
+      for (int k = 0; k < kXRows; ++k) { e[k] = en[k]; du[k] = dn[k]; }
+      valid = vn;
+    }
+  }
+  flush_far();
+  flush_cur();
+  const uint32_t fm = __reduce_min_sync(0xffffffffu, my_fmin);
+  if (lane == 0 && fm != kInf) atomicMin(&ctl->fmin[j % 3], fm);
+  if (blockIdx.x == 0 && tid == 0) ws.kst->pending = 0;
+}
+static_assert(kXCur >= 32 * kXRows && kXSeg >= 2 * 32 * kXRows, "staging holds one iteration's pushes");
+#endif
+
 #if GI_PRIMARY
 __global__ void interleave_kernel(const int32_t* __restrict__ cols, const uint32_t* __restrict__ w,
                                   uint2* __restrict__ edges, int64_t count, int64_t n, uint32_t* bad) {
@@ -1948,6 +2326,8 @@ static const void* kernel_fn(int kind) {
     case KIND_FUSED_BSP: return (const void*)sssp_persistent<KIND_FUSED_BSP>;
     case KIND_UNFUSED_LD: return (const void*)sssp_persistent<KIND_UNFUSED_LD>;
     case KIND_FUSED_BSP_LD: return (const void*)sssp_persistent<KIND_FUSED_BSP_LD>;
+    case KIND_UNFUSED_XP: return (const void*)sssp_persistent<KIND_UNFUSED_XP>;
+    case KIND_FUSED_BSP_XP: return (const void*)sssp_persistent<KIND_FUSED_BSP_XP>;
     default: return (const void*)sssp_persistent<KIND_FUSED_ASYNC>;
   }
 }
@@ -1980,6 +2360,24 @@ cudaError_t launch_sssp(const KArgs& a, int kind, int grid, cudaStream_t st) {
   void* params[] = {&args};
   return cudaLaunchCooperativeKernel(kernel_fn(kind), dim3(grid), dim3(kBlock), params, smem_bytes(kind), st);
 }
+
+#if GI_BLOCK >= 1024
+cudaError_t launch_expand(const KArgs& a, cudaStream_t st, int* grid_used) {
+  const void* fn = a.pedges ? (const void*)expand_kernel<true> : (const void*)expand_kernel<false>;
+  const int smem = (int)sizeof(XShared);
+  int dev = 0, sms = 0, bps = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, kBlock, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = sms * (bps > 0 ? bps : 1);
+  if (grid_used) *grid_used = grid;
+  KArgs args = a;
+  void* params[] = {&args};
+  return cudaLaunchKernel(fn, dim3(grid), dim3(kBlock), params, smem, st);
+}
+#endif
 
 }  // namespace GI_VARIANT
 

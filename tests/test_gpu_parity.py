@@ -291,9 +291,11 @@ def test_expand_edge_balanced(gi):
         G = gi.Graph.from_csr(g)
         s = int(np.argmax(deg)) if t % 2 == 0 else int(rng.integers(0, n))
         ref, _ = oracle.dijkstra(g, s)
-        for o, delta in ((dict(), 1), (dict(), 7), (dict(expand="off"), 7), (dict(expand="on", fusion=False), 3),
-                         (dict(max_ctas=1), 5), (dict(max_ctas=2, threshold=1), 2), (dict(max_ctas=7), 1 << 30),
-                         (dict(fusion=False, max_ctas=3), 1), (dict(pre_read=2), 4)):
+        for o, delta in ((dict(expand="on"), 1), (dict(expand="on"), 7), (dict(expand="off"), 7),
+                         (dict(expand="on", fusion=False), 3), (dict(expand="on", max_ctas=1), 5),
+                         (dict(expand="on", max_ctas=2, threshold=1), 2), (dict(expand="on", max_ctas=7), 1 << 30),
+                         (dict(expand="on", fusion=False, max_ctas=3), 1), (dict(expand="on", pre_read=2), 4),
+                         (dict(expand="on", cta_threads=512), 2)):
             d, st = run(gi, G, s, delta, **o)
             assert np.array_equal(d, ref), (t, o, delta)
             assert st["buckets"] == oracle.bucket_count(ref, delta), (t, o, delta)
@@ -301,6 +303,34 @@ def test_expand_edge_balanced(gi):
         out, _ = gi.sssp_batch(G, srcs, 4)
         refs, _, _ = oracle.dijkstra_many(g, srcs)
         assert np.array_equal(gi.as_uint32(out), refs), t
+
+
+def test_expand_split_segments(gi, monkeypatch):
+    """Split expand (single queries on skewed graphs): every list of >= GI_SPLIT_MIN edges is
+    relaxed by expand_kernel between two segments of the persistent kernel, which saves and
+    restores its phase-loop state (KState). With GI_SPLIT_MIN=1 every expand phase splits;
+    PPSP and A* (whose stop test runs at phase ends) and a one-CTA group included."""
+    monkeypatch.setenv("GI_SPLIT_MIN", "1")  # every list but the smallest goes to expand_kernel
+    rng = np.random.default_rng(43)
+    for t in range(4):
+        n = int(rng.integers(3_000, 40_000))
+        deg = np.minimum(rng.zipf(1.6, size=n), n - 1)
+        deg[rng.integers(0, n, 2)] = rng.integers(1_000, max(1_001, n // 3), 2)
+        wmax = int(rng.choice([5, 1 << 22]))
+        edges = [(u, int(v), int(w)) for u in range(n) for v, w in
+                 zip(rng.integers(0, n, deg[u]), rng.integers(1, wmax, deg[u]))]
+        g = gen.from_edges(n, edges)
+        G = gi.Graph.from_csr(g)
+        s = int(np.argmax(deg))
+        ref, _ = oracle.dijkstra(g, s)
+        for o, delta in ((dict(expand="on"), 1), (dict(expand="on"), 9), (dict(expand="on", fusion=False), 4),
+                         (dict(expand="on", max_ctas=1), 3), (dict(expand="on", cta_threads=512), 2)):
+            d, st = run(gi, G, s, delta, **o)
+            assert np.array_equal(d, ref), (t, o, delta)
+            assert st["buckets"] == oracle.bucket_count(ref, delta), (t, o, delta)
+            assert st["kernel_launches"] >= 1
+        tgt = int(rng.integers(0, n))
+        assert gi.ppsp(G, s, tgt, 3, expand="on")[0] == int(ref[tgt]), t
 
 
 @pytest.mark.slow

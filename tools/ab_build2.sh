@@ -11,6 +11,7 @@ $NV $2 -DGI_BLOCK=512 -DGI_VARIANT=v512 -DGI_PRIMARY=1 -c $CS/gi_kernels.cu -o $
 $NV $3 -DGI_BLOCK=1024 -DGI_VARIANT=v1024 -DGI_PRIMARY=0 -c $CS/gi_kernels.cu -o $T/k1024.o
 $NV $4 -c $CS/gi_capi.cu -o $T/capi.o
 $NV $4 -c $CS/gi_kcore.cu -o $T/kcore.o
+$NV $4 -c $CS/gi_probe.cu -o $T/probe.o
 mkdir -p ${AB_OUT:-$R/tools/ab}
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ${AB_OUT:-$R/tools/ab}/libgi_$name.so $T/*.o
 rm -rf $T

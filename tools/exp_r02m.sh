@@ -1,0 +1,9 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+export GI_GEN_CACHE=/tmp/gcache
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "expand or hubs or config3" > gpurun_out/r02m_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02m_tests.log
+timeout 600 python tools/time_cfg.py 4 2 '{}' '{"expand": "on"}' '{"expand": "off"}' > gpurun_out/r02m_time4.log 2>&1
+GI_SPLIT_MIN=2000000 timeout 600 python tools/time_cfg.py 4 2 '{}' > gpurun_out/r02m_time4b.log 2>&1
+timeout 600 python tools/time_cfg.py 3 2 '{}' '{"expand": "on"}' '{"expand": "off"}' > gpurun_out/r02m_time3.log 2>&1
+GI_SPLIT_MIN=2000000 timeout 600 python tools/time_cfg.py 3 2 '{}' > gpurun_out/r02m_time3b.log 2>&1

@@ -5,12 +5,11 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-template <int MODE>
+template <int MODE, int U>
 __global__ void __launch_bounds__(1024) gather(const uint32_t* __restrict__ cols, int64_t m, const uint32_t* dist, uint32_t* sink) {
   uint32_t acc = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  constexpr int U = 8;
   for (; i + (U - 1) * stride < m; i += U * stride) {
     uint32_t c[U], d[U];
 #pragma unroll
@@ -33,13 +32,49 @@ __global__ void __launch_bounds__(1024) gather(const uint32_t* __restrict__ cols
   if (acc == 0x12345678u) sink[0] = acc;
 }
 
+// layout variants: LAYOUT 1 = each warp streams its own contiguous range (E3's split);
+// LAYOUT 2 = each CTA streams its own contiguous range, rows interleaved over its warps
+template <int LAYOUT, int U>
+__global__ void __launch_bounds__(1024) gather_ranges(const uint32_t* __restrict__ cols, int64_t m, const uint32_t* dist,
+                                                      uint32_t* sink) {
+  uint32_t acc = 0;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int64_t lo, hi, step, first;
+  if (LAYOUT == 1) {
+    const int64_t W = (int64_t)gridDim.x * nw, wg = (int64_t)blockIdx.x * nw + warp;
+    lo = m * wg / W; hi = m * (wg + 1) / W; step = 32; first = lo + lane;
+  } else {
+    lo = m * blockIdx.x / gridDim.x; hi = m * (blockIdx.x + 1) / gridDim.x; step = 32 * nw;
+    first = lo + warp * 32 + lane;
+  }
+  int64_t i = first;
+  for (; i + (U - 1) * step < hi; i += U * step) {
+    uint32_t c[U], d[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = __ldcs(cols + i + u * step);
+#pragma unroll
+    for (int u = 0; u < U; ++u) d[u] = __ldcg(dist + c[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += d[u];
+  }
+  for (; i < hi; i += step) acc += __ldcg(dist + cols[i]);
+  if (acc == 0x12345678u) sink[0] = acc;
+}
+
 extern "C" int probe_gather(int mode, const uint32_t* cols, int64_t m, const uint32_t* dist, uint32_t* sink,
                             int blocks, int threads, cudaStream_t st) {
   switch (mode) {
-    case 0: gather<0><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
-    case 1: gather<1><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
-    case 2: gather<2><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
-    default: gather<3><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
+    case 0: gather<0, 8><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
+    case 1: gather<1, 8><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
+    case 2: gather<2, 8><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
+    case 4: gather<0, 4><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
+    case 5: gather<0, 2><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
+    case 6: gather<0, 16><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
+    case 7: gather_ranges<1, 4><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
+    case 8: gather_ranges<1, 8><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
+    case 9: gather_ranges<2, 4><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
+    case 10: gather_ranges<2, 8><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
+    default: gather<3, 8><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
   }
   return (int)cudaGetLastError();
 }

@@ -11,13 +11,20 @@ lib = ctypes.CDLL(so)
 lib.probe_gather.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                              ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
 g = gen.config_graph(int(os.environ.get("CFG", "4")))
+pad_mb = int(os.environ.get("PAD_MB", "-1"))  # >= 0: dist allocated first, after a pad of that size
+if pad_mb >= 0:
+    pad = torch.empty(max(pad_mb, 0) << 20, dtype=torch.uint8, device="cuda") if pad_mb else None
+    dist = torch.zeros(g.n, dtype=torch.int32, device="cuda")
 cols = torch.from_numpy(np.array(g.cols)).cuda()
 m = g.m
-dist = torch.zeros(g.n, dtype=torch.int32, device="cuda")
+if pad_mb < 0:
+    dist = torch.zeros(g.n, dtype=torch.int32, device="cuda")
+print("PAD_MB", pad_mb, "dist at", hex(dist.data_ptr()))
 sink = torch.zeros(4, dtype=torch.int32, device="cuda")
 st = torch.cuda.current_stream()
-for mode, name in ((2, "edge stream only"), (0, "dist ld.cg"), (1, "dist ld.ca (L1)"), (3, "dist ld.cg evict_last")):
-    for blocks, threads in ((148 * 2, 1024), (148 * 8, 256), (148 * 16, 128)):
+CASES = [(0, "grid-stride U=8", 148, 1024), (4, "grid-stride U=4", 148, 1024)]
+for mode, name, blocks, threads in CASES:
+    if True:
         ts = []
         for r in range(4):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
