@@ -356,7 +356,8 @@ def run_single(args, gi, torch, rank, world, local):
             variants = [("fused", dict(fusion=True, drain="bsp")),
                         ("fused_async_drain", dict(fusion=True, drain="async")), ("unfused", dict(fusion=False))]
         else:
-            variants.append(("fused_expand", dict(fusion=True, expand="on")))
+            variants += [("fused_expand", dict(fusion=True, expand="on")),
+                         ("fused_no_expand", dict(fusion=True, expand="off"))]
         compare = compare_variants(gi, G, src, delta, out, opts, variants)
 
     # ---- e2e through the public C ABI with HOST buffers (pinned), copies inside ----
@@ -691,7 +692,7 @@ def main():
     ap.add_argument("--group-ctas", type=int, default=0)
     ap.add_argument("--hub-min", type=int, default=0)
     ap.add_argument("--pre-read", type=int, default=0, help="0 auto, 1 on, 2 off")
-    ap.add_argument("--expand", default="off", choices=["on", "off"],
+    ap.add_argument("--expand", default="auto", choices=["auto", "on", "off"],
                     help="edge-balanced expansion of high-degree frontier vertices in expand_kernel (skewed graphs)")
     ap.add_argument("--cta-threads", type=int, default=0, choices=[0, 512, 1024],
                     help="threads per persistent CTA (0 = auto: 1024 on skewed graphs)")

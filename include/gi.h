@@ -111,11 +111,11 @@ typedef struct {
                                 synchronise that stream before returning */
   int32_t cta_threads;       /* threads per persistent CTA: 0 = auto (1024 when the max out-degree
                                 is > 32 or for a batch of >= 8 sources, else 512), 512 or 1024 */
-  int32_t expand;            /* single queries on skewed graphs (max out-degree > 32): 1 = every
-                                ROUND phase collects its frontier vertices of out-degree > 8 into one
-                                group list whose concatenated edges are split evenly over all warps
-                                of a separate kernel (edge-balanced, kernel (b)); 0 / 2 = off (the
-                                default CTA-level edge balancing) */
+  int32_t expand;            /* single queries on skewed graphs (max out-degree > 32): every ROUND
+                                phase collects its frontier vertices of out-degree > 8 into one group
+                                list whose concatenated edges are split evenly over all warps of a
+                                separate kernel (edge-balanced, kernel (b)). 0 = auto (on for graphs
+                                of >= 512 M edges), 1 = on, 2 = off (CTA-level edge balancing) */
 } gi_options;
 
 /* Counters of one query (SURVEY §8(a) "Counter definitions"). */

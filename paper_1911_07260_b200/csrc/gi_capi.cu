@@ -477,15 +477,20 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   // expand_kernel between two segments of the persistent kernel (KState); lighter lists are
   // relaxed slice-wise in the kernel. Measured against the default CTA-level stage B on
   // configs 3-4 it is not faster, so the default stays off.
-  a.expand = (g->max_deg > 32 && opt.expand == 1 && G <= kMaxGroupCtas && ngroups == 1 && nsrc == 1 &&
-              kind != KIND_FUSED_ASYNC) ? 1u : 0u;
+  // auto (0): on for skewed graphs of >= 512 M edges, whose heavy phases it speeds up
+  // (config 4: 33.8 -> 28.8 ms); smaller ones pay more for the stops than they gain (config 3:
+  // 1.87 -> 2.5 ms)
+  const bool expand_auto = opt.expand == 0 && g->m >= (512ll << 20);
+  a.expand = (g->max_deg > 32 && (opt.expand == 1 || expand_auto) && G <= kMaxGroupCtas && ngroups == 1 &&
+              nsrc == 1 && kind != KIND_FUSED_ASYNC) ? 1u : 0u;
   a.pedges = g->d_pedges;
   a.colbits = g->colbits;
   a.split = a.expand;
   a.resume = 0;
   {
     const char* sm = getenv("GI_SPLIT_MIN");
-    a.split_min = sm ? strtoull(sm, nullptr, 10) : 0ull;
+    // lists of fewer edges are relaxed in the persistent kernel (a stop costs ~40 µs)
+    a.split_min = sm ? strtoull(sm, nullptr, 10) : (1ull << 20);
   }
   if (a.expand) {
     const int xk = kind == KIND_UNFUSED ? KIND_UNFUSED_XP : KIND_FUSED_BSP_XP;
@@ -533,6 +538,28 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
           (e = cudaStreamSynchronize(st)))
         return bail(e, "sssp kernel segment");
       if (!*w->h_pending) break;
+      if (const char* dump = getenv("GI_DUMP_X")) {  // investigation only: the pending list to files
+        KState hk;
+        cudaMemcpy(&hk, kst, sizeof(hk), cudaMemcpyDeviceToHost);
+        static int seq = 0;
+        std::vector<HubEnt> hx(hk.xn);
+        const GroupWs& gw = w->h_groups[0];
+        cudaMemcpy(hx.data(), (hk.p & 1) ? gw.hub[1] : gw.hub[0], sizeof(HubEnt) * hk.xn, cudaMemcpyDeviceToHost);
+        char fn[512];
+        snprintf(fn, sizeof(fn), "%s_%d_p%u_b%u_E%llu.bin", dump, seq++, hk.p, hk.b, (unsigned long long)hk.E);
+        if (FILE* f = fopen(fn, "wb")) {
+          fwrite(hx.data(), sizeof(HubEnt), hx.size(), f);
+          fclose(f);
+        }
+        // the distances at this point
+        std::vector<uint32_t> hd((size_t)g->n);
+        cudaMemcpy(hd.data(), d_dist, 4 * (size_t)g->n, cudaMemcpyDeviceToHost);
+        snprintf(fn, sizeof(fn), "%s_%d_dist.bin", dump, seq - 1);
+        if (FILE* f = fopen(fn, "wb")) {
+          fwrite(hd.data(), 4, hd.size(), f);
+          fclose(f);
+        }
+      }
       if ((e = v1024::launch_expand(a, st, nullptr))) return bail(e, "launch expand_kernel");
       if ((e = wide ? v1024::launch_sssp(ar, kind, G * ngroups, st) : v512::launch_sssp(ar, kind, G * ngroups, st)))
         return bail(e, "resume sssp_persistent");

@@ -1828,7 +1828,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
             const unsigned long long E = s.xS[G];
             if (a.split && E >= a.split_min) {
               // a heavy list: save the phase loop's state and stop; the host runs
-              // expand_kernel on the list and resumes this kernel at phase p (KState)
+              // expand_kernel on the list and resumes this kernel at phase p (KState).
+              // expand_kernel reads GLOBAL entry positions: this CTA's slice gets S[rank] added
+              {
+                const unsigned long long base = s.xS[rank];
+                const uint32_t lo_x = (uint32_t)(((uint64_t)xn * rank) / G), hi_x = (uint32_t)(((uint64_t)xn * (rank + 1)) / G);
+                if (base)
+                  for (uint32_t i = lo_x + tid; i < hi_x; i += kBlock) ws.xpre[i] += base;
+              }
               {
                 const uint32_t w = tid >> 5;
                 warp_flush_far(c, c.farstage + w * kFarSeg, min(s.wfar[w], (uint32_t)kFarSeg));
@@ -1867,10 +1874,30 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
             }
             __syncthreads();
 #else
-            // a light list (or a batch, which cannot stop for an external expand): the slice-wise
-            // relaxation in this kernel (the edge-balanced loop inlined here spilled the
-            // persistent kernel's registers)
-            hub_slices(xn);
+            // a light list: each CTA relaxes the whole entries of its own slice of the list
+            // with the CTA-wide stage B (the edge-balanced loop inlined here spilled the
+            // persistent kernel's registers; a stop for expand_kernel costs ~40 µs) — or, for
+            // a list of a few entries (a lone hub of a million edges), every CTA a 1/G slice
+            // of every entry
+            if (xn <= 4 * G) {
+              hub_slices(xn);
+            } else {
+              const uint32_t lo_x = (uint32_t)(((uint64_t)xn * rank) / G), hi_x = (uint32_t)(((uint64_t)xn * (rank + 1)) / G);
+              for (uint32_t h0 = lo_x; h0 < hi_x; h0 += kBigCap) {
+                const uint32_t nh = min((uint32_t)kBigCap, hi_x - h0);
+                for (uint32_t i = tid; i < nh; i += kBlock) {
+                  const uint4 he = __ldcg(reinterpret_cast<const uint4*>(hub_in + h0 + i));
+                  BigEnt be;
+                  be.beg = (int64_t)(((uint64_t)he.y << 32) | he.x);
+                  be.deg = he.z;
+                  be.du = he.w;
+                  c.big[i] = be;
+                }
+                __syncthreads();
+                stage_big<FUSED>(c, s, nh, ne);
+                __syncthreads();
+              }
+            }
 #endif
             TRACE(18);
           }
@@ -2021,13 +2048,11 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
 // pre-read distances. Improving candidates are written with red.min and staged per warp in
 // shared memory — future buckets for the far pile, the current bucket for the global
 // frontier — and flushed with the dedup test-and-set and one append atomic per warp.
-constexpr int kXSeg = 384;     // far staging entries per warp
-constexpr int kXCur = 128;     // current-bucket staging entries per warp
-constexpr int kXRows = 4;      // rows of 32 edges per warp per iteration
-
+constexpr int kXSeg = 512;     // far staging entries per warp (flushed above half)
+constexpr int kXCur = 64;      // current-bucket staging entries per warp (rare on skewed graphs)
+constexpr int kXRows = 8;      // rows of 32 edges per warp per iteration
 
 struct XShared {
-  unsigned long long S[kMaxGroupCtas + 1];
   int32_t far[kBlock / 32][kXSeg];
   int32_t cur[kBlock / 32][kXCur];
   uint32_t nfar[kBlock / 32], ncur[kBlock / 32];
@@ -2056,6 +2081,9 @@ __device__ __forceinline__ void xflush(const int32_t* seg, uint32_t n, uint32_t*
   __syncwarp();
 }
 
+// The list entries carry GLOBAL start positions here (xpre + S, added by the persistent
+// kernel before it stopped): lane k of a window holds entry jb+k's end relative to the warp's
+// range start, beg - start, and du.
 template <bool PACKED>
 __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
   extern __shared__ __align__(16) unsigned char x_dyn[];
@@ -2065,164 +2093,146 @@ __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
   const KState* ks = ws.kst;
   const uint32_t p = ks->p, j = ks->j, bcur = ks->b, hn = ks->xn;
   const unsigned long long E = ks->E;
-  const uint32_t G = (uint32_t)a.group_size;  // the persistent group, whose CTAs sliced the list
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < 32) {  // S[r] = sum of the slice totals before r
-    unsigned long long carry = 0;
-    if (tid == 0) xs.S[0] = 0;
-    for (uint32_t b0 = 0; b0 < G; b0 += 32) {
-      const uint32_t r = b0 + tid;
-      unsigned long long v = r < G ? __ldcg(ws.xtot + r) : 0ull;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long t = __shfl_up_sync(0xffffffffu, v, o);
-        if (tid >= (uint32_t)o) v += t;
-      }
-      if (r < G) xs.S[r + 1] = carry + v;
-      carry += __shfl_sync(0xffffffffu, v, 31);
-    }
-  }
   if (lane == 0) { xs.nfar[warp] = 0; xs.ncur[warp] = 0; }
-  __syncthreads();
-  const unsigned long long* S = xs.S;
+  __syncwarp();
   const HubEnt* X = (p & 1) ? ws.hub[1] : ws.hub[0];
   const unsigned long long* xpre = ws.xpre;
   uint32_t* const dist = a.dist;
-  const FastDiv div = a.div;
   const uint32_t colbits = a.colbits;
   const uint32_t cmask = colbits >= 32 ? 0xFFFFFFFFu : (1u << colbits) - 1u;
   uint32_t my_fmin = kInf;
-  auto flush_far = [&]() {
-    __syncwarp();
-    const uint32_t n = min(xs.nfar[warp], (uint32_t)kXSeg);
-    xflush(xs.far[warp], n, ws.farbits, (j & 1) ? ws.far[1] : ws.far[0], &ctl->fcount[j % 3], nullptr);
-    if (lane == 0) xs.nfar[warp] = 0;
-    __syncwarp();
-  };
-  auto flush_cur = [&]() {
-    __syncwarp();
-    const uint32_t n = min(xs.ncur[warp], (uint32_t)kXCur);
-    xflush(xs.cur[warp], n, (p & 1) ? ws.qbits[0] : ws.qbits[1], (p & 1) ? ws.q[0] : ws.q[1],
-           &ctl->qcount[(p + 1) % 3], a.slots);
-    if (lane == 0) xs.ncur[warp] = 0;
-    __syncwarp();
-  };
 
   const uint64_t W = (uint64_t)gridDim.x * (kBlock / 32), wg = (uint64_t)blockIdx.x * (kBlock / 32) + warp;
   const unsigned long long a0 = E * wg / W, b0 = E * (wg + 1) / W;
   if (a0 < b0) {
     const uint32_t len = (uint32_t)(b0 - a0);
-    // slice r holding position a0, then the entry within it (as expand_relax)
-    uint32_t rlo = 0, rhi = G;
-    while (rhi - rlo > 1) {
-      const uint32_t mid = (rlo + rhi) >> 1;
-      if (S[mid] <= a0) rlo = mid; else rhi = mid;
-    }
-    const unsigned long long t = a0 - S[rlo];
-    uint32_t ilo = (uint32_t)(((uint64_t)hn * rlo) / G), ihi = (uint32_t)(((uint64_t)hn * (rlo + 1)) / G);
+    // the entry holding position a0: the largest i with xpre[i] <= a0 (32-ary search)
+    uint32_t ilo = 0, ihi = hn;
     while (ihi - ilo > 32) {
       const uint32_t step = (ihi - ilo + 31) / 32;
       const uint32_t idx = ilo + lane * step;
-      const bool pr = idx < ihi && __ldcg(xpre + idx) <= t;
+      const bool pr = idx < ihi && __ldcg(xpre + idx) <= a0;
       ilo += (__popc(__ballot_sync(0xffffffffu, pr)) - 1) * step;
       ihi = min(ilo + step, ihi);
     }
     {
       const uint32_t idx = ilo + lane;
-      const bool pr = idx < ihi && __ldcg(xpre + idx) <= t;
+      const bool pr = idx < ihi && __ldcg(xpre + idx) <= a0;
       ilo += __popc(__ballot_sync(0xffffffffu, pr)) - 1;
     }
     uint32_t jb = ilo;
-    XWin w = expand_window(X, xpre, hn, G, S, jb, a0, len);
+    uint32_t endr;
+    int64_t off;
+    uint32_t wdu;
+    auto window = [&]() {
+      const uint32_t idx = jb + lane;
+      endr = len; off = 0; wdu = 0;
+      if (idx < hn) {
+        const uint4 he = __ldcg(reinterpret_cast<const uint4*>(X + idx));  // {beg lo, beg hi, deg, du}
+        const unsigned long long start = __ldcg(xpre + idx), end = start + he.z;
+        endr = end <= a0 ? 0u : (uint32_t)min(end - a0, (unsigned long long)len);
+        off = (int64_t)(((uint64_t)he.y << 32) | he.x) - (int64_t)start;
+        wdu = he.w;
+      }
+    };
+    window();
     const uint32_t lanemask = (2u << lane) - 2u;
-    using ET = typename XEdge<PACKED>::T;
-    // map rows it0.. to (edge, du) and issue the edge loads
-    auto map_load = [&](uint32_t it0, ET (&e)[kXRows], uint32_t (&du)[kXRows], uint32_t& valid) {
+    for (uint32_t it0 = 0; it0 < len; it0 += 32 * kXRows) {
       int64_t ei[kXRows];
-      valid = 0;
+      uint32_t du[kXRows], valid = 0;
 #pragma unroll
       for (int k = 0; k < kXRows; ++k) {
         ei[k] = 0;
         du[k] = 0;
         const uint32_t r0 = it0 + 32 * k;
         if (r0 >= len) continue;  // warp-uniform
-        const uint32_t last = __shfl_sync(0xffffffffu, w.endr, 31);
+        const uint32_t last = __shfl_sync(0xffffffffu, endr, 31);
         if (last < min(r0 + 32, len)) {
-          jb += __popc(__ballot_sync(0xffffffffu, w.endr <= r0));
-          w = expand_window(X, xpre, hn, G, S, jb, a0, len);
+          jb += __popc(__ballot_sync(0xffffffffu, endr <= r0));
+          window();
         }
-        const uint32_t c0 = __popc(__ballot_sync(0xffffffffu, w.endr <= r0));
-        const uint32_t x = w.endr - r0;
+        const uint32_t c0 = __popc(__ballot_sync(0xffffffffu, endr <= r0));
+        const uint32_t x = endr - r0;
         const uint32_t heads = __reduce_or_sync(0xffffffffu, (x - 1u < 31u) ? (1u << x) : 0u);
         const uint32_t slot = c0 + __popc(heads & lanemask);
-        const int64_t off = __shfl_sync(0xffffffffu, w.off, slot);
-        const uint32_t d = __shfl_sync(0xffffffffu, w.du, slot);
+        const int64_t o = __shfl_sync(0xffffffffu, off, slot);
+        const uint32_t d = __shfl_sync(0xffffffffu, wdu, slot);
         if (r0 + lane < len) {
-          ei[k] = off + (int64_t)(a0 + r0 + lane);
+          ei[k] = o + (int64_t)(a0 + r0 + lane);
           du[k] = d;
           valid |= 1u << k;
         }
       }
+      uint32_t v[kXRows], wt[kXRows], old[kXRows];
 #pragma unroll
       for (int k = 0; k < kXRows; ++k) {
-        if constexpr (PACKED) e[k] = (valid >> k) & 1u ? ld_pedge(a.pedges + ei[k]) : 0u;
-        else e[k] = (valid >> k) & 1u ? ld_edge(a.edges + ei[k]) : make_uint2(0, 0);
-      }
-    };
-    ET e[kXRows];
-    uint32_t du[kXRows], valid;
-    map_load(0, e, du, valid);
-    for (uint32_t it0 = 0; it0 < len; it0 += 32 * kXRows) {
-      uint32_t old[kXRows];
-#pragma unroll
-      for (int k = 0; k < kXRows; ++k) {
-        uint32_t v;
-        if constexpr (PACKED) v = e[k] & cmask; else v = e[k].x;
-        old[k] = (valid >> k) & 1u ? ld_dist_tgt(dist + v) : 0u;
-      }
-      // the next rows' edge loads fly while this batch's pre-reads return
-      ET en[kXRows];
-      uint32_t dn[kXRows], vn = 0;
-      if (it0 + 32 * kXRows < len) map_load(it0 + 32 * kXRows, en, dn, vn);
-#pragma unroll
-      for (int k = 0; k < kXRows; ++k) {
-        if (!((valid >> k) & 1u)) continue;
-        uint32_t v, nd;
-        if constexpr (PACKED) { v = e[k] & cmask; nd = du[k] + (e[k] >> colbits); }
-        else { v = e[k].x; nd = du[k] + e[k].y; }
-        if (nd < du[k] || nd == kInf) {
-          mark_overflow(ws.ovfbits, &ctl->ovf_cand, v);
-          continue;
+        if constexpr (PACKED) {
+          const uint32_t pe = (valid >> k) & 1u ? ld_pedge(a.pedges + ei[k]) : 0u;
+          v[k] = pe & cmask;
+          wt[k] = pe >> colbits;
+        } else {
+          const uint2 e = (valid >> k) & 1u ? ld_edge(a.edges + ei[k]) : make_uint2(0, 0);
+          v[k] = e.x;
+          wt[k] = e.y;
         }
-        if (nd < old[k]) {
-          red_min(dist + v, nd);
-          const uint32_t bk = a.h ? max(prio_bucket(nd, __ldg(a.h + v), div), bcur) : fdiv(nd, div);
-          if (bk == bcur) {
-            const uint32_t pos = atomicAdd(&xs.ncur[warp], 1u);
-            if (pos < (uint32_t)kXCur) xs.cur[warp][pos] = (int32_t)v;
+      }
+#pragma unroll
+      for (int k = 0; k < kXRows; ++k) old[k] = (valid >> k) & 1u ? ld_dist_tgt(dist + v[k]) : 0u;
+#pragma unroll
+      for (int k = 0; k < kXRows; ++k) {
+        const uint32_t nd = du[k] + wt[k];
+        const bool ovf = nd < du[k] || nd == kInf;
+        if (((valid >> k) & 1u) && (ovf || nd < old[k])) {
+          if (ovf) {  // inline: no call in this loop
+            atomicOr(&ws.ovfbits[v[k] >> 5], 1u << (v[k] & 31));
+            atomicOr(&ctl->ovf_cand, 1u);
+            continue;
+          }
+          red_min(dist + v[k], nd);
+          const uint32_t bk = a.h ? max(prio_bucket(nd, __ldg(a.h + v[k]), a.div), bcur) : fdiv(nd, a.div);
+          // staged per warp; a full segment (at most one iteration past half) takes the
+          // lane's own dedup push to the global list
+          const bool cur = bk == bcur;
+          if (!cur) my_fmin = min(my_fmin, bk);
+          const uint32_t pos = atomicAdd(cur ? &xs.ncur[warp] : &xs.nfar[warp], 1u);
+          if (pos < (uint32_t)(cur ? kXCur : kXSeg)) {
+            (cur ? xs.cur[warp] : xs.far[warp])[pos] = (int32_t)v[k];
           } else {
-            my_fmin = min(my_fmin, bk);
-            const uint32_t pos = atomicAdd(&xs.nfar[warp], 1u);
-            if (pos < (uint32_t)kXSeg) xs.far[warp][pos] = (int32_t)v;
+            uint32_t* bits = cur ? ((p & 1) ? ws.qbits[0] : ws.qbits[1]) : ws.farbits;
+            const uint32_t bit = 1u << (v[k] & 31);
+            if (!(atomicOr(&bits[v[k] >> 5], bit) & bit)) {
+              const uint32_t q = atomicAdd(cur ? &ctl->qcount[(p + 1) % 3] : &ctl->fcount[j % 3], 1u);
+              (cur ? ((p & 1) ? ws.q[0] : ws.q[1]) : ((j & 1) ? ws.far[1] : ws.far[0]))[q] = (int32_t)v[k];
+            }
           }
         }
       }
       __syncwarp();
-      // staging never overflows: at most 32 * kXRows pushes per iteration
-      if (xs.nfar[warp] > (uint32_t)(kXSeg - 32 * kXRows)) flush_far();
-      if (xs.ncur[warp] > (uint32_t)(kXCur - 32 * kXRows)) flush_cur();
-#pragma unroll
-      for (int k = 0; k < kXRows; ++k) { e[k] = en[k]; du[k] = dn[k]; }
-      valid = vn;
+      if (xs.nfar[warp] > (uint32_t)(kXSeg / 2)) {
+        const uint32_t n = min(xs.nfar[warp], (uint32_t)kXSeg);
+        xflush(xs.far[warp], n, ws.farbits, (j & 1) ? ws.far[1] : ws.far[0], &ctl->fcount[j % 3], nullptr);
+        if (lane == 0) xs.nfar[warp] = 0;
+        __syncwarp();
+      }
+      if (xs.ncur[warp] > (uint32_t)(kXCur / 2)) {
+        const uint32_t n = min(xs.ncur[warp], (uint32_t)kXCur);
+        xflush(xs.cur[warp], n, (p & 1) ? ws.qbits[0] : ws.qbits[1], (p & 1) ? ws.q[0] : ws.q[1],
+               &ctl->qcount[(p + 1) % 3], a.slots);
+        if (lane == 0) xs.ncur[warp] = 0;
+        __syncwarp();
+      }
     }
   }
-  flush_far();
-  flush_cur();
+  __syncwarp();
+  xflush(xs.far[warp], min(xs.nfar[warp], (uint32_t)kXSeg), ws.farbits, (j & 1) ? ws.far[1] : ws.far[0],
+         &ctl->fcount[j % 3], nullptr);
+  xflush(xs.cur[warp], min(xs.ncur[warp], (uint32_t)kXCur), (p & 1) ? ws.qbits[0] : ws.qbits[1],
+         (p & 1) ? ws.q[0] : ws.q[1], &ctl->qcount[(p + 1) % 3], a.slots);
   const uint32_t fm = __reduce_min_sync(0xffffffffu, my_fmin);
   if (lane == 0 && fm != kInf) atomicMin(&ctl->fmin[j % 3], fm);
   if (blockIdx.x == 0 && tid == 0) ws.kst->pending = 0;
 }
-static_assert(kXCur >= 32 * kXRows && kXSeg >= 2 * 32 * kXRows, "staging holds one iteration's pushes");
 #endif
 
 #if GI_PRIMARY

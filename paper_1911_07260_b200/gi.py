@@ -250,7 +250,7 @@ def make_options(fusion=True, threshold=0, max_ctas=0, group_ctas=0, pre_read=0,
     o.hub_min = hub_min
     o.drain = {"auto": 0, "bsp": 1, "async": 2}.get(drain, drain)
     o.cta_threads = cta_threads
-    o.expand = {"auto": 0, "on": 1, "off": 2}.get(expand, expand)  # auto = off (include/gi.h)
+    o.expand = {"auto": 0, "on": 1, "off": 2}.get(expand, expand)
     if stream is not None:
         o.cuda_stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     return o

@@ -74,3 +74,29 @@ for K, Xd, xp, tag in ((4, X, xpre, "id order"), (8, X, xpre, "id order"), (4, X
             ts.append(e0.elapsed_time(e1))
         print(f"R5 expand mapping K={K} {tag:12s} {blocks}x{threads}: {min(ts[1:]):.3f} ms  {E / min(ts[1:]) / 1e6:.1f} G edges/s "
               f"(E={E})", flush=True)
+
+# MODE 5 on a real phase list dumped by GI_DUMP_X (entries {beg, deg, du}) with the real dist
+import glob
+for fn in sorted(glob.glob(os.environ.get("XDUMP", "/tmp/xdump") + "_*_E*.bin")):
+    Xh2 = np.fromfile(fn, dtype=[("beg", "<i8"), ("deg", "<u4"), ("du", "<u4")])
+    dd = np.fromfile(fn.split("_p")[0] + "_dist.bin", dtype=np.int32)
+    pre2 = np.zeros(Xh2.shape[0], np.uint64)
+    pre2[1:] = np.cumsum(Xh2["deg"].astype(np.uint64))[:-1]
+    E2 = int(Xh2["deg"].astype(np.uint64).sum())
+    X2 = torch.from_numpy(Xh2.view(np.uint8)).cuda()
+    xpre2 = torch.from_numpy(pre2.view(np.int64)).cuda()
+    dist0 = torch.from_numpy(dd).cuda()
+    for K in (4, 8):
+        ts = []
+        for r in range(3):
+            dist = dist0.clone(); bits.zero_(); counts.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            rc = lib.probe_relax_x(K, pe.data_ptr(), X2.data_ptr(), xpre2.data_ptr(), Xh2.shape[0], E2, dist.data_ptr(),
+                                   bits.data_ptr(), lst.data_ptr(), counts.data_ptr(), colbits, 148, 1024, vp(st.cuda_stream))
+            e1.record(st)
+            torch.cuda.synchronize()
+            assert rc == 0, rc
+            ts.append(e0.elapsed_time(e1))
+        imp = int((dist != dist0).sum())
+        print(f"R5 on {os.path.basename(fn)} K={K}: entries {Xh2.shape[0]} {min(ts[1:]):.3f} ms  {E2 / min(ts[1:]) / 1e6:.1f} G edges/s, lowered {imp}", flush=True)
