@@ -261,6 +261,7 @@ def counters_of(s):
 
 
 def compare_variants(gi, G, src, delta, out, opts, variants):
+    """Counters and device time of option variants (same Δ), 3 runs each (median time)."""
     res = {}
     for name, ov in variants:
         o2 = dict(opts)
@@ -286,9 +287,12 @@ def secondary_cfg2(gi, torch, local, stream, floors, opts):
     n_r, m_r = reached_stats(g, d)
     peak, _ = measured_peak()
     ba = b_alg(g, n_r, m_r)
+    # the GPU analogue of table:eager_lazy_perf_impact and table:fusion_perf_impact (PAPER.md
+    # :1105-1138): eager + fusion (default), eager without fusion, fully lazy
     comp = compare_variants(gi, G, src, delta, out, o, [("fused", dict(drain="bsp")),
                                                         ("fused_async_drain", dict(drain="async")),
-                                                        ("unfused", dict(fusion=False))])
+                                                        ("unfused", dict(fusion=False)),
+                                                        ("lazy", dict(fusion=False, lazy=True))])
     res = {"workload": WORKLOAD[2], "delta": delta, "ms_per_step": ms, "kernel_ms": kms,
            "value": g.m / (ms * 1e-3) / 1e9, "unit": UNIT,
            "roofline": {"bound": "hbm", "achieved": ba / (kms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
@@ -342,11 +346,17 @@ def run_single(args, gi, torch, rank, world, local):
     peak, peak_src = measured_peak()
     achieved = bytes_alg / (kms * 1e-3) / 1e9
     traffic = load_traffic(cfg, delta)
+    launches = stats[-1].kernel_launches
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "sssp_persistent", "kernel_ms": kms,
+                "traffic": traffic,
+                "kernel": "sssp_persistent" if launches == 1 else
+                          f"sssp_persistent segments + expand_kernel ({launches} launches per query)",
+                "kernel_ms": kms,
                 "bytes_alg_per_launch": bytes_alg, "peak_source": peak_src,
                 "bytes_alg_formula": "12*m_r + 16*n_r + 4*n (SURVEY §8(d))",
-                "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes_read.sum + dram__bytes_write.sum)"}
+                "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes_read.sum + dram__bytes_write.sum of the "
+                                  "query's launches)",
+                "note": "achieved = algorithmic bytes / the query's device time (CUDA events around every launch)"}
     s_last = stats[-1]
 
     compare = None
@@ -355,6 +365,7 @@ def run_single(args, gi, torch, rank, world, local):
         if int(np.diff(g.offsets).max(initial=0)) <= 8:  # both drains run on low-degree graphs
             variants = [("fused", dict(fusion=True, drain="bsp")),
                         ("fused_async_drain", dict(fusion=True, drain="async")), ("unfused", dict(fusion=False))]
+        variants.append(("lazy", dict(fusion=False, lazy=True)))
         else:
             variants += [("fused_expand", dict(fusion=True, expand="on")),
                          ("fused_no_expand", dict(fusion=True, expand="off"))]

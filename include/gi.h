@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GI_VERSION 100 /* 1.0.0 */
+#define GI_VERSION 200 /* 2.0.0: gi_options.expand / lazy, gi_probe_floors */
 
 typedef struct gi_graph gi_graph; /* opaque; owns device copies of the CSR */
 
@@ -116,6 +116,14 @@ typedef struct {
                                 list whose concatenated edges are split evenly over all warps of a
                                 separate kernel (edge-balanced, kernel (b)). 0 = auto (on for graphs
                                 of >= 512 M edges), 1 = on, 2 = off (CTA-level edge balancing) */
+  int32_t lazy;              /* 1: the fully lazy schedule of Fig. alg:lazy_delta_stepping
+                                (PAPER.md:409-434): every distance lowering, into the current bucket
+                                too, is appended to the bucket-update buffer (the far pile, one
+                                entry per vertex = reduceBucketUpdates) and the next round's frontier
+                                is the minimum bucket extracted from it (bulkUpdateBuckets +
+                                getMinBucket) — one group barrier and one pile scan per round.
+                                Requires fusion = 0 (GI_ERR_INVALID_ARGUMENT otherwise). 0 = the
+                                eager current bucket (default) */
 } gi_options;
 
 /* Counters of one query (SURVEY §8(a) "Counter definitions"). */

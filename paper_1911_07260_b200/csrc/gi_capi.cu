@@ -320,6 +320,8 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   const bool fused = opt.fusion != 0;
   if (opt.drain > 2) return fail(GI_ERR_INVALID_ARGUMENT, "drain must be 0 (auto), 1 (bsp) or 2 (async)");
   if (opt.expand < 0 || opt.expand > 2) return fail(GI_ERR_INVALID_ARGUMENT, "expand must be 0 (auto), 1 (on) or 2 (off)");
+  if (opt.lazy != 0 && opt.lazy != 1) return fail(GI_ERR_INVALID_ARGUMENT, "lazy must be 0 or 1");
+  if (opt.lazy && opt.fusion) return fail(GI_ERR_INVALID_ARGUMENT, "the lazy schedule runs without fusion (fusion = 0)");
   if (heur && fused && opt.drain == 2) return fail(GI_ERR_UNSUPPORTED, "A* runs with the bsp drain (drain 0/1)");
   if (fused && opt.drain == 2 && g->max_deg > kAsyncMaxDeg)
     return fail(GI_ERR_UNSUPPORTED, "async drain needs max out-degree <= %u (graph has %u)", kAsyncMaxDeg,
@@ -486,6 +488,7 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   a.pedges = g->d_pedges;
   a.colbits = g->colbits;
   a.split = a.expand;
+  a.lazy = opt.lazy ? 1u : 0u;
   a.resume = 0;
   {
     const char* sm = getenv("GI_SPLIT_MIN");

@@ -124,6 +124,7 @@ struct GroupWs {
 // of its own, 2 CTAs per SM) and then resumes the persistent kernel at the same phase.
 struct KState {
   uint32_t p, j, b, prev;       // phase loop position
+  uint32_t last_b;              // bucket of the last counted extraction
   unsigned long long phases, rounds, buckets, empty, critical;  // group counters (rank 0)
   unsigned long long E;         // edges of the pending list
   uint32_t xn;                  // entries of the pending list
@@ -171,6 +172,8 @@ struct KArgs {
   uint32_t expand;
   const uint32_t* pedges;  // [m] packed edges (w << colbits | col) or nullptr (use `edges`)
   uint32_t colbits;        // packed: bits of the column id
+  uint32_t lazy;           // fully lazy schedule (unfused kernels): every lowering, the current
+                           // bucket's included, goes through the far pile
   uint32_t split;          // single query: heavy expands run in expand_kernel (see KState)
   uint32_t resume;         // this launch resumes a query stopped for an external expand
   unsigned long long split_min;  // list edges from which a phase's expand runs outside

@@ -307,6 +307,7 @@ struct Ctx {
   Shared* s;
   uint32_t my_fmin;        // thread-local min far bucket (reduced at phase end)
   bool pre_read;
+  bool lazy;               // fully lazy schedule: no eager current-bucket pushes
 };
 
 // Append v to the global frontier once per phase (dedup bit), warp-aggregated.
@@ -481,7 +482,7 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     if ((ok & (1u << k)) && nd[k] < old[k]) {
-      if (bk[k] == c.b) curm |= 1u << k;
+      if (bk[k] == c.b && !c.lazy) curm |= 1u << k;
       else farm |= 1u << k;  // bk > b
     }
   }
@@ -903,7 +904,7 @@ template <bool FUSED>
 __device__ __forceinline__ void expand_push(Ctx& c, uint32_t v, uint32_t nd) {
   red_min(c.dist + v, nd);
   const uint32_t bk = c.h ? max(prio_bucket(nd, __ldg(c.h + v), c.div), c.b) : fdiv(nd, c.div);
-  if (bk == c.b) {
+  if (bk == c.b && !c.lazy) {
     if constexpr (FUSED) {
       const uint32_t pos = atomicAdd(c.outcnt, 1u);
       if (pos < (uint32_t)kBinCap) {
@@ -1476,6 +1477,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
     c.pre = reinterpret_cast<unsigned long long*>(c.big + kBigCap);
     c.s = &s;
     c.pre_read = a.pre_read != 0;
+    c.lazy = !FUSED && a.lazy != 0;
     c.hub_min = a.hub_min;
     c.h = a.h;
 
@@ -1494,10 +1496,11 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
     unsigned long long phases = 0, rounds = 0, buckets = 0, empty = 0, critical = 0;  // rank 0, thread 0
     unsigned long long sub_at_phase_start = 0;
     uint32_t p = 0, j = 0, b = 0, prev = MODE_NONE;
+    uint32_t last_b = kInf;  // bucket of the last extraction with live vertices (rank 0, thread 0)
     bool mid = false;  // resuming inside ROUND phase p, after its external expand
     if (resuming) {
       const KState* ks = ws.kst;
-      p = ks->p; j = ks->j; b = ks->b; prev = ks->prev;
+      p = ks->p; j = ks->j; b = ks->b; prev = ks->prev; last_b = ks->last_b;
       if (rank == 0 && tid == 0) {
         phases = ks->phases; rounds = ks->rounds; buckets = ks->buckets; empty = ks->empty; critical = ks->critical;
       }
@@ -1521,7 +1524,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
         const uint32_t fm = __ldcg(&ctl->fmin[j % 3]);
         if (p > 0 && rank == 0) critical += __ldcg(&ctl->maxsub[(p - 1) % 3]);
         if (prev == MODE_EXTRACT) {
-          if (xl) { ++buckets; if (FUSED) ++rounds; } else { ++empty; }
+          // a lazy schedule extracts a bucket once per round: it counts once
+          if (xl) { if (b != last_b) ++buckets; last_b = b; if (FUSED) ++rounds; } else { ++empty; }
         }
         uint32_t mode;
         s.hn = min(hn, a.hubcap);
@@ -1855,7 +1859,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
                 if (scanned) atomicAdd(&q->far_scanned, scanned);
                 if (rank == 0) {
                   KState* ks = ws.kst;
-                  ks->p = p; ks->j = j; ks->b = b; ks->prev = prev;
+                  ks->p = p; ks->j = j; ks->b = b; ks->prev = prev; ks->last_b = last_b;
                   ks->phases = phases; ks->rounds = rounds; ks->buckets = buckets; ks->empty = empty;
                   ks->critical = critical; ks->E = E; ks->xn = xn;
                   __threadfence();
@@ -2193,7 +2197,7 @@ __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
           const uint32_t bk = a.h ? max(prio_bucket(nd, __ldg(a.h + v[k]), a.div), bcur) : fdiv(nd, a.div);
           // staged per warp; a full segment (at most one iteration past half) takes the
           // lane's own dedup push to the global list
-          const bool cur = bk == bcur;
+          const bool cur = bk == bcur && !a.lazy;
           if (!cur) my_fmin = min(my_fmin, bk);
           const uint32_t pos = atomicAdd(cur ? &xs.ncur[warp] : &xs.nfar[warp], 1u);
           if (pos < (uint32_t)(cur ? kXCur : kXSeg)) {

@@ -50,7 +50,7 @@ def test_sm100a_code_only(gi):
 
 
 def test_version_status_strings_and_struct_layout(gi):
-    assert gi.version() == 100
+    assert gi.version() == 200
     lib = gi.lib()
     for code, name in gi.STATUS.items():
         assert lib.gi_status_string(code).decode() == name

@@ -131,6 +131,47 @@ def test_path_closed_form_rounds(gi):
         assert st["spills"] == 0
 
 
+def test_lazy_schedule(gi, config_graph):
+    """The fully lazy schedule (gi_options.lazy, Fig. alg:lazy_delta_stepping):
+    exact distances; path closed form (rounds = n, buckets = ⌈n/Δ⌉, the round counts of the
+    oracle's step-by-step transcription); Δ <= w_min gives one round per bucket; a skewed graph
+    and a road grid; lazy with fusion is an argument error."""
+    for n, delta in ((1000, 100), (257, 1)):
+        g = gen.path(n)
+        G = gi.Graph.from_csr(g)
+        d, st = run(gi, G, 0, delta, fusion=False, lazy=True)
+        lz = oracle.delta_stepping_lazy(g, 0, delta)
+        assert d.tolist() == list(range(n))
+        assert st["rounds"] == n == lz["rounds"] and st["buckets"] == -(-n // delta) == lz["buckets"], st
+    g = gen.grid(48, 48, 3, 40, 5)  # w >= 3
+    G = gi.Graph.from_csr(g)
+    ref, _ = oracle.dijkstra(g, 0)
+    for delta in (1, 3):
+        d, st = run(gi, G, 0, delta, fusion=False, lazy=True)
+        assert np.array_equal(d, ref)
+        assert st["rounds"] == st["buckets"] == oracle.bucket_count(ref, delta), st
+    rng = np.random.default_rng(17)
+    for t in range(8):
+        n = int(rng.integers(50, 4000))
+        m = int(rng.integers(n, 8 * n))
+        g = gen.uniform_random(n, m, 0 if t % 2 else 1, int(rng.choice([5, 1000])), 40 + t)
+        G = gi.Graph.from_csr(g)
+        s = int(rng.integers(0, n))
+        ref, _ = oracle.dijkstra(g, s)
+        for delta in (1, 7, 1 << 20):
+            for o in (dict(), dict(max_ctas=3), dict(pre_read=1)):
+                d, st = run(gi, G, s, delta, fusion=False, lazy=True, **o)
+                assert np.array_equal(d, ref), (t, delta, o)
+                assert st["buckets"] == oracle.bucket_count(ref, delta) and st["rounds"] >= st["buckets"]
+    g = config_graph(1)
+    G = gi.Graph.from_csr(g)
+    ref, _ = oracle.dijkstra(g, 0)
+    d, st = run(gi, G, 0, 1000, fusion=False, lazy=True)
+    assert np.array_equal(d, ref) and st["buckets"] == oracle.bucket_count(ref, 1000)
+    with pytest.raises(gi.GiError):
+        run(gi, G, 0, 1000, fusion=True, lazy=True)
+
+
 def test_delta_le_wmin_processes_each_vertex_once(gi):
     """Δ <= w_min: every reached vertex is processed exactly once."""
     g = gen.grid(64, 64, 3, 4, 0)
@@ -214,6 +255,69 @@ def test_config5_batch(gi, config_graph):
     assert np.array_equal(got, refs)
     for i in range(64):
         assert st[i]["buckets"] > 0
+
+
+@pytest.mark.slow
+def test_config5_batch_peers_two_ranks(gi, config_graph):
+    """The multi-GPU product path at full size (config 5: 64 sources on the 4096^2 road grid),
+    two 'ranks' in one process: each computes its contiguous block of 32 sources with
+    gi_sssp_batch_peers into its own [64, n] matrix and the kernel writes every finished row
+    into the other rank's matrix. Both matrices must equal the oracle on every row."""
+    import torch
+    from paper_1911_07260_b200.dist import peer_row_addresses, shard_bounds
+    g = config_graph(5)
+    G = gi.Graph.from_csr(g)
+    srcs = gen.config_sources(5, g).astype(np.int32)
+    mats = [torch.full((64, g.n), 7, dtype=torch.int32, device="cuda") for _ in range(2)]
+    bases = [m.data_ptr() for m in mats]
+    for r in range(2):
+        lo, hi = shard_bounds(64, r, 2)
+        gi.gi_sssp_batch_peers(G, srcs[lo:hi], 1 << 13, peer_row_addresses(bases, lo, g.n), r)
+    torch.cuda.synchronize()
+    refs, _, _ = oracle.dijkstra_many(g, srcs)
+    for m in mats:
+        assert np.array_equal(gi.as_uint32(m), refs)
+
+
+@pytest.mark.slow
+def test_stress_repeated_full_size(gi, config_graph):
+    """Race stress at full size (compute-sanitizer is closed on this pool): 20 runs each of
+    config 3 at Δ=8 (skewed; pre-read / red.min protocol, R11; the late staleness gate, R12)
+    and config 2 with the async drain (ring protocol, R10), with random CTA counts,
+    thresholds and pre-read settings, every run compared with the oracle element by element."""
+    rng = np.random.default_rng(2024)
+    for cfg, delta, base in ((3, 8, dict()), (2, 1 << 14, dict(drain="async"))):
+        g = config_graph(cfg)
+        G = gi.Graph.from_csr(g)
+        src = gen.config_source(cfg, g)
+        ref, _ = oracle.dijkstra(g, src)
+        for it in range(20):
+            o = dict(base)
+            o["max_ctas"] = int(rng.choice([0, 0, 1, 7, 64, 147]))
+            o["threshold"] = int(rng.choice([0, 1, 16, 256, 1000]))
+            if cfg == 3:
+                o["pre_read"] = int(rng.choice([0, 1, 2]))
+                o["expand"] = str(rng.choice(["auto", "on", "off"]))
+            d, st = run(gi, G, src, delta, **o)
+            assert np.array_equal(d, ref), (cfg, it, o)
+            assert st["buckets"] == oracle.bucket_count(ref, delta), (cfg, it, o)
+
+
+@pytest.mark.slow
+def test_ppsp_astar_config2(gi, config_graph):
+    """PPSP and A* at full size on the road grid (config 2): δ(s, t) equal to the oracle's
+    dist[t] for the centre source and seeded targets, and never more buckets than SSSP."""
+    g = config_graph(2)
+    G = gi.Graph.from_csr(g)
+    src = gen.config_source(2, g)
+    ref, _ = oracle.dijkstra(g, src)
+    full = run(gi, G, src, 1 << 16)[1]
+    for t in [int(x) for x in gen.sources(g.n, 6, 7)] + [src]:
+        d, st = gi.ppsp(G, src, t, 1 << 16)
+        assert d == int(ref[t]), t
+        assert st["buckets"] <= full["buckets"]
+        h = gen.grid_heuristic(4096, 4096, t, int(g.w.min()))
+        assert gi.astar(G, src, t, 1 << 16, h)[0] == int(ref[t]), t
 
 
 def test_async_drain_low_degree_random(gi):
