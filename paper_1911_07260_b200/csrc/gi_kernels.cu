@@ -63,6 +63,7 @@ enum : uint32_t { MODE_ROUND = 0, MODE_EXTRACT = 1, MODE_DONE = 2, MODE_NONE = 3
 constexpr int kXtr = GI_XTR;  // far-pile entries per thread per extraction chunk
 constexpr int kFarSeg = kFarStage / (kBlock / 32);  // bsp: far staging entries per warp
 static_assert(kFarSeg >= 32 * 8, "a warp's far segment must hold one relax batch (32 lanes x 8 edges)");
+static_assert(kFarSeg <= 1024, "warp_flush_far tracks up to 32 entries per lane");
 // A/B switches for measurements only (tools/ab_time.py); all 0 in the product build
 #ifndef GI_X_NOPF
 #define GI_X_NOPF 0
@@ -369,6 +370,47 @@ __device__ __forceinline__ void warp_append(uint32_t m, const int32_t (&v)[X], i
     }
 }
 
+// CTA-aggregated append of the entries v[x] with bit x of `m` set (per lane): a warp scan,
+// a scan of the warp totals, ONE global atomic per CTA call. Every thread of the CTA must
+// call it (two CTA barriers). Used where a whole grid appends to one counter at a high rate
+// (a big extraction: one atomic per warp per chunk on the same word serialised at ~150 M/s).
+template <int X>
+__device__ __forceinline__ void cta_append(uint32_t m, const int32_t (&v)[X], int32_t* list, uint32_t* count,
+                                           uint32_t* wslot, const uint2* slots_pf) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t nk = __popc(m);
+  uint32_t incl = nk;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += t;
+  }
+  if (lane == 31) wslot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = lane < kBlock / 32 ? wslot[lane] : 0u;
+    uint32_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= (uint32_t)o) wi += t;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, wi, kBlock / 32 - 1);
+    uint32_t base = 0;
+    if (lane == 0 && tot) base = atomicAdd(count, tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (lane < kBlock / 32) wslot[lane] = base + wi - w;
+  }
+  __syncthreads();
+  uint32_t off = wslot[warp] + incl - nk;
+#pragma unroll
+  for (int x = 0; x < X; ++x)
+    if (m & (1u << x)) {
+      if (slots_pf) prefetch_l2(slots_pf + 8 * (size_t)v[x]);
+      list[off++] = v[x];
+    }
+}
+
 // Dedup-append of n staged vertices to a global list: the bit test-and-set (atomicOr)
 // of 4 entries per thread is in flight at once, and the list positions come from one
 // global atomic per WARP per 128 entries (warp scan) — no CTA barrier, so that a small
@@ -399,22 +441,42 @@ __device__ __forceinline__ void bulk_append(uint32_t n, Get get, uint32_t* bits,
 // entries (atomicOr of 4 per lane in flight, one append atomic per 128 entries). Only this
 // warp touches its segment, so no CTA barrier is needed mid-phase.
 __device__ __forceinline__ void warp_flush_far(Ctx& c, const int32_t* seg, uint32_t n) {
+  // the segment's test-and-sets first (4 per lane in flight per round), then one warp scan
+  // and ONE append atomic (every warp of the grid appends to the same counter)
   const uint32_t lane = threadIdx.x & 31;
-  for (uint32_t base = 0; base < n; base += 4 * 32) {
+  uint32_t newm = 0;  // bit r*4+x: entry (r*128 + x*32 + lane) is new
+  for (uint32_t r = 0; r * 128 < n; ++r) {
     int32_t v[4];
     uint32_t old[4];
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
-      const uint32_t i = base + x * 32 + lane;
+      const uint32_t i = r * 128 + x * 32 + lane;
       v[x] = i < n ? seg[i] : -1;
     }
 #pragma unroll
     for (int x = 0; x < 4; ++x) old[x] = v[x] >= 0 ? atomicOr(&c.farbits[v[x] >> 5], 1u << (v[x] & 31)) : ~0u;
-    uint32_t newm = 0;
 #pragma unroll
     for (int x = 0; x < 4; ++x)
-      if (v[x] >= 0 && !(old[x] & (1u << (v[x] & 31)))) newm |= 1u << x;
-    warp_append(newm, v, c.far_live, c.fcount_live, nullptr);
+      if (v[x] >= 0 && !(old[x] & (1u << (v[x] & 31)))) newm |= 1u << (r * 4 + x);
+  }
+  const uint32_t nk = __popc(newm);
+  uint32_t incl = nk;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += t;
+  }
+  const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+  if (tot) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(c.fcount_live, tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    uint32_t off = base + incl - nk;
+    while (newm) {
+      const int b = __ffs(newm) - 1;
+      newm &= newm - 1;
+      c.far_live[off++] = seg[(b >> 2) * 128 + (b & 3) * 32 + lane];
+    }
   }
   __syncwarp();
 }
@@ -1637,6 +1699,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
         // per chunk (warp scan), not one per warp per entry.
         const int32_t* far_src = (j & 1) ? ws.far[0] : ws.far[1];
         uint32_t nlive = 0;
+        // a big pile (every CTA iterates many chunks): CTA-aggregated appends (cta_append)
+        const bool agg = cnt >= 2u * G * kXtr * kBlock;
         for (uint32_t base = lo; base < hi; base += kXtr * kBlock) {
           int32_t v[kXtr];
           uint32_t d[kXtr];
@@ -1661,7 +1725,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
               keepm |= 1u << x;
             }
           }
-          warp_append(keepm, v, c.far_live, c.fcount_live, nullptr);
+          if (agg) cta_append(keepm, v, c.far_live, c.fcount_live, s.redw, nullptr);
+          else warp_append(keepm, v, c.far_live, c.fcount_live, nullptr);
           // the extracted vertices: the CTA bin (fusion) while it has room, else — and
           // without fusion — the global frontier, deduplicated with all atomics in flight
           uint32_t ovm = FUSED ? 0u : livem;
@@ -1685,7 +1750,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
               }
             }
           }
-          if (__any_sync(0xffffffffu, ovm != 0)) {
+          if (agg || __any_sync(0xffffffffu, ovm != 0)) {  // agg: CTA-uniform
             uint32_t old[kXtr];
 #pragma unroll
             for (int x = 0; x < kXtr; ++x)
@@ -1694,7 +1759,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
 #pragma unroll
             for (int x = 0; x < kXtr; ++x)
               if (((ovm >> x) & 1u) && !(old[x] & (1u << (v[x] & 31)))) newm |= 1u << x;
-            warp_append(newm, v, c.q_next, c.qcount_next, c.slots);
+            if (agg) cta_append(newm, v, c.q_next, c.qcount_next, s.redw, c.slots);
+            else warp_append(newm, v, c.q_next, c.qcount_next, c.slots);
           }
         }
         TRACE(6);
@@ -2062,25 +2128,48 @@ struct XShared {
   uint32_t nfar[kBlock / 32], ncur[kBlock / 32];
 };
 
-// dedup-append of a warp's staged vertices (bits = dedup bitmap) to a global list
+// dedup-append of a warp's staged vertices (bits = dedup bitmap) to a global list: the
+// test-and-sets of the whole segment first (4 per lane in flight per round), then ONE warp
+// scan and ONE append atomic for the segment — every warp of the GPU appends to the same
+// counter, which serialises same-word atomics (~150 M/s)
 __device__ __forceinline__ void xflush(const int32_t* seg, uint32_t n, uint32_t* bits, int32_t* list,
                                        uint32_t* count, const uint2* slots_pf) {
   const uint32_t lane = threadIdx.x & 31;
-  for (uint32_t base = 0; base < n; base += 4 * 32) {
+  uint32_t newm = 0;  // bit r*4+x: entry (r*128 + x*32 + lane) is new (n <= 1024)
+  for (uint32_t r = 0; r * 128 < n; ++r) {
     int32_t v[4];
     uint32_t old[4];
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
-      const uint32_t i = base + x * 32 + lane;
+      const uint32_t i = r * 128 + x * 32 + lane;
       v[x] = i < n ? seg[i] : -1;
     }
 #pragma unroll
     for (int x = 0; x < 4; ++x) old[x] = v[x] >= 0 ? atomicOr(&bits[v[x] >> 5], 1u << (v[x] & 31)) : ~0u;
-    uint32_t newm = 0;
 #pragma unroll
     for (int x = 0; x < 4; ++x)
-      if (v[x] >= 0 && !(old[x] & (1u << (v[x] & 31)))) newm |= 1u << x;
-    warp_append(newm, v, list, count, slots_pf);
+      if (v[x] >= 0 && !(old[x] & (1u << (v[x] & 31)))) newm |= 1u << (r * 4 + x);
+  }
+  const uint32_t nk = __popc(newm);
+  uint32_t incl = nk;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += t;
+  }
+  const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+  if (tot) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(count, tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    uint32_t off = base + incl - nk;
+    while (newm) {
+      const int b = __ffs(newm) - 1;
+      newm &= newm - 1;
+      const int32_t v = seg[(b >> 2) * 128 + (b & 3) * 32 + lane];
+      if (slots_pf) prefetch_l2(slots_pf + 8 * (size_t)v);
+      list[off++] = v;
+    }
   }
   __syncwarp();
 }
