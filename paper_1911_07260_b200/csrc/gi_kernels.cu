@@ -2122,10 +2122,28 @@ constexpr int kXSeg = 512;     // far staging entries per warp (flushed above ha
 constexpr int kXCur = 64;      // current-bucket staging entries per warp (rare on skewed graphs)
 constexpr int kXRows = 8;      // rows of 32 edges per warp per iteration
 
+// the pointers of expand_kernel's cold paths (pushes, flushes, overflow), read from shared
+// memory where used so that the edge loop keeps only its own values in registers
+struct XPtrs {
+  uint32_t* farbits;
+  int32_t* far_live;
+  uint32_t* fcount;
+  uint32_t* qbits;
+  int32_t* q;
+  uint32_t* qcount;
+  uint32_t* ovfbits;
+  uint32_t* ovf_cand;
+  const uint2* slots;
+  const uint32_t* h;
+  FastDiv div;
+  uint32_t bcur;
+};
+
 struct XShared {
   int32_t far[kBlock / 32][kXSeg];
   int32_t cur[kBlock / 32][kXCur];
   uint32_t nfar[kBlock / 32], ncur[kBlock / 32];
+  XPtrs ps;
 };
 
 // dedup-append of a warp's staged vertices (bits = dedup bitmap) to a global list: the
@@ -2181,20 +2199,51 @@ template <bool PACKED>
 __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
   extern __shared__ __align__(16) unsigned char x_dyn[];
   XShared& xs = *reinterpret_cast<XShared*>(x_dyn);
-  const GroupWs ws = a.groups[0];
-  Ctl* ctl = ws.ctl;
-  const KState* ks = ws.kst;
-  const uint32_t p = ks->p, j = ks->j, bcur = ks->b, hn = ks->xn;
-  const unsigned long long E = ks->E;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    const GroupWs& ws = a.groups[0];
+    const KState* ks = ws.kst;
+    const uint32_t p = ks->p, j = ks->j;
+    XPtrs& ps = xs.ps;
+    ps.farbits = ws.farbits;
+    ps.far_live = (j & 1) ? ws.far[1] : ws.far[0];
+    ps.fcount = &ws.ctl->fcount[j % 3];
+    ps.qbits = (p & 1) ? ws.qbits[0] : ws.qbits[1];
+    ps.q = (p & 1) ? ws.q[0] : ws.q[1];
+    ps.qcount = &ws.ctl->qcount[(p + 1) % 3];
+    ps.ovfbits = ws.ovfbits;
+    ps.ovf_cand = &ws.ctl->ovf_cand;
+    ps.slots = a.slots;
+    ps.h = a.h;
+    ps.div = a.div;
+    ps.bcur = ks->b;
+  }
   if (lane == 0) { xs.nfar[warp] = 0; xs.ncur[warp] = 0; }
-  __syncwarp();
-  const HubEnt* X = (p & 1) ? ws.hub[1] : ws.hub[0];
-  const unsigned long long* xpre = ws.xpre;
+  __syncthreads();
+  const KState* ks = a.groups[0].kst;
+  const uint32_t hn = ks->xn;
+  const unsigned long long E = ks->E;
+  const HubEnt* X = (ks->p & 1) ? a.groups[0].hub[1] : a.groups[0].hub[0];
+  const unsigned long long* xpre = a.groups[0].xpre;
   uint32_t* const dist = a.dist;
   const uint32_t colbits = a.colbits;
   const uint32_t cmask = colbits >= 32 ? 0xFFFFFFFFu : (1u << colbits) - 1u;
+  const bool lazy = a.lazy != 0;
   uint32_t my_fmin = kInf;
+  auto flush_far = [&]() {
+    __syncwarp();
+    const XPtrs& ps = xs.ps;
+    xflush(xs.far[warp], min(xs.nfar[warp], (uint32_t)kXSeg), ps.farbits, ps.far_live, ps.fcount, nullptr);
+    if (lane == 0) xs.nfar[warp] = 0;
+    __syncwarp();
+  };
+  auto flush_cur = [&]() {
+    __syncwarp();
+    const XPtrs& ps = xs.ps;
+    xflush(xs.cur[warp], min(xs.ncur[warp], (uint32_t)kXCur), ps.qbits, ps.q, ps.qcount, ps.slots);
+    if (lane == 0) xs.ncur[warp] = 0;
+    __syncwarp();
+  };
 
   const uint64_t W = (uint64_t)gridDim.x * (kBlock / 32), wg = (uint64_t)blockIdx.x * (kBlock / 32) + warp;
   const unsigned long long a0 = E * wg / W, b0 = E * (wg + 1) / W;
@@ -2277,54 +2326,41 @@ __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
         const uint32_t nd = du[k] + wt[k];
         const bool ovf = nd < du[k] || nd == kInf;
         if (((valid >> k) & 1u) && (ovf || nd < old[k])) {
+          const XPtrs& ps = xs.ps;
           if (ovf) {  // inline: no call in this loop
-            atomicOr(&ws.ovfbits[v[k] >> 5], 1u << (v[k] & 31));
-            atomicOr(&ctl->ovf_cand, 1u);
+            atomicOr(&ps.ovfbits[v[k] >> 5], 1u << (v[k] & 31));
+            atomicOr(ps.ovf_cand, 1u);
             continue;
           }
           red_min(dist + v[k], nd);
-          const uint32_t bk = a.h ? max(prio_bucket(nd, __ldg(a.h + v[k]), a.div), bcur) : fdiv(nd, a.div);
+          const uint32_t bk = ps.h ? max(prio_bucket(nd, __ldg(ps.h + v[k]), ps.div), ps.bcur) : fdiv(nd, ps.div);
           // staged per warp; a full segment (at most one iteration past half) takes the
           // lane's own dedup push to the global list
-          const bool cur = bk == bcur && !a.lazy;
+          const bool cur = bk == ps.bcur && !lazy;
           if (!cur) my_fmin = min(my_fmin, bk);
           const uint32_t pos = atomicAdd(cur ? &xs.ncur[warp] : &xs.nfar[warp], 1u);
           if (pos < (uint32_t)(cur ? kXCur : kXSeg)) {
             (cur ? xs.cur[warp] : xs.far[warp])[pos] = (int32_t)v[k];
           } else {
-            uint32_t* bits = cur ? ((p & 1) ? ws.qbits[0] : ws.qbits[1]) : ws.farbits;
+            uint32_t* bits = cur ? ps.qbits : ps.farbits;
             const uint32_t bit = 1u << (v[k] & 31);
             if (!(atomicOr(&bits[v[k] >> 5], bit) & bit)) {
-              const uint32_t q = atomicAdd(cur ? &ctl->qcount[(p + 1) % 3] : &ctl->fcount[j % 3], 1u);
-              (cur ? ((p & 1) ? ws.q[0] : ws.q[1]) : ((j & 1) ? ws.far[1] : ws.far[0]))[q] = (int32_t)v[k];
+              const uint32_t q = atomicAdd(cur ? ps.qcount : ps.fcount, 1u);
+              (cur ? ps.q : ps.far_live)[q] = (int32_t)v[k];
             }
           }
         }
       }
       __syncwarp();
-      if (xs.nfar[warp] > (uint32_t)(kXSeg / 2)) {
-        const uint32_t n = min(xs.nfar[warp], (uint32_t)kXSeg);
-        xflush(xs.far[warp], n, ws.farbits, (j & 1) ? ws.far[1] : ws.far[0], &ctl->fcount[j % 3], nullptr);
-        if (lane == 0) xs.nfar[warp] = 0;
-        __syncwarp();
-      }
-      if (xs.ncur[warp] > (uint32_t)(kXCur / 2)) {
-        const uint32_t n = min(xs.ncur[warp], (uint32_t)kXCur);
-        xflush(xs.cur[warp], n, (p & 1) ? ws.qbits[0] : ws.qbits[1], (p & 1) ? ws.q[0] : ws.q[1],
-               &ctl->qcount[(p + 1) % 3], a.slots);
-        if (lane == 0) xs.ncur[warp] = 0;
-        __syncwarp();
-      }
+      if (xs.nfar[warp] > (uint32_t)(kXSeg / 2)) flush_far();
+      if (xs.ncur[warp] > (uint32_t)(kXCur / 2)) flush_cur();
     }
   }
-  __syncwarp();
-  xflush(xs.far[warp], min(xs.nfar[warp], (uint32_t)kXSeg), ws.farbits, (j & 1) ? ws.far[1] : ws.far[0],
-         &ctl->fcount[j % 3], nullptr);
-  xflush(xs.cur[warp], min(xs.ncur[warp], (uint32_t)kXCur), (p & 1) ? ws.qbits[0] : ws.qbits[1],
-         (p & 1) ? ws.q[0] : ws.q[1], &ctl->qcount[(p + 1) % 3], a.slots);
+  flush_far();
+  flush_cur();
   const uint32_t fm = __reduce_min_sync(0xffffffffu, my_fmin);
-  if (lane == 0 && fm != kInf) atomicMin(&ctl->fmin[j % 3], fm);
-  if (blockIdx.x == 0 && tid == 0) ws.kst->pending = 0;
+  if (lane == 0 && fm != kInf) atomicMin(&a.groups[0].ctl->fmin[ks->j % 3], fm);
+  if (blockIdx.x == 0 && tid == 0) a.groups[0].kst->pending = 0;
 }
 #endif
 
