@@ -309,6 +309,8 @@ struct Ctx {
   uint32_t my_fmin;        // thread-local min far bucket (reduced at phase end)
   bool pre_read;
   bool lazy;               // fully lazy schedule: no eager current-bucket pushes
+  bool collect;            // expand collection (E1): every deg > 8 vertex goes to the CTA list,
+                           // which process_bin copies to the group list with one atomic
 };
 
 // Append v to the global frontier once per phase (dedup bit), warp-aggregated.
@@ -710,7 +712,7 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
         const int64_t beg = (int64_t)(((uint64_t)hi << 32) | lo);
         // hubs (deg >= hub_min): the group hub list, split over every CTA next phase;
         // one global atomic per warp (every CTA appends to the same counter)
-        const bool hub = mine && deg >= c.hub_min;
+        const bool hub = mine && deg >= c.hub_min && !c.collect;
         const uint32_t mh = __ballot_sync(0xffffffffu, hub);
         uint32_t hbase = 0;
         if (mh) {
@@ -1114,6 +1116,37 @@ __device__ __forceinline__ void process_bin(Ctx& c, Shared& s, const uint2* in, 
   TRACE(4);
   if constexpr (LD) return;  // no high-degree list on a low-degree graph
   const uint32_t nb = min(s.bigtail, (uint32_t)kBigCap);
+  if (c.collect && nb) {
+    // expand collection: the CTA's list joins the group list with ONE reservation (the
+    // whole grid appends to one counter); a list that no longer fits is relaxed here
+    if (threadIdx.x == 0) {
+      uint32_t old = ld_relaxed(c.hcount_next), got = kInf;
+      while (old + nb <= c.hubcap) {
+        const uint32_t seen = atomicCAS(c.hcount_next, old, old + nb);
+        if (seen == old) { got = old; break; }
+        old = seen;
+      }
+      s.xbase = got;
+      s.bigtail = 0;
+    }
+    __syncthreads();
+    const uint32_t base = s.xbase;
+    if (base != kInf) {
+      for (uint32_t i = threadIdx.x; i < nb; i += kBlock) {
+        const BigEnt be = c.big[i];
+        HubEnt he;
+        he.beg = be.beg;
+        he.deg = be.deg;
+        he.du = be.du;
+        c.hub_next[base + i] = he;
+      }
+      __syncthreads();  // c.big is refilled by the next chunk
+      return;
+    }
+    stage_big<FUSED>(c, s, nb, ne);
+    __syncthreads();
+    return;
+  }
   if (nb) {
     __syncthreads();  // everyone has read bigtail
     if (threadIdx.x == 0) s.bigtail = 0;
@@ -1540,6 +1573,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
     c.s = &s;
     c.pre_read = a.pre_read != 0;
     c.lazy = !FUSED && a.lazy != 0;
+    c.collect = false;
     c.hub_min = a.hub_min;
     c.h = a.h;
 
@@ -1776,6 +1810,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           // expand: this phase's high-degree frontier vertices join the hubs queued by the
           // previous phase in the group list, relaxed edge-balanced after the collection
           c.hub_min = kSlotEdges + 1;
+          c.collect = true;
           c.hub_next = hub_in;
           c.hcount_next = &ctl->hcount[p % 3];
           // split: a phase may stop for an external expand, which would drop this CTA's bin —
@@ -1865,6 +1900,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
         __syncthreads();
         if (XP && a.expand) {
           c.hub_min = a.hub_min;
+          c.collect = false;
           c.hub_next = (p & 1) ? ws.hub[0] : ws.hub[1];
           c.hcount_next = &ctl->hcount[(p + 1) % 3];
           if (a.split && tid == 0) s.cnt3[0] = 0;  // nothing was written to the bin
@@ -2120,7 +2156,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
 // frontier — and flushed with the dedup test-and-set and one append atomic per warp.
 constexpr int kXSeg = 512;     // far staging entries per warp (flushed above half)
 constexpr int kXCur = 64;      // current-bucket staging entries per warp (rare on skewed graphs)
-constexpr int kXRows = 8;      // rows of 32 edges per warp per iteration
+#ifndef GI_XROWS
+#define GI_XROWS 8
+#endif
+constexpr int kXRows = GI_XROWS;  // rows of 32 edges per warp per iteration
 
 // the pointers of expand_kernel's cold paths (pushes, flushes, overflow), read from shared
 // memory where used so that the edge loop keeps only its own values in registers

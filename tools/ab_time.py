@@ -28,6 +28,10 @@ for so in libs:
     res = []
     for fusion in ((1,) if cfg == 5 else (1, 0)):
         o = Opt(); lib.gi_options_default(ctypes.byref(o)); o.fusion = fusion
+        for kv in os.environ.get("AB_OPTS", "").split(","):  # e.g. AB_OPTS=cta_threads=512,expand=1
+            if kv:
+                k_, v_ = kv.split("=")
+                setattr(o, k_, int(v_))
         st = St(); ts = []
         for i in range(6):
             if cfg == 5:  # batch: every entry's gpu_ms is the whole batch's device time
