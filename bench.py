@@ -365,10 +365,10 @@ def run_single(args, gi, torch, rank, world, local):
         if int(np.diff(g.offsets).max(initial=0)) <= 8:  # both drains run on low-degree graphs
             variants = [("fused", dict(fusion=True, drain="bsp")),
                         ("fused_async_drain", dict(fusion=True, drain="async")), ("unfused", dict(fusion=False))]
-        variants.append(("lazy", dict(fusion=False, lazy=True)))
         else:
             variants += [("fused_expand", dict(fusion=True, expand="on")),
                          ("fused_no_expand", dict(fusion=True, expand="off"))]
+        variants.append(("lazy", dict(fusion=False, lazy=True)))
         compare = compare_variants(gi, G, src, delta, out, opts, variants)
 
     # ---- e2e through the public C ABI with HOST buffers (pinned), copies inside ----

@@ -124,6 +124,12 @@ typedef struct {
                                 getMinBucket) — one group barrier and one pile scan per round.
                                 Requires fusion = 0 (GI_ERR_INVALID_ARGUMENT otherwise). 0 = the
                                 eager current bucket (default) */
+  int32_t rung;              /* execution-group rung of the query groups (SURVEY.md §8(a) ladder,
+                                the thread-local bins of PAPER.md:471-476 generalised): 0 = auto
+                                (grid), 1 = one CTA per group (CTA barrier only), 2 = one
+                                thread-block cluster per group of group_ctas CTAs (default 8,
+                                at most 16; hardware cluster barrier), 3 = grid (group barrier of
+                                global atomics over every co-resident CTA, or group_ctas of them) */
 } gi_options;
 
 /* Counters of one query (SURVEY §8(a) "Counter definitions"). */
@@ -146,6 +152,7 @@ typedef struct {
   int32_t groups;              /* concurrent query groups (1 for single source) */
   int32_t kernel_kind;         /* persistent kernel that ran: 0 unfused, 1 fused + bsp drain,
                                   2 fused + async drain, 3 k-core */
+  int32_t rung;                /* rung the groups ran on: 1 CTA, 2 cluster, 3 grid */
 } gi_stats;
 
 /* Fill *opt with defaults (fusion on, library-default threshold, all CTAs). */

@@ -258,7 +258,8 @@ void ws_release(gi_graph* g, Workspace* w, bool healthy) {
 }
 
 void fill_stats(gi_stats* st, const QStats& q, float ms, int ctas, int groups, int kind, int threads,
-                int launches) {
+                int launches, int rung) {
+  st->rung = rung;
   st->buckets = q.buckets;
   st->rounds = q.rounds;
   st->grid_syncs = q.phases;
@@ -321,6 +322,9 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   if (opt.drain > 2) return fail(GI_ERR_INVALID_ARGUMENT, "drain must be 0 (auto), 1 (bsp) or 2 (async)");
   if (opt.expand < 0 || opt.expand > 2) return fail(GI_ERR_INVALID_ARGUMENT, "expand must be 0 (auto), 1 (on) or 2 (off)");
   if (opt.lazy != 0 && opt.lazy != 1) return fail(GI_ERR_INVALID_ARGUMENT, "lazy must be 0 or 1");
+  if (opt.rung < 0 || opt.rung > 3) return fail(GI_ERR_INVALID_ARGUMENT, "rung must be 0 (auto), 1 (cta), 2 (cluster) or 3 (grid)");
+  if (opt.rung == 2 && (opt.group_ctas < 0 || opt.group_ctas > 16))
+    return fail(GI_ERR_INVALID_ARGUMENT, "a cluster group has at most 16 CTAs");
   if (opt.lazy && opt.fusion) return fail(GI_ERR_INVALID_ARGUMENT, "the lazy schedule runs without fusion (fusion = 0)");
   if (heur && fused && opt.drain == 2) return fail(GI_ERR_UNSUPPORTED, "A* runs with the bsp drain (drain 0/1)");
   if (fused && opt.drain == 2 && g->max_deg > kAsyncMaxDeg)
@@ -379,6 +383,23 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
     if (ngroups < 1) ngroups = 1;
   }
 
+  // execution-group rung: a one-CTA group or one cluster per group
+  int rung = opt.rung == 1 ? 1 : opt.rung == 2 ? 2 : 0;
+  if (rung == 1) {
+    G = 1;
+    ngroups = batch ? std::min(nsrc, total) : 1;
+  } else if (rung == 2) {
+    const int cl = opt.group_ctas > 0 ? opt.group_ctas : 8;
+    int maxc = 0;
+    cudaError_t qe = wide ? v1024::query_clusters(kind, cl, &maxc) : v512::query_clusters(kind, cl, &maxc);
+    if (qe != cudaSuccess || maxc < 1) {
+      cudaGetLastError();
+      ws_release(g, w, true);
+      return fail(GI_ERR_UNSUPPORTED, "clusters of %d CTAs of this kernel cannot be resident", cl);
+    }
+    G = cl;
+    ngroups = batch ? std::min(nsrc, maxc) : 1;
+  }
   gi_status s = ws_prepare(g, w, ngroups, nsrc);
   if (s) { ws_release(g, w, false); return s; }
   cudaStream_t st = opt.cuda_stream ? (cudaStream_t)opt.cuda_stream : w->stream;
@@ -489,6 +510,7 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   a.colbits = g->colbits;
   a.split = a.expand;
   a.lazy = opt.lazy ? 1u : 0u;
+  a.rung = (uint32_t)rung;
   a.resume = 0;
   {
     const char* sm = getenv("GI_SPLIT_MIN");
@@ -587,7 +609,9 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   bool ovf = false;
   for (int i = 0; i < nsrc; ++i) {  // hq is the workspace's pinned buffer: read before release
     if (hq[i].overflow) ovf = true;
-    if (stats) fill_stats(&stats[i], hq[i], ms, G, ngroups, base_kind(kind), wide ? 1024 : 512, launches);
+    if (stats)
+      fill_stats(&stats[i], hq[i], ms, G, ngroups, base_kind(kind), wide ? 1024 : 512, launches,
+                 a.rung == 1 ? 1 : a.rung == 2 ? 2 : 3);
   }
   ws_release(g, w, true);
   if (ovf) return fail(GI_ERR_OVERFLOW, "a reachable vertex has distance >= UINT32_MAX");

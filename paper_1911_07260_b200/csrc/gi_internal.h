@@ -174,6 +174,9 @@ struct KArgs {
   uint32_t colbits;        // packed: bits of the column id
   uint32_t lazy;           // fully lazy schedule (unfused kernels): every lowering, the current
                            // bucket's included, goes through the far pile
+  uint32_t rung;           // execution-group rung (SURVEY §8(a) ladder): 0 = grid (group barrier
+                           // of global atomics), 1 = one CTA (CTA barrier), 2 = one thread-block
+                           // cluster per group (hardware cluster barrier)
   uint32_t split;          // single query: heavy expands run in expand_kernel (see KState)
   uint32_t resume;         // this launch resumes a query stopped for an external expand
   unsigned long long split_min;  // list edges from which a phase's expand runs outside
@@ -217,11 +220,13 @@ struct KcArgs {
 // The SSSP-family persistent kernels, compiled once per CTA width (gi_kernels.cu).
 namespace v512 {
 cudaError_t launch_sssp(const KArgs& a, int kind, int grid, cudaStream_t st);
+cudaError_t query_clusters(int kind, int cluster, int* max_clusters);
 cudaError_t query_occupancy(int kind, int* blocks_per_sm);
 int smem_bytes(int kind);
 }  // namespace v512
 namespace v1024 {
 cudaError_t launch_sssp(const KArgs& a, int kind, int grid, cudaStream_t st);
+cudaError_t query_clusters(int kind, int cluster, int* max_clusters);
 // the external expand of a split query (KState), 1024-thread CTAs on every SM
 cudaError_t launch_expand(const KArgs& a, cudaStream_t st, int* grid_used);
 cudaError_t query_occupancy(int kind, int* blocks_per_sm);

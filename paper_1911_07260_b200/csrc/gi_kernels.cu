@@ -243,7 +243,19 @@ __device__ __forceinline__ uint32_t prio_bucket(uint32_t d, uint32_t hv, const F
   return fdiv((p < d || p == kInf) ? kInf - 1u : p, f);
 }
 
-__device__ __forceinline__ void group_barrier(Ctl* ctl, uint32_t G) { dev::group_barrier(&ctl->bar, G); }
+// The group barrier of the execution-group ladder: a one-CTA group needs only
+// the CTA barrier, a group that is one thread-block cluster the hardware cluster barrier
+// (release / acquire at cluster scope), any other group the barrier of global atomics.
+__device__ __forceinline__ void group_barrier_r(Ctl* ctl, uint32_t G, uint32_t rung) {
+  if (rung == 1) {
+    __syncthreads();
+  } else if (rung == 2) {
+    __syncthreads();
+    cg::this_cluster().sync();
+  } else {
+    dev::group_barrier(&ctl->bar, G);
+  }
+}
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T x) {
@@ -1563,7 +1575,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
       ws.far[0][0] = src;
       atomicOr(&ws.farbits[src >> 5], 1u << (src & 31));
     }
-    if (!resuming) group_barrier(ctl, G);
+    if (!resuming) group_barrier_r(ctl, G, a.rung);
 
     Ctx c;
     c.dist = dist; c.slots = a.slots; c.edges = a.edges; c.div = a.div;
@@ -1904,7 +1916,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           c.hub_next = (p & 1) ? ws.hub[0] : ws.hub[1];
           c.hcount_next = &ctl->hcount[(p + 1) % 3];
           if (a.split && tid == 0) s.cnt3[0] = 0;  // nothing was written to the bin
-          group_barrier(ctl, G);  // the group list is complete
+          group_barrier_r(ctl, G, a.rung);  // the group list is complete
           ++phases;
           TRACE(19);
           if (tid == 0) s.xhn = min(__ldcg(&ctl->hcount[p % 3]), a.hubcap);
@@ -1912,7 +1924,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           const uint32_t xn = s.xhn;
           if (xn) {
             expand_scan(hub_in, ws.xpre, ws.xtot, xn, G, rank, s);
-            group_barrier(ctl, G);  // slice prefixes and totals are final
+            group_barrier_r(ctl, G, a.rung);  // slice prefixes and totals are final
             ++phases;
             if (tid < 32) {  // S[r] = sum of the slice totals before r
               unsigned long long carry = 0;
@@ -2074,7 +2086,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
         atomicAdd(&g_phase[3][p], busy);
       }
 #endif
-      group_barrier(ctl, G);
+      group_barrier_r(ctl, G, a.rung);
       TRACE(9);
       ++p;
       ++phases;
@@ -2137,7 +2149,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
       }
     }
     if (rank == 0 && tid == 0) ctl->next_si = a.ngroups + (int32_t)atomicAdd(a.src_next, 1u);
-    group_barrier(ctl, G);  // the next query re-initialises ctl
+    group_barrier_r(ctl, G, a.rung);  // the next query re-initialises ctl
     if (tid == 0) s.cnt = (uint32_t)__ldcg(&ctl->next_si);
     __syncthreads();
     si = (int32_t)s.cnt;
@@ -2536,7 +2548,45 @@ cudaError_t launch_sssp(const KArgs& a, int kind, int grid, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   KArgs args = a;
   void* params[] = {&args};
-  return cudaLaunchCooperativeKernel(kernel_fn(kind), dim3(grid), dim3(kBlock), params, smem_bytes(kind), st);
+  if (a.rung != 2)
+    return cudaLaunchCooperativeKernel(kernel_fn(kind), dim3(grid), dim3(kBlock), params, smem_bytes(kind), st);
+  // cluster rung: every group is one thread-block cluster (co-scheduled by the hardware;
+  // groups never wait on each other, so the launch need not be cooperative)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kBlock);
+  cfg.dynamicSmemBytes = smem_bytes(kind);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = a.group_size;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, kernel_fn(kind), params);
+}
+
+// How many clusters of `cluster` CTAs of this kernel variant fit on the device at once.
+cudaError_t query_clusters(int kind, int cluster, int* max_clusters) {
+  cudaError_t e = set_attrs(kind);
+  if (e != cudaSuccess) return e;
+  if (cluster > 8) {
+    e = cudaFuncSetAttribute(kernel_fn(kind), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cluster);
+  cfg.blockDim = dim3(kBlock);
+  cfg.dynamicSmemBytes = smem_bytes(kind);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaOccupancyMaxActiveClusters(max_clusters, kernel_fn(kind), &cfg);
 }
 
 #if GI_BLOCK >= 1024

@@ -172,6 +172,41 @@ def test_lazy_schedule(gi, config_graph):
         run(gi, G, 0, 1000, fusion=True, lazy=True)
 
 
+def test_execution_group_rungs(gi, config_graph):
+    """The execution-group ladder: one CTA per group (CTA barrier), one
+    thread-block cluster per group (hardware cluster barrier; 2..16 CTAs) and the grid give
+    the same exact distances, single and batch, fused / unfused / lazy / async drain; the
+    rung is reported."""
+    rng = np.random.default_rng(5)
+    graphs = [config_graph(1), gen.from_edges(1, []),
+              gen.uniform_random(3000, 20000, 0, 50, 9)]
+    for g in graphs:
+        G = gi.Graph.from_csr(g)
+        s = 0 if g.n < 3 else int(rng.integers(0, g.n))
+        ref, _ = oracle.dijkstra(g, s)
+        for o, want in ((dict(rung="cta"), 1), (dict(rung="cluster", group_ctas=2), 2),
+                        (dict(rung="cluster"), 2), (dict(rung="cluster", group_ctas=16), 2),
+                        (dict(rung="grid"), 3), (dict(rung="cta", fusion=False), 1),
+                        (dict(rung="cluster", group_ctas=4, fusion=False, lazy=True), 2),
+                        (dict(rung="cta", threshold=1), 1)):
+            for delta in (7, 1000):
+                d, st = run(gi, G, s, delta, **o)
+                assert np.array_equal(d, ref), (g.n, o, delta)
+                assert st["rung"] == want and st["buckets"] == oracle.bucket_count(ref, delta)
+        if g.n > 100:
+            srcs = rng.integers(0, g.n, 13).astype(np.int32)
+            refs, _, _ = oracle.dijkstra_many(g, srcs)
+            for o in (dict(rung="cta"), dict(rung="cluster", group_ctas=4), dict(rung="grid")):
+                out, sts = gi.sssp_batch(G, srcs, 100, **o)
+                assert np.array_equal(gi.as_uint32(out), refs), o
+    g = config_graph(1)
+    if max(np.diff(g.offsets)) <= 8:
+        G = gi.Graph.from_csr(g)
+        ref, _ = oracle.dijkstra(g, 0)
+        d, st = run(gi, G, 0, 1000, rung="cluster", drain="async")
+        assert np.array_equal(d, ref) and st["rung"] == 2
+
+
 def test_delta_le_wmin_processes_each_vertex_once(gi):
     """Δ <= w_min: every reached vertex is processed exactly once."""
     g = gen.grid(64, 64, 3, 4, 0)

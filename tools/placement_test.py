@@ -20,7 +20,8 @@ class Opt(ctypes.Structure):  # gi_options (include/gi.h)
     _fields_ = [("struct_size", ctypes.c_uint32), ("fusion", ctypes.c_int32), ("fusion_threshold", ctypes.c_uint32),
                 ("max_ctas", ctypes.c_int32), ("hub_min", ctypes.c_uint32), ("drain", ctypes.c_uint32),
                 ("group_ctas", ctypes.c_int32), ("pre_read", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p),
-                ("cta_threads", ctypes.c_int32), ("expand", ctypes.c_int32), ("lazy", ctypes.c_int32)]
+                ("cta_threads", ctypes.c_int32), ("expand", ctypes.c_int32), ("lazy", ctypes.c_int32),
+                ("rung", ctypes.c_int32)]
 
 
 class St(ctypes.Structure):  # gi_stats
@@ -28,7 +29,7 @@ class St(ctypes.Structure):  # gi_stats
                                                "spills", "vertices_processed", "edges_relaxed", "empty_extractions",
                                                "far_scanned", "critical_subrounds")] + [
         ("gpu_ms", ctypes.c_float), ("ctas", ctypes.c_int32), ("threads_per_cta", ctypes.c_int32),
-        ("groups", ctypes.c_int32), ("kernel_kind", ctypes.c_int32)]
+        ("groups", ctypes.c_int32), ("kernel_kind", ctypes.c_int32), ("rung", ctypes.c_int32)]
 
 
 def load(path):
