@@ -2551,7 +2551,12 @@ cudaError_t launch_sssp(const KArgs& a, int kind, int grid, cudaStream_t st) {
   if (a.rung != 2)
     return cudaLaunchCooperativeKernel(kernel_fn(kind), dim3(grid), dim3(kBlock), params, smem_bytes(kind), st);
   // cluster rung: every group is one thread-block cluster (co-scheduled by the hardware;
-  // groups never wait on each other, so the launch need not be cooperative)
+  // groups never wait on each other, so the launch need not be cooperative). The
+  // non-portable size flag belongs to each kernel variant: the expand (XP) variant chosen
+  // after query_clusters needs it too.
+  if (a.group_size > 8 &&
+      (e = cudaFuncSetAttribute(kernel_fn(kind), cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+    return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kBlock);
