@@ -11,14 +11,16 @@ import numpy as np  # noqa: E402
 
 import gen  # noqa: E402
 
-so = os.environ.get("TRACE_SO", "/tmp/libgi_trace.so")
+# TRACE_W=1024: the 1024-thread build is the primary one (the trace buffers live there)
+W = int(os.environ.get("TRACE_W", "512"))
+so = os.environ.get("TRACE_SO", f"/tmp/libgi_trace{W}.so")
 CS = os.path.join(ROOT, "paper_1911_07260_b200/csrc")
 if not os.path.exists(so) or os.environ.get("REBUILD"):
     nv = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-DGI_TRACE", "-Xcompiler",
           "-fPIC", "-I", os.path.join(ROOT, "include")]
     objs = []
-    for src, defs, obj in ((f"{CS}/gi_kernels.cu", ["-DGI_BLOCK=512", "-DGI_VARIANT=v512", "-DGI_PRIMARY=1"], "/tmp/tk512.o"),
-                           (f"{CS}/gi_kernels.cu", ["-DGI_BLOCK=1024", "-DGI_VARIANT=v1024", "-DGI_PRIMARY=0"], "/tmp/tk1024.o"),
+    for src, defs, obj in ((f"{CS}/gi_kernels.cu", ["-DGI_BLOCK=512", "-DGI_VARIANT=v512", f"-DGI_PRIMARY={int(W == 512)}"], "/tmp/tk512.o"),
+                           (f"{CS}/gi_kernels.cu", ["-DGI_BLOCK=1024", "-DGI_VARIANT=v1024", f"-DGI_PRIMARY={int(W == 1024)}"], "/tmp/tk1024.o"),
                            (f"{CS}/gi_capi.cu", [], "/tmp/tcapi.o"), (f"{CS}/gi_kcore.cu", [], "/tmp/tkcore.o")):
         subprocess.check_call(nv + defs + ["-c", src, "-o", obj])
         objs.append(obj)
@@ -57,7 +59,7 @@ out = torch.empty(g.n, dtype=torch.int32, device="cuda")
 opt = gi_options()
 lib.gi_options_default(ctypes.byref(opt))
 opt.max_ctas = max_ctas
-opt.cta_threads = 512  # the trace buffers live in the primary (512-thread) build
+opt.cta_threads = W  # the trace buffers live in the primary build
 opt.drain = {"async": 2, "bsp": 1, "unfused": 1}[drain]
 opt.fusion = 0 if drain == "unfused" else 1
 st = gi_stats()
