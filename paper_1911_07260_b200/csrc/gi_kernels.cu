@@ -1129,34 +1129,44 @@ __device__ __forceinline__ void process_bin(Ctx& c, Shared& s, const uint2* in, 
   if constexpr (LD) return;  // no high-degree list on a low-degree graph
   const uint32_t nb = min(s.bigtail, (uint32_t)kBigCap);
   if (c.collect && nb) {
-    // expand collection: the CTA's list joins the group list with ONE reservation (the
-    // whole grid appends to one counter); a list that no longer fits is relaxed here
+    // expand collection: the CTA's list joins the group list with ONE atomicAdd (the whole
+    // grid appends to one counter; a CAS reservation loop serialised the CTAs at one
+    // success per L2 round trip). Readers clamp the counter to hubcap; the entries past
+    // hubcap (possible only with hubs queued twice) are relaxed here.
     if (threadIdx.x == 0) {
-      uint32_t old = ld_relaxed(c.hcount_next), got = kInf;
-      while (old + nb <= c.hubcap) {
-        const uint32_t seen = atomicCAS(c.hcount_next, old, old + nb);
-        if (seen == old) { got = old; break; }
-        old = seen;
-      }
-      s.xbase = got;
+      s.xbase = atomicAdd(c.hcount_next, nb);
       s.bigtail = 0;
     }
     __syncthreads();
     const uint32_t base = s.xbase;
-    if (base != kInf) {
-      for (uint32_t i = threadIdx.x; i < nb; i += kBlock) {
-        const BigEnt be = c.big[i];
-        HubEnt he;
-        he.beg = be.beg;
-        he.deg = be.deg;
-        he.du = be.du;
-        c.hub_next[base + i] = he;
-      }
-      __syncthreads();  // c.big is refilled by the next chunk
-      return;
+    const uint32_t fit = base >= c.hubcap ? 0u : min(nb, c.hubcap - base);
+    for (uint32_t i = threadIdx.x; i < fit; i += kBlock) {
+      const BigEnt be = c.big[i];
+      HubEnt he;
+      he.beg = be.beg;
+      he.deg = be.deg;
+      he.du = be.du;
+      c.hub_next[base + i] = he;
     }
-    stage_big<FUSED>(c, s, nb, ne);
-    __syncthreads();
+    if (fit < nb) {  // block-uniform: move the tail to the front and relax it here
+      constexpr int PER = kBigCap / kBlock;
+      BigEnt t[PER];
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const uint32_t i = fit + threadIdx.x + k * kBlock;
+        if (i < nb) t[k] = c.big[i];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const uint32_t i = threadIdx.x + k * kBlock;
+        if (fit + i < nb) c.big[i] = t[k];
+      }
+      __syncthreads();
+      stage_big<FUSED>(c, s, nb - fit, ne);
+    }
+    __syncthreads();  // c.big is refilled by the next chunk
+    TRACE(24);
     return;
   }
   if (nb) {
@@ -1771,8 +1781,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
               keepm |= 1u << x;
             }
           }
+          TRACE(26);
           if (agg) cta_append(keepm, v, c.far_live, c.fcount_live, s.redw, nullptr);
           else warp_append(keepm, v, c.far_live, c.fcount_live, nullptr);
+          TRACE(27);
           // the extracted vertices: the CTA bin (fusion) while it has room, else — and
           // without fusion — the global frontier, deduplicated with all atomics in flight
           uint32_t ovm = FUSED ? 0u : livem;
@@ -1808,6 +1820,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
             if (agg) cta_append(newm, v, c.q_next, c.qcount_next, s.redw, c.slots);
             else warp_append(newm, v, c.q_next, c.qcount_next, c.slots);
           }
+          TRACE(28);
         }
         TRACE(6);
         const uint32_t tl = block_sum(nlive, s);  // ends with a barrier: ring fill is final
@@ -1905,6 +1918,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
               if (dyn && next < cnt) next = (uint32_t)first + atomicAdd(qclaim, claim);
             }
             __syncthreads();
+            TRACE(25);
           } else {
             base_static = base + chunk;
           }
