@@ -530,12 +530,17 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
     const char* sm = getenv("GI_SPLIT_MIN");
     // lists of fewer edges are relaxed in the persistent kernel (a stop costs ~40 µs)
     a.split_min = sm ? strtoull(sm, nullptr, 10) : (1ull << 20);
+    // big extractions too run outside (extract_kernel), from 2^21 pile entries (GI_XSPLIT_MIN;
+    // 0 keeps every extraction in the persistent kernel)
+    const char* xm = getenv("GI_XSPLIT_MIN");
+    a.xsplit_min = xm ? (uint32_t)strtoul(xm, nullptr, 10) : (1u << 21);
   }
   if (a.expand) {
     const int xk = kind == KIND_UNFUSED ? KIND_UNFUSED_XP : KIND_FUSED_BSP_XP;
     if (g->bps[wide][xk] >= bps) kind = xk;  // same co-residency as the kernel G was sized for
     else a.expand = a.split = 0;
   }
+  if (!a.split) a.xsplit_min = 0;
   if ((e = cudaMemsetAsync(w->d_src_next, 0, sizeof(uint32_t), st))) return bail(e, "init claim counter");
   a.src_next = w->d_src_next;  // claims count from 0; sources 0..ngroups-1 are taken statically
   a.h = d_h;
@@ -577,7 +582,7 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
           (e = cudaStreamSynchronize(st)))
         return bail(e, "sssp kernel segment");
       if (!*w->h_pending) break;
-      if (const char* dump = getenv("GI_DUMP_X")) {  // investigation only: the pending list to files
+      if (const char* dump = *w->h_pending == 1 ? getenv("GI_DUMP_X") : nullptr) {  // investigation only: the pending list to files
         KState hk;
         cudaMemcpy(&hk, kst, sizeof(hk), cudaMemcpyDeviceToHost);
         static int seq = 0;
@@ -599,7 +604,11 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
           fclose(f);
         }
       }
-      if ((e = v1024::launch_expand(a, st, nullptr))) return bail(e, "launch expand_kernel");
+      if (*w->h_pending == 2) {
+        if ((e = v1024::launch_extract(a, st))) return bail(e, "launch extract_kernel");
+      } else if ((e = v1024::launch_expand(a, st, nullptr))) {
+        return bail(e, "launch expand_kernel");
+      }
       if ((e = wide ? v1024::launch_sssp(ar, kind, G * ngroups, st) : v512::launch_sssp(ar, kind, G * ngroups, st)))
         return bail(e, "resume sssp_persistent");
       launches += 2;
@@ -977,6 +986,11 @@ gi_status gi_kcore_ex(const gi_graph* cg_, const gi_options* opt_in, uint32_t* c
   a.hubcap = w->hubcap;
   a.ctl = w->kc_ctl;
   a.stats = w->kc_stats;
+  a.slots = g->d_slots;
+  {
+    const char* e_ld = getenv("GI_KC_SLOTS");  // 0: the generic CSR path on every graph
+    a.ld = (g->max_deg <= (uint32_t)kSlotEdges && !(e_ld && e_ld[0] == '0')) ? 1u : 0u;
+  }
   int grid = g->sm_count * g->bps_kcore;
   if (opt.max_ctas > 0 && opt.max_ctas < grid) grid = opt.max_ctas;
   if ((e = cudaEventRecord(w->ev0, st))) return bail(e, "event");

@@ -127,8 +127,10 @@ struct KState {
   uint32_t last_b;              // bucket of the last counted extraction
   unsigned long long phases, rounds, buckets, empty, critical;  // group counters (rank 0)
   unsigned long long E;         // edges of the pending list
-  uint32_t xn;                  // entries of the pending list
-  uint32_t pending;             // 1 = the kernel stopped for an external expand of phase p
+  uint32_t xn;                  // entries of the pending list (extract: of the far pile)
+  uint32_t pending;             // 1 = the kernel stopped for an external expand of phase p,
+                                // 2 = for an external extraction of phase p (extract_kernel)
+  uint32_t rkind;               // what the resumed segment continues after (1 expand, 2 extract)
 };
 
 constexpr int kMaxGroupCtas = 1024;  // expand: largest group (CTAs) the slice totals are sized for
@@ -180,6 +182,7 @@ struct KArgs {
   uint32_t split;          // single query: heavy expands run in expand_kernel (see KState)
   uint32_t resume;         // this launch resumes a query stopped for an external expand
   unsigned long long split_min;  // list edges from which a phase's expand runs outside
+  uint32_t xsplit_min;     // far-pile entries from which an extraction runs outside (0: never)
 };
 
 // k-core (gi_kcore.cu): control block, statistics and arguments.
@@ -214,6 +217,8 @@ struct KcArgs {
   uint32_t hubcap;
   KcCtl* ctl;
   KcStats* stats;
+  const uint2* slots;   // [n][8] ELL slots (deg <= 8: the edges inline)
+  uint32_t ld;          // every adjacency fits its slot (max degree <= 8): the slot path
 };
 
 // Host-side launchers (gi_kernels.cu).
@@ -229,6 +234,8 @@ cudaError_t launch_sssp(const KArgs& a, int kind, int grid, cudaStream_t st);
 cudaError_t query_clusters(int kind, int cluster, int* max_clusters);
 // the external expand of a split query (KState), 1024-thread CTAs on every SM
 cudaError_t launch_expand(const KArgs& a, cudaStream_t st, int* grid_used);
+// the external extraction of a split query (KState.pending == 2), a streaming partition
+cudaError_t launch_extract(const KArgs& a, cudaStream_t st);
 cudaError_t query_occupancy(int kind, int* blocks_per_sm);
 int smem_bytes(int kind);
 }  // namespace v1024

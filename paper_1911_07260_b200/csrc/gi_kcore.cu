@@ -84,6 +84,7 @@ struct KcCtx {
 };
 
 __device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) { return __ldcg(p); }
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 // Warp-aggregated append of v (lanes with `want`) to a global list.
 __device__ __forceinline__ void kc_append(bool want, int32_t v, int32_t* list, uint32_t* count) {
@@ -280,6 +281,64 @@ __device__ __forceinline__ void kc_relax_entries(const KcArgs& a, KcShared& s, c
   __syncthreads();
 }
 
+// Low-degree graphs (every adjacency in its 64-byte ELL slot, a.ld): relax the edges of the
+// cnt vertices of `list` (global frontier or shared-memory bin) with one octet of lanes per
+// vertex — lane k of the octet takes entry k of the slot (one coalesced 64-byte load per
+// vertex, prefetched into L1 when the vertex was pushed into this CTA's bin). The chain of
+// a fused sub-round is then slot (L1) -> decrement (L2) -> push, instead of offsets ->
+// edges -> coreness probe -> decrement -> claim:
+//   - no coreness probe: a finished vertex's priority is <= its coreness and every later
+//     decrement keeps it there (the decrements of a vertex sum to its degree, its initial
+//     priority, so it never wraps), so only an unfinished vertex can cross from > k to <= k;
+//   - no CAS claim: in the slot path the extraction and the drains of a phase are separated
+//     by a group barrier, so the one crossing subtraction is the vertex's only claimant and
+//     writes its coreness with a plain store.
+// Called by all threads; ends with a CTA barrier.
+template <int U>
+__device__ __forceinline__ void kc_relax_slots(const KcArgs& a, KcCtx& c, const int32_t* list, uint32_t cnt) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, sub = tid & 7;
+  const uint32_t k = c.k;
+  const uint32_t nitems = cnt * 8;
+  for (uint32_t base = 0; base < nitems; base += kKcBlock * U) {  // block-uniform trip count
+    uint32_t tv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t item = base + u * kKcBlock + tid;
+      tv[u] = kColEmpty;
+      if (item < nitems) tv[u] = __ldg(a.slots + 8 * (size_t)list[item >> 3] + sub).x;
+    }
+    uint32_t lead = 0, cntp[U], old[U];
+    unsigned ne = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool want = tv[u] != kColEmpty;
+      ne += want;
+      const uint32_t peers = __match_any_sync(0xffffffffu, tv[u]);
+      cntp[u] = __popc(peers);
+      if (want && (__ffs(peers) - 1) == (int)lane) lead |= 1u << u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) old[u] = (lead & (1u << u)) ? atomicSub(a.prio + tv[u], cntp[u]) : 0u;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      bool cross = false;
+      if (lead & (1u << u)) {
+        if (old[u] > k && old[u] - cntp[u] <= k) {
+          cross = true;
+          a.core[tv[u]] = k;
+          prefetch_l1(a.slots + 8 * (size_t)tv[u]);  // relaxed by this CTA next sub-round
+        } else if (old[u] > k) {
+          c.my_kmin = min(c.my_kmin, old[u] - cntp[u]);
+        }
+      }
+      c.nfin += cross;
+      kc_push(c, cross, (int32_t)tv[u]);
+    }
+    c.nedge += ne;
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
   extern __shared__ unsigned long long kc_dyn[];  // beg, pre [kKcChunk] 8 B; bins [2][kKcChunk] 4 B
   __shared__ KcShared s;
@@ -391,7 +450,16 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
           const bool live = v[x] >= 0 && cc[x] == kUnset;  // finished entries are dropped
           // a vertex is finished exactly once (its edges are decrements, not idempotent):
           // the extraction and a concurrent crossing in another CTA's drain race for it
-          const bool fin = live && pr[x] <= k && atomicCAS(a.core + v[x], kUnset, k) == kUnset;
+          // (slot path: no drain runs during the extraction — a group barrier follows it)
+          bool fin = live && pr[x] <= k;
+          if (fin) {
+            if (a.ld) {
+              a.core[v[x]] = k;
+              prefetch_l1(a.slots + 8 * (size_t)v[x]);
+            } else {
+              fin = atomicCAS(a.core + v[x], kUnset, k) == kUnset;
+            }
+          }
           const bool keep = live && pr[x] > k;
           if (fin) { ++c.nfin; ++nx; }
           if (keep) { c.my_kmin = min(c.my_kmin, pr[x]); keepm |= 1u << x; }
@@ -429,6 +497,9 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
       nx = __reduce_add_sync(0xffffffffu, nx);
       if (lane == 0 && nx) atomicAdd(&ctl->xfin[j % 3], nx);
       __syncthreads();
+      // slot path: the drains below claim crossings without a CAS, so no CTA may still be
+      // extracting (the extraction's own claims are plain stores too)
+      if (a.ld) dev::group_barrier(&ctl->bar, G);
     } else {
       // edges.from(frontier).applyUpdatePriority(apply_f). Hubs queued in
       // the previous phase first: every CTA relaxes its 1/G slice of every hub's edges.
@@ -461,8 +532,12 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
         const uint32_t base = s.claim;
         if (base >= cnt) break;
         const uint32_t chunk = min(claim, cnt - base);
-        kc_stage_vertices(a, sm, c, q_in + base, chunk);
-        kc_relax_entries(a, s, sm, c, chunk);
+        if (a.ld) {
+          kc_relax_slots<4>(a, c, q_in + base, chunk);
+        } else {
+          kc_stage_vertices(a, sm, c, q_in + base, chunk);
+          kc_relax_entries(a, s, sm, c, chunk);
+        }
         if (tid == 0) {
           s.claim = dyn ? next : cnt;
           if (dyn && next < cnt) next = (uint32_t)first + atomicAdd(qclaim, claim);
@@ -489,8 +564,13 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
       if (tid == 0) { s.bincnt[(it + 1) % 3] = 0; ++subrounds; }
       c.out = sm.bin[it & 1];
       c.outcnt = &s.bincnt[it % 3];
-      kc_stage_vertices(a, sm, c, in, nin);
-      kc_relax_entries(a, s, sm, c, nin);  // ends with a barrier
+      if (a.ld) {
+        if (nin * 8 <= (uint32_t)kKcBlock) kc_relax_slots<1>(a, c, in, nin);
+        else kc_relax_slots<4>(a, c, in, nin);
+      } else {
+        kc_stage_vertices(a, sm, c, in, nin);
+        kc_relax_entries(a, s, sm, c, nin);  // ends with a barrier
+      }
     }
 
     if (tid == 0 && subrounds != sub0) {
@@ -512,8 +592,11 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
   // statistics
   const unsigned nf = __reduce_add_sync(0xffffffffu, (unsigned)c.nfin);
   if (lane == 0 && nf) atomicAdd(&a.stats->vertices, (unsigned long long)nf);
+  unsigned long long ned = c.nedge;  // per thread (slot path) or per CTA (thread 0)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ned += __shfl_down_sync(0xffffffffu, ned, o);
+  if (lane == 0 && ned) atomicAdd(&a.stats->edges, ned);
   if (tid == 0) {
-    if (c.nedge) atomicAdd(&a.stats->edges, c.nedge);
     if (subrounds) atomicAdd(&a.stats->subrounds, subrounds);
     if (spills) atomicAdd(&a.stats->spills, spills);
     if (rank == 0) {

@@ -181,8 +181,13 @@ __device__ __forceinline__ uint64_t pol_evict_first() {
 #define GI_X_EDGE_EF 0
 #endif
 // relaxation-target reads / writes of dist (skewed graphs: the hot targets should stay in L2)
+#ifndef GI_X_DIST_L1
+#define GI_X_DIST_L1 0
+#endif
 __device__ __forceinline__ uint32_t ld_dist_tgt(const uint32_t* p) {
-#if GI_X_DIST_EL
+#if GI_X_DIST_L1
+  return __ldca(p);  // L1-cached pre-read: a stale value is only ever too high (dist decreases)
+#elif GI_X_DIST_EL
   uint32_t v;
   asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_evict_last()));
   return v;
@@ -1615,16 +1620,53 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
     unsigned long long sub_at_phase_start = 0;
     uint32_t p = 0, j = 0, b = 0, prev = MODE_NONE;
     uint32_t last_b = kInf;  // bucket of the last extraction with live vertices (rank 0, thread 0)
-    bool mid = false;  // resuming inside ROUND phase p, after its external expand
+    bool mid = false;  // resuming inside phase p, after its external expand / extraction
+    bool xmid = false;  // ... after its external extraction: phase p was an EXTRACT phase
+    bool xprev = false;  // the previous phase's extraction ran outside (its bucket went to q)
     if (resuming) {
       const KState* ks = ws.kst;
       p = ks->p; j = ks->j; b = ks->b; prev = ks->prev; last_b = ks->last_b;
+      xmid = ks->rkind == 2;
       if (rank == 0 && tid == 0) {
         phases = ks->phases; rounds = ks->rounds; buckets = ks->buckets; empty = ks->empty; critical = ks->critical;
       }
       mid = true;
     }
 
+    // split query (XP kernels): save the phase loop's state in KState and flush this
+    // segment's statistics, before the kernel returns for an external expand (kind 1) of
+    // phase p's group list (E edges, xn entries) or an external extraction (kind 2) of the
+    // xn-entry far pile; the host runs it and resumes this kernel at phase p
+    auto stop_for_outside = [&](unsigned long long E, uint32_t xn, uint32_t kind) {
+      {
+        const uint32_t w = tid >> 5;
+        warp_flush_far(c, c.farstage + w * kFarSeg, min(s.wfar[w], (uint32_t)kFarSeg));
+        const uint32_t fm = __reduce_min_sync(0xffffffffu, c.my_fmin);
+        if ((tid & 31) == 0 && fm != kInf) atomicMin(&s.fmin, fm);
+      }
+      tnv += nv; tne += ne;
+      const unsigned long long tv = block_sum(tnv, s);
+      const unsigned long long te = block_sum(tne, s);
+      if (tid == 0) {
+        if (s.fmin != kInf) atomicMin(&ctl->fmin[j % 3], s.fmin);
+        QStats* q = &a.qstats[si];
+        atomicAdd(&q->vertices, tv);
+        atomicAdd(&q->edges, te + (rank == 0 ? E : 0ull));  // the external expand's edges
+        if (subrounds) atomicAdd(&q->subrounds, subrounds);
+        if (spills) atomicAdd(&q->spills, spills);
+        if (kind == 2 && rank == 0) scanned += xn;  // the external extraction's scan
+        if (scanned) atomicAdd(&q->far_scanned, scanned);
+        if (rank == 0) {
+          KState* ks = ws.kst;
+          ks->p = p; ks->j = j; ks->b = b; ks->prev = prev; ks->last_b = last_b;
+          ks->phases = phases; ks->rounds = rounds; ks->buckets = buckets; ks->empty = empty;
+          ks->critical = critical; ks->E = E; ks->xn = xn; ks->rkind = kind;
+          __threadfence();
+          ks->pending = kind;
+        }
+      }
+      TRACE_FLUSH();
+    };
     for (;;) {
       if (mid && tid == 0) {  // phase p continues: its list was relaxed outside, the bins are empty
         s.mode = MODE_ROUND; s.cnt = 0; s.hn = 0;
@@ -1643,7 +1685,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
         if (p > 0 && rank == 0) critical += __ldcg(&ctl->maxsub[(p - 1) % 3]);
         if (prev == MODE_EXTRACT) {
           // a lazy schedule extracts a bucket once per round: it counts once
-          if (xl) { if (b != last_b) ++buckets; last_b = b; if (FUSED) ++rounds; } else { ++empty; }
+          // (an extraction that ran outside sent its bucket to the global frontier: the
+          // next ROUND phase counts that round)
+          if (xl) { if (b != last_b) ++buckets; last_b = b; if (FUSED && !xprev) ++rounds; } else { ++empty; }
         }
         uint32_t mode;
         s.hn = min(hn, a.hubcap);
@@ -1749,6 +1793,15 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           }
         }
       } else if (mode == MODE_EXTRACT) {
+        if constexpr (XP) {
+          // split query, big pile: the partition runs outside as a streaming kernel
+          // (extract_kernel), its bucket going to the global frontier; this kernel resumes
+          // at phase p with empty bins
+          if (a.xsplit_min && cnt >= a.xsplit_min) {
+            stop_for_outside(0ull, cnt, 2u);
+            return;
+          }
+        }
         // (d)+(a): partition the far pile by recomputed bucket.
         // kXtr entries per thread per chunk with every load in flight together; the
         // entries kept for later buckets are compacted with one global atomic per warp
@@ -1968,33 +2021,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
                 if (base)
                   for (uint32_t i = lo_x + tid; i < hi_x; i += kBlock) ws.xpre[i] += base;
               }
-              {
-                const uint32_t w = tid >> 5;
-                warp_flush_far(c, c.farstage + w * kFarSeg, min(s.wfar[w], (uint32_t)kFarSeg));
-                const uint32_t fm = __reduce_min_sync(0xffffffffu, c.my_fmin);
-                if ((tid & 31) == 0 && fm != kInf) atomicMin(&s.fmin, fm);
-              }
-              tnv += nv; tne += ne;
-              const unsigned long long tv = block_sum(tnv, s);
-              const unsigned long long te = block_sum(tne, s);
-              if (tid == 0) {
-                if (s.fmin != kInf) atomicMin(&ctl->fmin[j % 3], s.fmin);
-                QStats* q = &a.qstats[si];
-                atomicAdd(&q->vertices, tv);
-                atomicAdd(&q->edges, te + (rank == 0 ? E : 0ull));  // the external expand's edges
-                if (subrounds) atomicAdd(&q->subrounds, subrounds);
-                if (spills) atomicAdd(&q->spills, spills);
-                if (scanned) atomicAdd(&q->far_scanned, scanned);
-                if (rank == 0) {
-                  KState* ks = ws.kst;
-                  ks->p = p; ks->j = j; ks->b = b; ks->prev = prev; ks->last_b = last_b;
-                  ks->phases = phases; ks->rounds = rounds; ks->buckets = buckets; ks->empty = empty;
-                  ks->critical = critical; ks->E = E; ks->xn = xn;
-                  __threadfence();
-                  ks->pending = 1;
-                }
-              }
-              TRACE_FLUSH();
+              stop_for_outside(E, xn, 1u);
               return;
             }
 #if GI_INKERNEL_EXPAND
@@ -2104,7 +2131,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
       TRACE(9);
       ++p;
       ++phases;
-      prev = mode;
+      prev = xmid ? (uint32_t)MODE_EXTRACT : mode;
+      xprev = xmid;
+      xmid = false;
     }
 
     // ---- overflow resolution: a vertex with an overflowing candidate that never
@@ -2427,6 +2456,110 @@ __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
   if (lane == 0 && fm != kInf) atomicMin(&a.groups[0].ctl->fmin[ks->j % 3], fm);
   if (blockIdx.x == 0 && tid == 0) a.groups[0].kst->pending = 0;
 }
+
+// The external extraction of a split query (KState.pending == 2): phase p's partition of
+// the far pile by recomputed bucket, (d)+(a) as a streaming
+// kernel — the persistent kernel's in-phase extraction keeps 4 entries per thread in flight
+// between CTA barriers and same-word appends; here every CTA takes tiles of kETile entries,
+// all loads of a tile in flight together, and appends with ONE atomic per list per tile.
+// An entry of bucket b joins the global frontier of phase p+1 (the pile holds a vertex at
+// most once, so no dedup test is needed); a later bucket is kept in the live pile and
+// min-reduced into the next bucket bound; an earlier one is stale and dropped. The dedup
+// bit of every leaving entry is cleared.
+constexpr int kEBlock = 512;
+constexpr int kEPer = 8;
+constexpr uint32_t kETile = kEBlock * kEPer;
+
+__global__ void __launch_bounds__(kEBlock) extract_kernel(KArgs a) {
+  __shared__ uint32_t s_keep[kEBlock / 32], s_live[kEBlock / 32];
+  __shared__ uint32_t s_fmin, s_nlive;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const GroupWs& ws = a.groups[0];
+  const KState* ks = ws.kst;
+  const uint32_t p = ks->p, j = ks->j, b = ks->b, cnt = ks->xn;
+  const int32_t* far_src = (j & 1) ? ws.far[0] : ws.far[1];
+  int32_t* far_live = (j & 1) ? ws.far[1] : ws.far[0];
+  uint32_t* fcount_live = &ws.ctl->fcount[j % 3];
+  int32_t* q_next = (p & 1) ? ws.q[0] : ws.q[1];
+  uint32_t* qcount_next = &ws.ctl->qcount[(p + 1) % 3];
+  const uint32_t* dist = a.dist;
+  if (tid == 0) { s_fmin = kInf; s_nlive = 0; }
+  uint32_t my_fmin = kInf;
+  for (uint32_t t0 = blockIdx.x * kETile; t0 < cnt; t0 += gridDim.x * kETile) {
+    int32_t v[kEPer];
+    uint32_t d[kEPer], hv[kEPer];
+#pragma unroll
+    for (int x = 0; x < kEPer; ++x) {
+      const uint32_t i = t0 + x * kEBlock + tid;
+      v[x] = i < cnt ? __ldcs(far_src + i) : -1;  // read once
+    }
+#pragma unroll
+    for (int x = 0; x < kEPer; ++x) d[x] = v[x] >= 0 ? ld_dist(dist + v[x]) : kInf;
+#pragma unroll
+    for (int x = 0; x < kEPer; ++x) hv[x] = (a.h && v[x] >= 0) ? __ldg(a.h + v[x]) : 0u;
+    uint32_t keepm = 0, livem = 0;
+#pragma unroll
+    for (int x = 0; x < kEPer; ++x) {
+      if (v[x] < 0) continue;
+      const uint32_t bk = prio_bucket(d[x], hv[x], a.div);
+      if (bk <= b) {
+        atomicAnd(&ws.farbits[v[x] >> 5], ~(1u << (v[x] & 31)));
+        if (bk == b) livem |= 1u << x;  // else: stale (already settled)
+      } else {
+        my_fmin = min(my_fmin, bk);
+        keepm |= 1u << x;
+      }
+    }
+    // per-warp counts, one reservation per list per tile
+    uint32_t km[kEPer], lm[kEPer], kpre[kEPer], lpre[kEPer], kt = 0, lt = 0;
+#pragma unroll
+    for (int x = 0; x < kEPer; ++x) {
+      km[x] = __ballot_sync(0xffffffffu, (keepm >> x) & 1u);
+      lm[x] = __ballot_sync(0xffffffffu, (livem >> x) & 1u);
+      kpre[x] = kt; lpre[x] = lt;
+      kt += __popc(km[x]); lt += __popc(lm[x]);
+    }
+    if (lane == 0) { s_keep[warp] = kt; s_live[warp] = lt; }
+    __syncthreads();
+    if (tid < 32) {
+      const uint32_t k0 = tid < kEBlock / 32 ? s_keep[tid] : 0u, l0 = tid < kEBlock / 32 ? s_live[tid] : 0u;
+      uint32_t ki = k0, li = l0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t a1 = __shfl_up_sync(0xffffffffu, ki, o), a2 = __shfl_up_sync(0xffffffffu, li, o);
+        if (tid >= (uint32_t)o) { ki += a1; li += a2; }
+      }
+      const uint32_t ktot = __shfl_sync(0xffffffffu, ki, 31), ltot = __shfl_sync(0xffffffffu, li, 31);
+      uint32_t kb = 0, lb = 0;
+      if (tid == 0) {
+        if (ktot) kb = atomicAdd(fcount_live, ktot);
+        if (ltot) { lb = atomicAdd(qcount_next, ltot); s_nlive += ltot; }
+      }
+      kb = __shfl_sync(0xffffffffu, kb, 0);
+      lb = __shfl_sync(0xffffffffu, lb, 0);
+      if (tid < kEBlock / 32) { s_keep[tid] = kb + ki - k0; s_live[tid] = lb + li - l0; }
+    }
+    __syncthreads();
+    const uint32_t kw = s_keep[warp], lw = s_live[warp], ltm = (1u << lane) - 1u;
+#pragma unroll
+    for (int x = 0; x < kEPer; ++x) {
+      if ((keepm >> x) & 1u) far_live[kw + kpre[x] + __popc(km[x] & ltm)] = v[x];
+      if ((livem >> x) & 1u) {
+        prefetch_l2(a.slots + 8 * (size_t)v[x]);  // read by the next ROUND phase
+        q_next[lw + lpre[x] + __popc(lm[x] & ltm)] = v[x];
+      }
+    }
+    __syncthreads();  // s_keep / s_live are rewritten by the next tile
+  }
+  const uint32_t fm = __reduce_min_sync(0xffffffffu, my_fmin);
+  if (lane == 0 && fm != kInf) atomicMin(&s_fmin, fm);
+  __syncthreads();
+  if (tid == 0) {
+    if (s_fmin != kInf) atomicMin(&ws.ctl->fmin[j % 3], s_fmin);
+    if (s_nlive) atomicAdd(&ws.ctl->xlive[j % 3], s_nlive);
+    if (blockIdx.x == 0) ws.kst->pending = 0;
+  }
+}
 #endif
 
 #if GI_PRIMARY
@@ -2623,6 +2756,17 @@ cudaError_t launch_expand(const KArgs& a, cudaStream_t st, int* grid_used) {
   KArgs args = a;
   void* params[] = {&args};
   return cudaLaunchKernel(fn, dim3(grid), dim3(kBlock), params, smem, st);
+}
+
+cudaError_t launch_extract(const KArgs& a, cudaStream_t st) {
+  int dev = 0, sms = 0, bps = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, extract_kernel, kEBlock, 0);
+  if (e != cudaSuccess) return e;
+  // the pile size is read by the kernel (KState.xn): one resident wave, tiles grid-strided
+  extract_kernel<<<sms * (bps > 0 ? bps : 1), kEBlock, 0, st>>>(a);
+  return cudaGetLastError();
 }
 #endif
 

@@ -472,6 +472,50 @@ def test_expand_split_segments(gi, monkeypatch):
         assert gi.ppsp(G, s, tgt, 3, expand="on")[0] == int(ref[tgt]), t
 
 
+def test_extract_split_segments(gi, monkeypatch, config_graph):
+    """Split extraction (single queries on skewed graphs with expand): an EXTRACT phase whose
+    far pile holds >= GI_XSPLIT_MIN entries stops the persistent kernel (KState, pending 2);
+    extract_kernel partitions the pile (bucket b -> the global frontier, later buckets kept,
+    earlier ones dropped) and the kernel resumes at the same phase. With GI_XSPLIT_MIN=1 every
+    extraction splits, mixed with split expands; fused / unfused / lazy, PPSP and A*; and
+    config 3 at full size."""
+    monkeypatch.setenv("GI_XSPLIT_MIN", "1")
+    rng = np.random.default_rng(47)
+    for t in range(3):
+        n = int(rng.integers(3_000, 40_000))
+        deg = np.minimum(rng.zipf(1.6, size=n), n - 1)
+        deg[rng.integers(0, n, 2)] = rng.integers(1_000, max(1_001, n // 3), 2)
+        wmax = int(rng.choice([5, 1 << 22]))
+        edges = [(u, int(v), int(w)) for u in range(n) for v, w in
+                 zip(rng.integers(0, n, deg[u]), rng.integers(1, wmax, deg[u]))]
+        g = gen.from_edges(n, edges)
+        G = gi.Graph.from_csr(g)
+        s = int(np.argmax(deg))
+        ref, _ = oracle.dijkstra(g, s)
+        for split_min in ("1", str(1 << 40)):  # with / without split expands
+            monkeypatch.setenv("GI_SPLIT_MIN", split_min)
+            for o, delta in ((dict(expand="on"), 1), (dict(expand="on"), 9), (dict(expand="on", fusion=False), 4),
+                             (dict(expand="on", fusion=False, lazy=True), 2), (dict(expand="on", max_ctas=3), 3)):
+                d, st = run(gi, G, s, delta, **o)
+                assert np.array_equal(d, ref), (t, split_min, o, delta)
+                assert st["buckets"] == oracle.bucket_count(ref, delta), (t, split_min, o, delta)
+                assert st["kernel_launches"] > 2, (t, split_min, o, delta)  # it did split
+        tgt = int(rng.integers(0, n))
+        assert gi.ppsp(G, s, tgt, 3, expand="on")[0] == int(ref[tgt]), t
+        h = np.zeros(n, np.uint32)
+        assert gi.astar(G, s, tgt, 3, h, expand="on")[0] == int(ref[tgt]), t
+    monkeypatch.setenv("GI_SPLIT_MIN", str(1 << 20))
+    monkeypatch.setenv("GI_XSPLIT_MIN", "4096")
+    g = config_graph(3)
+    G = gi.Graph.from_csr(g)
+    src = gen.config_source(3, g)
+    ref, _ = oracle.dijkstra(g, src)
+    for delta in (1, 2, 8):
+        d, st = run(gi, G, src, delta, expand="on")
+        assert np.array_equal(d, ref), delta
+        assert st["buckets"] == oracle.bucket_count(ref, delta), delta
+
+
 @pytest.mark.slow
 @pytest.mark.skipif(os.environ.get("GI_SKIP_CFG4") == "1",
                     reason="config 4 (RMAT-26, 2.1 B edges): ~2 min and ~25 GB of host RAM (GI_SKIP_CFG4=1)")
