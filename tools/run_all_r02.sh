@@ -1,12 +1,13 @@
 #!/bin/bash
 # round-2 full run: GPU tests, the default bench (no generator cache, as the driver runs it),
-# the reference arm, and the secondary app lines
+# the reference arm, and the secondary app lines. Usage: run_all_r02.sh [tag] (default r02aj)
+T=${1:-r02aj}
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 2400 python -m pytest tests -x -q -m gpu > gpurun_out/r02aj_tests.log 2>&1
-echo "tests rc=$?" >> gpurun_out/r02aj_tests.log
-( time timeout 1500 python bench.py ) > gpurun_out/r02aj_bench.log 2> gpurun_out/r02aj_bench.err
-( time timeout 1500 python bench.py --impl reference --steps 3 --warmup 1 ) > gpurun_out/r02aj_ref.log 2> gpurun_out/r02aj_ref.err
-for c in 1 2 3; do timeout 600 python bench.py --config $c --steps 10 --warmup 3; done > gpurun_out/r02aj_cfgs.log 2>&1
-timeout 900 python bench.py --config 5 --steps 5 --warmup 2 > gpurun_out/r02aj_cfg5.log 2>&1
-for app in ppsp astar kcore; do timeout 600 python bench.py --config 2 --app $app --steps 10 --warmup 3; done > gpurun_out/r02aj_apps.log 2>&1
-timeout 600 python bench.py --config 3 --app kcore --steps 10 --warmup 3 >> gpurun_out/r02aj_apps.log 2>&1
+timeout 2400 python -m pytest tests -x -q -m gpu > gpurun_out/${T}_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/${T}_tests.log
+( time timeout 1500 python bench.py ) > gpurun_out/${T}_bench.log 2> gpurun_out/${T}_bench.err
+( time timeout 1500 python bench.py --impl reference --steps 3 --warmup 1 ) > gpurun_out/${T}_ref.log 2> gpurun_out/${T}_ref.err
+for c in 1 2 3; do timeout 600 python bench.py --config $c --steps 10 --warmup 3; done > gpurun_out/${T}_cfgs.log 2>&1
+timeout 900 python bench.py --config 5 --steps 5 --warmup 2 > gpurun_out/${T}_cfg5.log 2>&1
+for app in ppsp astar kcore; do timeout 600 python bench.py --config 2 --app $app --steps 10 --warmup 3; done > gpurun_out/${T}_apps.log 2>&1
+timeout 600 python bench.py --config 3 --app kcore --steps 10 --warmup 3 >> gpurun_out/${T}_apps.log 2>&1
