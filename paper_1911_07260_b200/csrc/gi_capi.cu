@@ -74,6 +74,7 @@ struct Workspace {
   uint32_t** d_peers = nullptr;  // gi_sssp_batch_peers: device copy of the peer row bases
   int peercap = 0;
   uint32_t* h_pending = nullptr;  // pinned: KState.pending of a split query, read between segments
+  uint8_t* d_mirror = nullptr;    // expand: 1-byte saturated copy of dist [n] (KArgs.mirror)
   uint32_t* d_h = nullptr;      // staging for a host A* heuristic
   size_t hcap = 0;
   uint32_t* kc_prio = nullptr;  // k-core: priorities [n]
@@ -93,6 +94,7 @@ struct Workspace {
     if (h_srcs) cudaFreeHost(h_srcs);
     if (h_qstats) cudaFreeHost(h_qstats);
     if (h_pending) cudaFreeHost(h_pending);
+    if (d_mirror) cudaFree(d_mirror);
     if (d_src_next) cudaFree(d_src_next);
     if (kc_prio) cudaFree(kc_prio);
     if (kc_ctl) cudaFree(kc_ctl);
@@ -567,7 +569,39 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   if (a.split && !w->h_pending) {
     if ((e = cudaMallocHost(&w->h_pending, sizeof(uint32_t))) != cudaSuccess) return bail(e, "alloc pinned flag");
   }
+  // the expand pre-read filter (KArgs.mirror): every byte 0xFF ("unknown") at query start
+  a.mirror = nullptr;
+  if (a.split) {
+    const char* mv = getenv("GI_MIRROR");  // investigation: GI_MIRROR=0 pre-reads dist itself
+    if (!mv || atoi(mv) != 0) {
+      if (!w->d_mirror && (e = cudaMalloc(&w->d_mirror, (size_t)g->n)) != cudaSuccess) return bail(e, "alloc mirror");
+      a.mirror = w->d_mirror;
+    }
+  }
+  // investigation (GI_L2_PERSIST=1): dist as a persisting L2 access-policy window on the
+  // query's stream, so that the slot stream cannot evict the wavefront's distances
+  bool l2win = false;
+  if (const char* lp = getenv("GI_L2_PERSIST")) {
+    if (atoi(lp) > 0) {
+      int maxwin = 0, maxpers = 0;
+      cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, g->device);
+      cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, g->device);
+      const size_t bytes = std::min((size_t)total_elems * 4, (size_t)maxwin);
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxpers);
+      cudaStreamAttrValue at = {};
+      at.accessPolicyWindow.base_ptr = d_dist;
+      at.accessPolicyWindow.num_bytes = bytes;
+      at.accessPolicyWindow.hitRatio = std::min(1.0f, (float)maxpers / (float)std::max<size_t>(bytes, 1));
+      at.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      at.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      if (cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &at) == cudaSuccess) l2win = true;
+      static bool said = false;
+      if (!said) { fprintf(stderr, "gi: L2 window %zu B (max window %d, max persisting %d)\n", bytes, maxwin, maxpers); said = true; }
+      cudaGetLastError();
+    }
+  }
   if ((e = cudaEventRecord(w->ev0, st))) return bail(e, "event");
+  if (a.mirror && (e = cudaMemsetAsync(a.mirror, 0xFF, (size_t)g->n, st))) return bail(e, "init mirror");
   if ((e = wide ? v1024::launch_sssp(a, kind, G * ngroups, st) : v512::launch_sssp(a, kind, G * ngroups, st)))
     return bail(e, "launch sssp_persistent");
   int launches = 1;
@@ -615,6 +649,12 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
     }
   }
   if ((e = cudaEventRecord(w->ev1, st))) return bail(e, "event");
+  if (l2win) {
+    cudaStreamAttrValue at = {};
+    at.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &at);
+    cudaCtxResetPersistingL2Cache();
+  }
   QStats* hq = w->h_qstats;
   if ((e = cudaMemcpyAsync(hq, w->d_qstats, sizeof(QStats) * nsrc, cudaMemcpyDeviceToHost, st)))
     return bail(e, "copy stats");

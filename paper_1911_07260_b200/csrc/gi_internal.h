@@ -183,6 +183,10 @@ struct KArgs {
   uint32_t resume;         // this launch resumes a query stopped for an external expand
   unsigned long long split_min;  // list edges from which a phase's expand runs outside
   uint32_t xsplit_min;     // far-pile entries from which an extraction runs outside (0: never)
+  // expand's pre-read filter (split queries): a 1-byte saturated copy of dist, n bytes, small
+  // enough to stay in L2 where dist (4n bytes) does not. Invariant: mirror[v] == 0xFF, or
+  // mirror[v] is a value dist[v] held (so dist[v] <= mirror[v]). nullptr = pre-read dist.
+  uint8_t* mirror;
 };
 
 // k-core (gi_kcore.cu): control block, statistics and arguments.

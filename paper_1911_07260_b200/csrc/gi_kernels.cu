@@ -177,6 +177,9 @@ __device__ __forceinline__ uint64_t pol_evict_first() {
 #ifndef GI_X_DIST_EL
 #define GI_X_DIST_EL 0
 #endif
+#ifndef GI_X_WSKIP
+#define GI_X_WSKIP 0
+#endif
 #ifndef GI_X_EDGE_EF
 #define GI_X_EDGE_EF 0
 #endif
@@ -193,6 +196,42 @@ __device__ __forceinline__ uint32_t ld_dist_tgt(const uint32_t* p) {
   return v;
 #else
   return __ldcg(p);
+#endif
+}
+// the expand filter's mirror bytes (KArgs.mirror): coherent L2 reads, plain byte stores
+__device__ __forceinline__ uint32_t ld_mirror(const uint8_t* p) {
+  uint16_t x;
+  asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(x) : "l"(p));
+  return x;
+}
+__device__ __forceinline__ void st_mirror(uint8_t* p, uint32_t v) {
+  asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "h"((uint16_t)v) : "memory");
+}
+// relaxation atomics on dist (no pre-read) and ELL slot loads, with optional L2 policies
+// (investigation: keep the wavefront's distances in L2 while the slots stream through)
+#ifndef GI_X_ATOM_EL
+#define GI_X_ATOM_EL 0
+#endif
+#ifndef GI_X_SLOT_EF
+#define GI_X_SLOT_EF 0
+#endif
+__device__ __forceinline__ uint32_t atom_min_dist(uint32_t* p, uint32_t v) {
+#if GI_X_ATOM_EL
+  uint32_t old;
+  asm volatile("atom.relaxed.gpu.global.min.L2::cache_hint.u32 %0, [%1], %2, %3;"
+               : "=r"(old) : "l"(p), "r"(v), "l"(pol_evict_last()) : "memory");
+  return old;
+#else
+  return atomicMin(p, v);
+#endif
+}
+__device__ __forceinline__ uint2 ld_slot(const uint2* p) {
+#if GI_X_SLOT_EF
+  uint2 x;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(x.x), "=r"(x.y) : "l"(p), "l"(pol_evict_first()));
+  return x;
+#else
+  return __ldg(p);
 #endif
 }
 // packed edges (w << colbits | col), streamed
@@ -517,6 +556,7 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
       else ok |= 1u << k;
     }
   }
+  TRACE(29);  // the slots have arrived (nd consumed them)
   if (!LD && c.pre_read) {
     // pre-read dist[v]; only an improving candidate is written, with a fire-and-forget
     // red.min, and the pre-read value stands for the atomic's old value. Two threads that
@@ -533,7 +573,7 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
       if (ok & (1u << k)) red_min(c.dist + e[k].x, nd[k]);
   } else {
 #pragma unroll
-    for (int k = 0; k < K; ++k) old[k] = (ok & (1u << k)) ? atomicMin(c.dist + e[k].x, nd[k]) : 0u;
+    for (int k = 0; k < K; ++k) old[k] = (ok & (1u << k)) ? atom_min_dist(c.dist + e[k].x, nd[k]) : 0u;
   }
   // late staleness: the probe of the source vertex (cur, issued with the slot load) was
   // not waited for before the atomics; an entry superseded by a newer one of the same
@@ -549,6 +589,10 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
   // A*: priority bucket of nd + h(v), raised to the current bucket if an inconsistent
   // heuristic would put it below (the monotone max(f + h, g[src]) of SPEC.md:355-358).
   uint32_t curm = 0, farm = 0;
+#ifdef GI_TRACE
+  if (threadIdx.x == 0 && ok) { volatile uint32_t sink_ = old[0]; (void)sink_; }  // wait for the atomic
+#endif
+  TRACE(30);  // the atomics have returned
   uint32_t bk[K];
   if (c.h) {  // uniform branch: SSSP / PPSP never pay for the heuristic
     uint32_t hv[K];
@@ -688,6 +732,10 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
   const uint32_t nitems = nin * 8;
   const uint32_t sub = threadIdx.x & 7;
   for (uint32_t base = 0; base < nitems; base += kBlock * U) {
+    // a warp with no item here (nor in any later pass) goes straight to the CTA barrier:
+    // a sub-round at a chain's tail holds a few vertices, and 15 idle warps stepping through
+    // the predicated-off batch would take the issue slots of the one with work
+    if (GI_X_WSKIP && base + (threadIdx.x & ~31u) >= nitems) break;  // warp-uniform
     uint2 e[U];
     uint32_t du[U], v[U];
     uint32_t have = 0;
@@ -699,7 +747,7 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
       if (item < nitems) {
         const uint2 en = in[item >> 3];
         v[u] = en.x; du[u] = en.y;
-        e[u] = __ldg(c.slots + 8 * (size_t)en.x + sub);
+        e[u] = ld_slot(c.slots + 8 * (size_t)en.x + sub);
         have |= 1u << u;
       }
     }
@@ -2289,7 +2337,15 @@ __device__ __forceinline__ void xflush(const int32_t* seg, uint32_t n, uint32_t*
 // The list entries carry GLOBAL start positions here (xpre + S, added by the persistent
 // kernel before it stopped): lane k of a window holds entry jb+k's end relative to the warp's
 // range start, beg - start, and du.
-template <bool PACKED>
+//
+// MIRROR (KArgs.mirror): the pre-read is the vertex's byte in the mirror (n bytes, L2-resident)
+// instead of dist[v] (4n bytes, twice the L2 on config 4, so most pre-reads went to DRAM). A
+// candidate passes when it could improve (nd < mirror[v], or the byte is 0xFF: unknown); a
+// passing candidate takes atomicMin, whose old value decides the push exactly as the
+// pre-read did (R11 without the race: the improving thread knows it improved). The byte is
+// then set to the new distance, or tightened to the old one: both are values dist[v] held,
+// so the invariant dist[v] <= mirror[v] survives racing byte stores.
+template <bool PACKED, bool MIRROR>
 __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
   extern __shared__ __align__(16) unsigned char x_dyn[];
   XShared& xs = *reinterpret_cast<XShared*>(x_dyn);
@@ -2413,20 +2469,48 @@ __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
           wt[k] = e.y;
         }
       }
+      if constexpr (MIRROR) {
+        // mirror bytes first (L2 hits), then atomicMin for the candidates that pass; the
+        // others take no dist access at all
+        uint32_t mb[kXRows];
 #pragma unroll
-      for (int k = 0; k < kXRows; ++k) old[k] = (valid >> k) & 1u ? ld_dist_tgt(dist + v[k]) : 0u;
+        for (int k = 0; k < kXRows; ++k) mb[k] = (valid >> k) & 1u ? ld_mirror(a.mirror + v[k]) : 0u;
+#pragma unroll
+        for (int k = 0; k < kXRows; ++k) {
+          const uint32_t nd = du[k] + wt[k];
+          const bool ovf = nd < du[k] || nd == kInf;
+          const bool pass = ((valid >> k) & 1u) && !ovf && (mb[k] == 0xFFu || nd < mb[k]);
+          old[k] = pass ? atomicMin(dist + v[k], nd) : 0u;
+          if (!pass) valid &= ~(((valid >> k) & 1u && !ovf) ? 1u << k : 0u);  // filtered: done
+        }
+#pragma unroll
+        for (int k = 0; k < kXRows; ++k) {
+          if (!((valid >> k) & 1u)) continue;
+          const uint32_t nd = du[k] + wt[k];
+          if (nd < du[k] || nd == kInf) continue;
+          if (nd < old[k]) {
+            if (nd < 0xFFu) st_mirror(a.mirror + v[k], nd);
+          } else {
+            if (old[k] < mb[k]) st_mirror(a.mirror + v[k], old[k]);  // tighten (old < 0xFF)
+            valid &= ~(1u << k);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < kXRows; ++k) old[k] = (valid >> k) & 1u ? ld_dist_tgt(dist + v[k]) : 0u;
+      }
 #pragma unroll
       for (int k = 0; k < kXRows; ++k) {
         const uint32_t nd = du[k] + wt[k];
         const bool ovf = nd < du[k] || nd == kInf;
-        if (((valid >> k) & 1u) && (ovf || nd < old[k])) {
+        if (((valid >> k) & 1u) && (ovf || MIRROR || nd < old[k])) {
           const XPtrs& ps = xs.ps;
           if (ovf) {  // inline: no call in this loop
             atomicOr(&ps.ovfbits[v[k] >> 5], 1u << (v[k] & 31));
             atomicOr(ps.ovf_cand, 1u);
             continue;
           }
-          red_min(dist + v[k], nd);
+          if constexpr (!MIRROR) red_min(dist + v[k], nd);
           const uint32_t bk = ps.h ? max(prio_bucket(nd, __ldg(ps.h + v[k]), ps.div), ps.bcur) : fdiv(nd, ps.div);
           // staged per warp; a full segment (at most one iteration past half) takes the
           // lane's own dedup push to the global list
@@ -2743,7 +2827,8 @@ cudaError_t query_clusters(int kind, int cluster, int* max_clusters) {
 
 #if GI_BLOCK >= 1024
 cudaError_t launch_expand(const KArgs& a, cudaStream_t st, int* grid_used) {
-  const void* fn = a.pedges ? (const void*)expand_kernel<true> : (const void*)expand_kernel<false>;
+  const void* fn = a.pedges ? (a.mirror ? (const void*)expand_kernel<true, true> : (const void*)expand_kernel<true, false>)
+                            : (a.mirror ? (const void*)expand_kernel<false, true> : (const void*)expand_kernel<false, false>);
   const int smem = (int)sizeof(XShared);
   int dev = 0, sms = 0, bps = 0;
   cudaError_t e = cudaGetDevice(&dev);

@@ -472,6 +472,34 @@ def test_expand_split_segments(gi, monkeypatch):
         assert gi.ppsp(G, s, tgt, 3, expand="on")[0] == int(ref[tgt]), t
 
 
+def test_expand_mirror_filter(gi, monkeypatch):
+    """expand_kernel's pre-read filter (KArgs.mirror, a 1-byte saturated copy of dist):
+    distances that straddle the byte's range (some below 255, some above, 0xFF = unknown),
+    zero-weight edges, and the mirror switched off (GI_MIRROR=0) — all equal to the oracle."""
+    monkeypatch.setenv("GI_SPLIT_MIN", "1")
+    rng = np.random.default_rng(53)
+    for t, wmax in enumerate((30, 200, 3000)):
+        n = int(rng.integers(5_000, 30_000))
+        deg = np.minimum(rng.zipf(1.7, size=n), n - 1)
+        deg[rng.integers(0, n, 3)] = rng.integers(1_000, max(1_001, n // 4), 3)
+        edges = [(u, int(v), int(w)) for u in range(n) for v, w in
+                 zip(rng.integers(0, n, deg[u]), rng.integers(0 if t == 0 else 1, wmax, deg[u]))]
+        g = gen.from_edges(n, edges)
+        G = gi.Graph.from_csr(g)
+        s = int(np.argmax(deg))
+        ref, _ = oracle.dijkstra(g, s)
+        fin = ref[ref != 0xFFFFFFFF]
+        if t == 2:  # distances on both sides of the byte's range
+            assert (fin < 255).sum() > 1 and fin.max() >= 255, (int(fin.min()), int(fin.max()))
+        for mv in ("1", "0"):
+            monkeypatch.setenv("GI_MIRROR", mv)
+            for o, delta in ((dict(expand="on"), 1), (dict(expand="on"), 7), (dict(expand="on", fusion=False), 3)):
+                d, st = run(gi, G, s, delta, **o)
+                assert np.array_equal(d, ref), (t, mv, o, delta)
+                assert st["buckets"] == oracle.bucket_count(ref, delta), (t, mv, o, delta)
+    monkeypatch.delenv("GI_MIRROR")
+
+
 def test_extract_split_segments(gi, monkeypatch, config_graph):
     """Split extraction (single queries on skewed graphs with expand): an EXTRACT phase whose
     far pile holds >= GI_XSPLIT_MIN entries stops the persistent kernel (KState, pending 2);

@@ -61,6 +61,48 @@ __global__ void __launch_bounds__(1024) gather_ranges(const uint32_t* __restrict
   if (acc == 0x12345678u) sink[0] = acc;
 }
 
+// mirror variants: a 1-byte (MODE 8) or 2-byte (MODE 16) saturated copy of dist per vertex,
+// i.e. a 67 MB / 134 MB array instead of the 268 MB one
+template <typename T, int U>
+__global__ void __launch_bounds__(1024) gather_mirror(const uint32_t* __restrict__ cols, int64_t m, const T* mir, uint32_t* sink) {
+  uint32_t acc = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < m; i += U * stride) {
+    uint32_t c[U], d[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = __ldcs(cols + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) d[u] = __ldcg(mir + c[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += d[u];
+  }
+  for (; i < m; i += stride) acc += __ldcg(mir + cols[i]);
+  if (acc == 0x12345678u) sink[0] = acc;
+}
+
+// relaxation without a pre-read: red.min of a candidate on every edge (MODE 20), or
+// atomicMin with its old value consumed (MODE 21)
+template <int MODE, int U>
+__global__ void __launch_bounds__(1024) red_all(const uint32_t* __restrict__ cols, int64_t m, uint32_t* dist, uint32_t* sink) {
+  uint32_t acc = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < m; i += U * stride) {
+    uint32_t c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = __ldcs(cols + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t nd = 1000u - (c[u] & 511u);
+      if (MODE == 20) asm volatile("red.global.min.u32 [%0], %1;" :: "l"(dist + c[u]), "r"(nd) : "memory");
+      else acc += atomicMin(dist + c[u], nd);
+    }
+  }
+  for (; i < m; i += stride) atomicMin(dist + cols[i], 7u);
+  if (acc == 0x12345678u) sink[0] = acc;
+}
+
 extern "C" int probe_gather(int mode, const uint32_t* cols, int64_t m, const uint32_t* dist, uint32_t* sink,
                             int blocks, int threads, cudaStream_t st) {
   switch (mode) {
@@ -74,6 +116,12 @@ extern "C" int probe_gather(int mode, const uint32_t* cols, int64_t m, const uin
     case 8: gather_ranges<1, 8><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
     case 9: gather_ranges<2, 4><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
     case 10: gather_ranges<2, 8><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
+    case 11: gather_mirror<uint8_t, 8><<<blocks, threads, 0, st>>>(cols, m, (const uint8_t*)dist, sink); break;
+    case 12: gather_mirror<uint16_t, 8><<<blocks, threads, 0, st>>>(cols, m, (const uint16_t*)dist, sink); break;
+    case 13: gather_mirror<uint8_t, 16><<<blocks, threads, 0, st>>>(cols, m, (const uint8_t*)dist, sink); break;
+    case 20: red_all<20, 8><<<blocks, threads, 0, st>>>(cols, m, (uint32_t*)dist, sink); break;
+    case 21: red_all<21, 8><<<blocks, threads, 0, st>>>(cols, m, (uint32_t*)dist, sink); break;
+    case 22: red_all<20, 4><<<blocks, threads, 0, st>>>(cols, m, (uint32_t*)dist, sink); break;
     default: gather<3, 8><<<blocks, threads, 0, st>>>(cols, m, dist, sink); break;
   }
   return (int)cudaGetLastError();

@@ -86,7 +86,8 @@ clk = 1.965e3  # cycles per µs at the max SM clock
 names = {0: "bsp drain loop top", 2: "slot load", 3: "relax", 4: "rest", 5: "decision", 6: "feed (async) / extract",
          7: "phase work end", 8: "far flush + fmin", 9: "group barrier", 11: "drain (async, CTA 0)",
          12: "stage B scan", 13: "stage B edge loop", 14: "ROUND claim+staging", 15: "hub slices (after B)",
-         16: "B iter: search + edge-load issue", 17: "B iter: relax_batch (waits)", 18: "expand relax tail", 19: "expand: collection barrier", 20: "expand: scan + barrier + S", 21: "expand it: pre-read issue + next map/load", 22: "expand it: consume (waits pre-reads) + pushes", 23: "expand it: far flush", 24: "E1 collect (reserve + copy)", 25: "ROUND next claim", 26: "EXTRACT chunk loads + classify", 27: "EXTRACT keep append", 28: "EXTRACT bins + frontier append"}
+         16: "B iter: search + edge-load issue", 17: "B iter: relax_batch (waits)", 18: "expand relax tail", 19: "expand: collection barrier", 20: "expand: scan + barrier + S", 21: "expand it: pre-read issue + next map/load", 22: "expand it: consume (waits pre-reads) + pushes", 23: "expand it: far flush", 24: "E1 collect (reserve + copy)", 25: "ROUND next claim", 26: "EXTRACT chunk loads + classify", 27: "EXTRACT keep append", 28: "EXTRACT bins + frontier append",
+         29: "relax: slot wait (in relax)", 30: "relax: atomic wait"}
 tot = 0
 for k in range(32):
     c = int(buf[32 + k])
