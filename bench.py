@@ -350,7 +350,7 @@ def run_single(args, gi, torch, rank, world, local):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic,
                 "kernel": "sssp_persistent" if launches == 1 else
-                          f"sssp_persistent segments + expand_kernel ({launches} launches per query)",
+                          f"sssp_persistent segments + expand_kernel + extract_kernel ({launches} launches per query)",
                 "kernel_ms": kms,
                 "bytes_alg_per_launch": bytes_alg, "peak_source": peak_src,
                 "bytes_alg_formula": "12*m_r + 16*n_r + 4*n (SURVEY §8(d))",

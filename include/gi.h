@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GI_VERSION 200 /* 2.0.0: gi_options.expand / lazy, gi_probe_floors */
+#define GI_VERSION 201 /* 2.0.1: gi_options.window (2.0.0: expand / lazy, gi_probe_floors) */
 
 typedef struct gi_graph gi_graph; /* opaque; owns device copies of the CSR */
 
@@ -130,6 +130,14 @@ typedef struct {
                                 thread-block cluster per group of group_ctas CTAs (default 8,
                                 at most 16; hardware cluster barrier), 3 = grid (group barrier of
                                 global atomics over every co-resident CTA, or group_ctas of them) */
+  int32_t window;            /* materialized buckets ("only materialize a fixed
+                                number of buckets, and store the rest of the vertices in an overflow
+                                bucket"; Julienne's open window) for queries running with expand:
+                                far-pile entries whose bucket lies >= `window` buckets past the
+                                window start wait in an overflow (later) pile that is rescanned only
+                                when the window's buckets are done. 0 = off (default: every far
+                                entry is recomputed at every extraction), else the
+                                window width in buckets; ignored without expand */
 } gi_options;
 
 /* Counters of one query (SURVEY §8(a) "Counter definitions"). */

@@ -204,6 +204,8 @@ gi_status ws_prepare(gi_graph* g, Workspace* w, int k, int nsrc) {
       if ((s = dmalloc(&gw.hub[1], (size_t)w->hubcap, &w->allocs, "alloc hub list"))) return s;
       gw.xpre = nullptr;
       gw.xtot = nullptr;
+      gw.laterbits = nullptr;  // the bucket window's later pile: allocated on first use
+      gw.later[0] = gw.later[1] = nullptr;
       if ((s = dmalloc(&gw.kst, 1, &w->allocs, "alloc expand state"))) return s;
       GI_CUDA(cudaMemsetAsync(gw.kst, 0, sizeof(KState), w->stream), "memset");
       if (g->max_deg > 32) {  // expand (skewed graphs)
@@ -327,6 +329,7 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   if (opt.rung < 0 || opt.rung > 3) return fail(GI_ERR_INVALID_ARGUMENT, "rung must be 0 (auto), 1 (cta), 2 (cluster) or 3 (grid)");
   if (opt.rung == 2 && (opt.group_ctas < 0 || opt.group_ctas > 16))
     return fail(GI_ERR_INVALID_ARGUMENT, "a cluster group has at most 16 CTAs");
+  if (opt.window < 0) return fail(GI_ERR_INVALID_ARGUMENT, "window must be >= 0 (0 = off)");
   if (opt.lazy && opt.fusion) return fail(GI_ERR_INVALID_ARGUMENT, "the lazy schedule runs without fusion (fusion = 0)");
   if (heur && fused && opt.drain == 2) return fail(GI_ERR_UNSUPPORTED, "A* runs with the bsp drain (drain 0/1)");
   if (fused && opt.drain == 2 && g->max_deg > kAsyncMaxDeg)
@@ -568,6 +571,26 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
 
   if (a.split && !w->h_pending) {
     if ((e = cudaMallocHost(&w->h_pending, sizeof(uint32_t))) != cudaSuccess) return bail(e, "alloc pinned flag");
+  }
+  // bucket window (split queries): far entries beyond the open window wait in a later pile
+  a.window = 0;
+  if (a.split) {
+    const char* wv = getenv("GI_WINDOW");  // investigation override (buckets; 0 = off)
+    a.window = wv ? (uint32_t)strtoul(wv, nullptr, 10) : opt.window ? (uint32_t)opt.window : (uint32_t)kDefaultWindow;
+    GroupWs& g0 = w->h_groups[0];
+    if (a.window && !g0.laterbits) {
+      const size_t nwords = (size_t)((g->n + 31) / 32);
+      gi_status s2;
+      if ((s2 = dmalloc(&g0.laterbits, nwords, &w->allocs, "alloc laterbits")) ||
+          (s2 = dmalloc(&g0.later[0], (size_t)g->n, &w->allocs, "alloc later pile")) ||
+          (s2 = dmalloc(&g0.later[1], (size_t)g->n, &w->allocs, "alloc later pile"))) {
+        g0.laterbits = nullptr;
+        return s2;
+      }
+      if ((e = cudaMemsetAsync(g0.laterbits, 0, nwords * 4, st)) ||
+          (e = cudaMemcpyAsync(w->d_groups, &g0, sizeof(GroupWs), cudaMemcpyHostToDevice, st)))
+        return bail(e, "init later pile");
+    }
   }
   // the expand pre-read filter (KArgs.mirror): every byte 0xFF ("unknown") at query start
   a.mirror = nullptr;

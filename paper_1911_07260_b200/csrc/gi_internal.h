@@ -24,6 +24,7 @@ constexpr int kBinCap = kBinCapW[GI_BLOCK >= 1024 ? 1 : 0];
 constexpr int kBigCap = 2048;        // CTA-local list of high-degree vertices (deg > 8) per bin
 constexpr uint32_t kDefaultT = 1024; // fusion threshold default (vertices per CTA bin), max out-degree <= 32
 constexpr uint32_t kDefaultTSkewed = 256;  // ... and on skewed graphs (max out-degree > 32); DESIGN.md §10
+constexpr uint32_t kDefaultWindow = 0;  // bucket window width (buckets) of split queries: off (measured slower)
 constexpr int kSlotEdges = 8;        // ELL slot: up to 8 {col, w} edges inline (64 B per vertex)
 constexpr uint32_t kColEmpty = 0xFFFFFFFFu;  // unused slot entry
 constexpr uint32_t kColBig = 0xFFFFFFFEu;    // deg > 8: all 8 entries {kColBig, payload}; payloads deg, beg_lo, beg_hi
@@ -91,7 +92,8 @@ struct alignas(128) Ctl {
   uint32_t qclaim[3];   // ROUND phases: next unclaimed global-frontier position, by phase mod 3
   uint32_t tdist[3];    // PPSP: min over CTAs of dist[target] read at the phase end, by phase mod 3
   int32_t next_si;      // batch: the source index this group runs next (claimed by its CTA 0)
-  uint32_t pad0[6];
+  uint32_t lcount[3];   // bucket window: later-pile sizes, by window advance mod 3
+  uint32_t lmin[3];     // bucket window: lower bound of the later pile's buckets, by advance mod 3
   uint32_t bar;         // group barrier: arrivals (low 16 bits) | generation (high 16), own 128 B line
   uint32_t pad1[31];
 };
@@ -116,6 +118,11 @@ struct GroupWs {
   unsigned long long* xtot;  // [kMaxGroupCtas] expand: edge total of each CTA's slice of the list
   struct KState* kst;        // split expand: the phase loop's state while the relaxation runs outside
   Ctl* ctl;
+  // bucket window (KArgs.window; single split queries): far-pile entries whose bucket lies
+  // beyond the open window wait in the later pile (one entry per vertex, laterbits) and are
+  // rescanned only when the window advances, not at every extraction
+  uint32_t* laterbits;  // [nwords] "in the later pile" dedup bits; nullptr = no window
+  int32_t* later[2];    // [n] later pile, double-buffered across window advances
 };
 
 // Split expand (single queries on skewed graphs): when a ROUND phase's group list holds at
@@ -131,6 +138,7 @@ struct KState {
   uint32_t pending;             // 1 = the kernel stopped for an external expand of phase p,
                                 // 2 = for an external extraction of phase p (extract_kernel)
   uint32_t rkind;               // what the resumed segment continues after (1 expand, 2 extract)
+  uint32_t t, wend;             // bucket window: advances so far, end of the open window
 };
 
 constexpr int kMaxGroupCtas = 1024;  // expand: largest group (CTAs) the slice totals are sized for
@@ -187,6 +195,8 @@ struct KArgs {
   // enough to stay in L2 where dist (4n bytes) does not. Invariant: mirror[v] == 0xFF, or
   // mirror[v] is a value dist[v] held (so dist[v] <= mirror[v]). nullptr = pre-read dist.
   uint8_t* mirror;
+  uint32_t window;         // bucket window width in buckets (0 = off: every far entry is
+                           // rescanned at every extraction); needs GroupWs.laterbits
 };
 
 // k-core (gi_kcore.cu): control block, statistics and arguments.

@@ -56,7 +56,7 @@ namespace cg = cooperative_groups;
 namespace gi {
 namespace {
 
-enum : uint32_t { MODE_ROUND = 0, MODE_EXTRACT = 1, MODE_DONE = 2, MODE_NONE = 3, MODE_STOP = 4 };
+enum : uint32_t { MODE_ROUND = 0, MODE_EXTRACT = 1, MODE_DONE = 2, MODE_NONE = 3, MODE_STOP = 4, MODE_ADVANCE = 5 };
 #ifndef GI_XTR
 #define GI_XTR 4
 #endif
@@ -213,7 +213,7 @@ __device__ __forceinline__ void st_mirror(uint8_t* p, uint32_t v) {
 #define GI_X_ATOM_EL 0
 #endif
 #ifndef GI_X_SLOT_EF
-#define GI_X_SLOT_EF 0
+#define GI_X_SLOT_EF 1
 #endif
 __device__ __forceinline__ uint32_t atom_min_dist(uint32_t* p, uint32_t v) {
 #if GI_X_ATOM_EL
@@ -333,6 +333,8 @@ struct Shared {
   uint32_t maxdep;          // max depth (sub-round equivalent) processed this phase
   uint32_t spilled;         // some push overflowed the ring threshold this phase
   uint32_t xhn;             // expand: entries of the group list after collection
+  uint32_t wend, ws;        // bucket window: end of the open window, start of a new one (ADVANCE)
+  uint32_t lcnt;            // bucket window: later-pile entries (PPSP stop cleanup)
   unsigned long long xS[kMaxGroupCtas + 1];  // expand: exclusive prefix of the CTA slice totals
 };
 
@@ -1633,6 +1635,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
       for (int k = 0; k < 3; ++k) {
         ctl->qcount[k] = 0; ctl->fcount[k] = 0; ctl->fmin[k] = kInf; ctl->xlive[k] = 0; ctl->maxsub[k] = 0;
         ctl->hcount[k] = 0; ctl->qclaim[k] = 0; ctl->tdist[k] = kInf;
+        ctl->lcount[k] = 0; ctl->lmin[k] = kInf;
       }
       ctl->fcount[0] = 1; ctl->fmin[0] = 0; ctl->ovf_cand = 0;
       ws.far[0][0] = src;
@@ -1667,6 +1670,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
     unsigned long long phases = 0, rounds = 0, buckets = 0, empty = 0, critical = 0;  // rank 0, thread 0
     unsigned long long sub_at_phase_start = 0;
     uint32_t p = 0, j = 0, b = 0, prev = MODE_NONE;
+    // bucket window (a.window buckets; off: wend = inf): t = advances so far, the later pile
+    // of advance t is later[t & 1] with counters lcount / lmin [t % 3]
+    uint32_t t = 0, wend = (XP && a.window) ? a.window : kInf;  // constants outside the XP kernels
     uint32_t last_b = kInf;  // bucket of the last extraction with live vertices (rank 0, thread 0)
     bool mid = false;  // resuming inside phase p, after its external expand / extraction
     bool xmid = false;  // ... after its external extraction: phase p was an EXTRACT phase
@@ -1674,6 +1680,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
     if (resuming) {
       const KState* ks = ws.kst;
       p = ks->p; j = ks->j; b = ks->b; prev = ks->prev; last_b = ks->last_b;
+      t = ks->t; wend = ks->wend;
       xmid = ks->rkind == 2;
       if (rank == 0 && tid == 0) {
         phases = ks->phases; rounds = ks->rounds; buckets = ks->buckets; empty = ks->empty; critical = ks->critical;
@@ -1709,6 +1716,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           ks->p = p; ks->j = j; ks->b = b; ks->prev = prev; ks->last_b = last_b;
           ks->phases = phases; ks->rounds = rounds; ks->buckets = buckets; ks->empty = empty;
           ks->critical = critical; ks->E = E; ks->xn = xn; ks->rkind = kind;
+          ks->t = t; ks->wend = wend;
           __threadfence();
           ks->pending = kind;
         }
@@ -1717,7 +1725,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
     };
     for (;;) {
       if (mid && tid == 0) {  // phase p continues: its list was relaxed outside, the bins are empty
-        s.mode = MODE_ROUND; s.cnt = 0; s.hn = 0;
+        s.mode = MODE_ROUND; s.cnt = 0; s.hn = 0; s.wend = wend;
         s.cnt3[0] = 0; s.cnt3[1] = 0; s.bigtail = 0; s.farcnt = 0;
         for (int w = 0; w < kBlock / 32; ++w) s.wfar[w] = 0;
         s.fmin = kInf;
@@ -1739,9 +1747,23 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
         }
         uint32_t mode;
         s.hn = min(hn, a.hubcap);
+        // bucket window: extract while the far pile's next bucket lies inside the window
+        // [ws, wend); else advance it (rescan the later pile) or, with nothing waiting
+        // there, move it to the far pile's next bucket without a phase
+        const uint32_t lc = (XP && a.window) ? __ldcg(&ctl->lcount[t % 3]) : 0u;
+        s.lcnt = lc;
         if (qn > 0 || hn > 0) { mode = MODE_ROUND; s.cnt = qn; }
-        else if (fc > 0) { mode = MODE_EXTRACT; s.cnt = fc; s.b = fm; }
-        else mode = MODE_DONE;
+        else if (fc > 0 && fm < wend) { mode = MODE_EXTRACT; s.cnt = fc; s.b = fm; }
+        else if (XP && lc > 0) {
+          const uint32_t lm = __ldcg(&ctl->lmin[t % 3]);
+          const uint32_t ws0 = min(fc > 0 ? fm : kInf, lm);
+          mode = MODE_ADVANCE; s.cnt = lc; s.ws = ws0;
+          wend = ws0 >= kInf - a.window ? kInf : ws0 + a.window;
+        } else if (XP && fc > 0) {
+          mode = MODE_EXTRACT; s.cnt = fc; s.b = fm;
+          wend = fm >= kInf - a.window ? kInf : fm + a.window;
+        } else mode = MODE_DONE;
+        s.wend = wend;
         // PPSP: entering bucket i with iΔ >= the best distance found
         // to the target ends the query — every vertex below iΔ is settled. The snapshot
         // of dist[target] is a slot every CTA wrote before the barrier (identical
@@ -1784,10 +1806,21 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           const int32_t v = pile[i];
           if (v >= 0) atomicAnd(&ws.farbits[v >> 5], ~(1u << (v & 31)));  // < 0: an expand chunk's hole
         }
+        if (XP && ws.laterbits) {  // ... and the later pile's
+          const int32_t* lp = ws.later[t & 1];
+          const uint32_t lc = s.lcnt;
+          const uint32_t lo3 = (uint32_t)(((uint64_t)lc * rank) / G), hi3 = (uint32_t)(((uint64_t)lc * (rank + 1)) / G);
+          for (uint32_t i = lo3 + tid; i < hi3; i += kBlock) {
+            const int32_t v = lp[i];
+            atomicAnd(&ws.laterbits[v >> 5], ~(1u << (v & 31)));
+          }
+        }
         break;
       }
       const uint32_t cnt = s.cnt;
+      if constexpr (XP) wend = s.wend;
       if (mode == MODE_EXTRACT) { ++j; b = s.b; }
+      if (XP && mode == MODE_ADVANCE) ++t;
       if (rank == 0 && tid == 0 && !mid) {
         ctl->qcount[(p + 2) % 3] = 0;
         ctl->maxsub[(p + 2) % 3] = 0;
@@ -1796,6 +1829,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
         ctl->tdist[(p + 1) % 3] = kInf;  // written at the end of phase p+1
         if (mode == MODE_EXTRACT) {
           ctl->fcount[(j + 1) % 3] = 0; ctl->fmin[(j + 1) % 3] = kInf; ctl->xlive[(j + 1) % 3] = 0;
+        }
+        if (XP && mode == MODE_ADVANCE) {  // the later pile of advance t+1 (last read by advance t-1)
+          ctl->lcount[(t + 1) % 3] = 0; ctl->lmin[(t + 1) % 3] = kInf;
         }
         if (mode == MODE_ROUND) ++rounds;
       }
@@ -1856,6 +1892,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
         // per chunk (warp scan), not one per warp per entry.
         const int32_t* far_src = (j & 1) ? ws.far[0] : ws.far[1];
         uint32_t nlive = 0;
+        uint32_t my_lmin = kInf;  // bucket window: min bucket sent to the later pile
         // a big pile (every CTA iterates many chunks): CTA-aggregated appends (cta_append)
         const bool agg = cnt >= 2u * G * kXtr * kBlock;
         for (uint32_t base = lo; base < hi; base += kXtr * kBlock) {
@@ -1870,6 +1907,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           for (int x = 0; x < kXtr; ++x) d[x] = v[x] >= 0 ? ld_dist(dist + v[x]) : kInf;
           uint32_t keepm = 0;
           uint32_t livem = 0;
+          uint32_t latm = 0;  // beyond the window and new to the later pile
 #pragma unroll
           for (int x = 0; x < kXtr; ++x) {
             if (v[x] < 0) continue;
@@ -1877,6 +1915,11 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
             if (bk <= b) {
               atomicAnd(&ws.farbits[v[x] >> 5], ~(1u << (v[x] & 31)));
               if (bk == b) { ++nlive; livem |= 1u << x; }  // else: stale (already settled)
+            } else if (XP && bk >= wend) {  // (window off: wend = inf, never; XP kernels only)
+              atomicAnd(&ws.farbits[v[x] >> 5], ~(1u << (v[x] & 31)));
+              my_lmin = min(my_lmin, bk);
+              const uint32_t bit = 1u << (v[x] & 31);
+              if (!(atomicOr(&ws.laterbits[v[x] >> 5], bit) & bit)) latm |= 1u << x;
             } else {
               c.my_fmin = min(c.my_fmin, bk);
               keepm |= 1u << x;
@@ -1885,6 +1928,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           TRACE(26);
           if (agg) cta_append(keepm, v, c.far_live, c.fcount_live, s.redw, nullptr);
           else warp_append(keepm, v, c.far_live, c.fcount_live, nullptr);
+          if (XP && wend != kInf) {  // CTA-uniform
+            if (agg) cta_append(latm, v, ws.later[t & 1], &ctl->lcount[t % 3], s.redw, nullptr);
+            else warp_append(latm, v, ws.later[t & 1], &ctl->lcount[t % 3], nullptr);
+          }
           TRACE(27);
           // the extracted vertices: the CTA bin (fusion) while it has room, else — and
           // without fusion — the global frontier, deduplicated with all atomics in flight
@@ -1924,11 +1971,62 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           TRACE(28);
         }
         TRACE(6);
+        if (XP && wend != kInf) {
+          const uint32_t lm = __reduce_min_sync(0xffffffffu, my_lmin);
+          if ((tid & 31) == 0 && lm != kInf) atomicMin(&ctl->lmin[t % 3], lm);
+        }
         const uint32_t tl = block_sum(nlive, s);  // ends with a barrier: ring fill is final
         if (tid == 0) {
           if (tl) atomicAdd(&ctl->xlive[j % 3], tl);
           scanned += hi - lo;
         }
+      } else if (XP && mode == MODE_ADVANCE) {
+        // bucket window advance (only expand queries, hence the XP kernels, open a window):
+        // the later pile of advance t-1 is partitioned against the new window [ws, wend):
+        // settled entries dropped, entries inside the window moved to the far pile (the next
+        // extraction's), the rest kept in the later pile of advance t
+        const int32_t* lsrc = ws.later[(t - 1) & 1];
+        const uint32_t ws0 = s.ws;
+        uint32_t my_lmin = kInf;
+        const bool agg = cnt >= 2u * G * kXtr * kBlock;
+        for (uint32_t base = lo; base < hi; base += kXtr * kBlock) {
+          int32_t v[kXtr];
+          uint32_t d[kXtr];
+#pragma unroll
+          for (int x = 0; x < kXtr; ++x) {
+            const uint32_t i = base + x * kBlock + tid;
+            v[x] = i < hi ? lsrc[i] : -1;
+          }
+#pragma unroll
+          for (int x = 0; x < kXtr; ++x) d[x] = v[x] >= 0 ? ld_dist(dist + v[x]) : kInf;
+          uint32_t keepm = 0, movem = 0;
+#pragma unroll
+          for (int x = 0; x < kXtr; ++x) {
+            if (v[x] < 0) continue;
+            const uint32_t bk = prio_bucket(d[x], c.h ? __ldg(c.h + v[x]) : 0u, c.div);
+            const uint32_t bit = 1u << (v[x] & 31);
+            if (bk >= wend) {
+              my_lmin = min(my_lmin, bk);
+              keepm |= 1u << x;
+              continue;
+            }
+            atomicAnd(&ws.laterbits[v[x] >> 5], ~bit);
+            if (bk >= ws0 && !(atomicOr(&ws.farbits[v[x] >> 5], bit) & bit)) {  // else settled,
+              c.my_fmin = min(c.my_fmin, bk);                                  // or in the pile
+              movem |= 1u << x;
+            }
+          }
+          if (agg) {
+            cta_append(keepm, v, ws.later[t & 1], &ctl->lcount[t % 3], s.redw, nullptr);
+            cta_append(movem, v, c.far_live, c.fcount_live, s.redw, nullptr);
+          } else {
+            warp_append(keepm, v, ws.later[t & 1], &ctl->lcount[t % 3], nullptr);
+            warp_append(movem, v, c.far_live, c.fcount_live, nullptr);
+          }
+        }
+        const uint32_t lm = __reduce_min_sync(0xffffffffu, my_lmin);
+        if ((tid & 31) == 0 && lm != kInf) atomicMin(&ctl->lmin[t % 3], lm);
+        if (tid == 0) scanned += hi - lo;
       } else if (!mid) {
         const uint32_t hn = s.hn;
         HubEnt* hub_in = (p & 1) ? ws.hub[1] : ws.hub[0];
@@ -2555,20 +2653,24 @@ constexpr int kEPer = 8;
 constexpr uint32_t kETile = kEBlock * kEPer;
 
 __global__ void __launch_bounds__(kEBlock) extract_kernel(KArgs a) {
-  __shared__ uint32_t s_keep[kEBlock / 32], s_live[kEBlock / 32];
-  __shared__ uint32_t s_fmin, s_nlive;
+  __shared__ uint32_t s_keep[kEBlock / 32], s_live[kEBlock / 32], s_lat[kEBlock / 32];
+  __shared__ uint32_t s_fmin, s_nlive, s_lmin;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const GroupWs& ws = a.groups[0];
   const KState* ks = ws.kst;
   const uint32_t p = ks->p, j = ks->j, b = ks->b, cnt = ks->xn;
+  // bucket window: entries of buckets >= wend go to the later pile of advance t
+  const uint32_t wend = ks->wend, t = ks->t;
+  int32_t* later = ws.laterbits ? ws.later[t & 1] : nullptr;
+  uint32_t* lcount = &ws.ctl->lcount[t % 3];
   const int32_t* far_src = (j & 1) ? ws.far[0] : ws.far[1];
   int32_t* far_live = (j & 1) ? ws.far[1] : ws.far[0];
   uint32_t* fcount_live = &ws.ctl->fcount[j % 3];
   int32_t* q_next = (p & 1) ? ws.q[0] : ws.q[1];
   uint32_t* qcount_next = &ws.ctl->qcount[(p + 1) % 3];
   const uint32_t* dist = a.dist;
-  if (tid == 0) { s_fmin = kInf; s_nlive = 0; }
-  uint32_t my_fmin = kInf;
+  if (tid == 0) { s_fmin = kInf; s_nlive = 0; s_lmin = kInf; }
+  uint32_t my_fmin = kInf, my_lmin = kInf;
   for (uint32_t t0 = blockIdx.x * kETile; t0 < cnt; t0 += gridDim.x * kETile) {
     int32_t v[kEPer];
     uint32_t d[kEPer], hv[kEPer];
@@ -2581,7 +2683,7 @@ __global__ void __launch_bounds__(kEBlock) extract_kernel(KArgs a) {
     for (int x = 0; x < kEPer; ++x) d[x] = v[x] >= 0 ? ld_dist(dist + v[x]) : kInf;
 #pragma unroll
     for (int x = 0; x < kEPer; ++x) hv[x] = (a.h && v[x] >= 0) ? __ldg(a.h + v[x]) : 0u;
-    uint32_t keepm = 0, livem = 0;
+    uint32_t keepm = 0, livem = 0, latm = 0;
 #pragma unroll
     for (int x = 0; x < kEPer; ++x) {
       if (v[x] < 0) continue;
@@ -2589,45 +2691,57 @@ __global__ void __launch_bounds__(kEBlock) extract_kernel(KArgs a) {
       if (bk <= b) {
         atomicAnd(&ws.farbits[v[x] >> 5], ~(1u << (v[x] & 31)));
         if (bk == b) livem |= 1u << x;  // else: stale (already settled)
+      } else if (bk >= wend) {  // beyond the window (off: wend = inf, never)
+        atomicAnd(&ws.farbits[v[x] >> 5], ~(1u << (v[x] & 31)));
+        my_lmin = min(my_lmin, bk);
+        const uint32_t bit = 1u << (v[x] & 31);
+        if (!(atomicOr(&ws.laterbits[v[x] >> 5], bit) & bit)) latm |= 1u << x;
       } else {
         my_fmin = min(my_fmin, bk);
         keepm |= 1u << x;
       }
     }
     // per-warp counts, one reservation per list per tile
-    uint32_t km[kEPer], lm[kEPer], kpre[kEPer], lpre[kEPer], kt = 0, lt = 0;
+    uint32_t km[kEPer], lm[kEPer], am[kEPer], kpre[kEPer], lpre[kEPer], apre[kEPer], kt = 0, lt = 0, at = 0;
 #pragma unroll
     for (int x = 0; x < kEPer; ++x) {
       km[x] = __ballot_sync(0xffffffffu, (keepm >> x) & 1u);
       lm[x] = __ballot_sync(0xffffffffu, (livem >> x) & 1u);
-      kpre[x] = kt; lpre[x] = lt;
-      kt += __popc(km[x]); lt += __popc(lm[x]);
+      am[x] = __ballot_sync(0xffffffffu, (latm >> x) & 1u);
+      kpre[x] = kt; lpre[x] = lt; apre[x] = at;
+      kt += __popc(km[x]); lt += __popc(lm[x]); at += __popc(am[x]);
     }
-    if (lane == 0) { s_keep[warp] = kt; s_live[warp] = lt; }
+    if (lane == 0) { s_keep[warp] = kt; s_live[warp] = lt; s_lat[warp] = at; }
     __syncthreads();
     if (tid < 32) {
       const uint32_t k0 = tid < kEBlock / 32 ? s_keep[tid] : 0u, l0 = tid < kEBlock / 32 ? s_live[tid] : 0u;
-      uint32_t ki = k0, li = l0;
+      const uint32_t a0 = tid < kEBlock / 32 ? s_lat[tid] : 0u;
+      uint32_t ki = k0, li = l0, ai = a0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t a1 = __shfl_up_sync(0xffffffffu, ki, o), a2 = __shfl_up_sync(0xffffffffu, li, o);
-        if (tid >= (uint32_t)o) { ki += a1; li += a2; }
+        const uint32_t a3 = __shfl_up_sync(0xffffffffu, ai, o);
+        if (tid >= (uint32_t)o) { ki += a1; li += a2; ai += a3; }
       }
       const uint32_t ktot = __shfl_sync(0xffffffffu, ki, 31), ltot = __shfl_sync(0xffffffffu, li, 31);
-      uint32_t kb = 0, lb = 0;
+      const uint32_t atot = __shfl_sync(0xffffffffu, ai, 31);
+      uint32_t kb = 0, lb = 0, ab = 0;
       if (tid == 0) {
         if (ktot) kb = atomicAdd(fcount_live, ktot);
         if (ltot) { lb = atomicAdd(qcount_next, ltot); s_nlive += ltot; }
+        if (atot) ab = atomicAdd(lcount, atot);
       }
       kb = __shfl_sync(0xffffffffu, kb, 0);
       lb = __shfl_sync(0xffffffffu, lb, 0);
-      if (tid < kEBlock / 32) { s_keep[tid] = kb + ki - k0; s_live[tid] = lb + li - l0; }
+      ab = __shfl_sync(0xffffffffu, ab, 0);
+      if (tid < kEBlock / 32) { s_keep[tid] = kb + ki - k0; s_live[tid] = lb + li - l0; s_lat[tid] = ab + ai - a0; }
     }
     __syncthreads();
-    const uint32_t kw = s_keep[warp], lw = s_live[warp], ltm = (1u << lane) - 1u;
+    const uint32_t kw = s_keep[warp], lw = s_live[warp], aw = s_lat[warp], ltm = (1u << lane) - 1u;
 #pragma unroll
     for (int x = 0; x < kEPer; ++x) {
       if ((keepm >> x) & 1u) far_live[kw + kpre[x] + __popc(km[x] & ltm)] = v[x];
+      if ((latm >> x) & 1u) later[aw + apre[x] + __popc(am[x] & ltm)] = v[x];
       if ((livem >> x) & 1u) {
         prefetch_l2(a.slots + 8 * (size_t)v[x]);  // read by the next ROUND phase
         q_next[lw + lpre[x] + __popc(lm[x] & ltm)] = v[x];
@@ -2637,9 +2751,12 @@ __global__ void __launch_bounds__(kEBlock) extract_kernel(KArgs a) {
   }
   const uint32_t fm = __reduce_min_sync(0xffffffffu, my_fmin);
   if (lane == 0 && fm != kInf) atomicMin(&s_fmin, fm);
+  const uint32_t lmn = __reduce_min_sync(0xffffffffu, my_lmin);
+  if (lane == 0 && lmn != kInf) atomicMin(&s_lmin, lmn);
   __syncthreads();
   if (tid == 0) {
     if (s_fmin != kInf) atomicMin(&ws.ctl->fmin[j % 3], s_fmin);
+    if (s_lmin != kInf) atomicMin(&ws.ctl->lmin[t % 3], s_lmin);
     if (s_nlive) atomicAdd(&ws.ctl->xlive[j % 3], s_nlive);
     if (blockIdx.x == 0) ws.kst->pending = 0;
   }

@@ -49,7 +49,7 @@ class gi_options(ctypes.Structure):
                 ("hub_min", ctypes.c_uint32), ("drain", ctypes.c_uint32),
                 ("group_ctas", ctypes.c_int32), ("pre_read", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p),
                 ("cta_threads", ctypes.c_int32), ("expand", ctypes.c_int32), ("lazy", ctypes.c_int32),
-                ("rung", ctypes.c_int32)]
+                ("rung", ctypes.c_int32), ("window", ctypes.c_int32)]
 
 
 class gi_stats(ctypes.Structure):
@@ -240,7 +240,7 @@ def _default_stream(options, *tensors):
 
 
 def make_options(fusion=True, threshold=0, max_ctas=0, group_ctas=0, pre_read=0, hub_min=0,
-                 drain=0, stream=None, cta_threads=0, expand=0, lazy=False, rung=0) -> gi_options:
+                 drain=0, stream=None, cta_threads=0, expand=0, lazy=False, rung=0, window=0) -> gi_options:
     o = gi_options()
     _lib.gi_options_default(ctypes.byref(o))
     o.fusion = 1 if fusion else 0
@@ -254,6 +254,7 @@ def make_options(fusion=True, threshold=0, max_ctas=0, group_ctas=0, pre_read=0,
     o.expand = {"auto": 0, "on": 1, "off": 2}.get(expand, expand)
     o.lazy = 1 if lazy else 0
     o.rung = {"auto": 0, "cta": 1, "cluster": 2, "grid": 3}.get(rung, rung)
+    o.window = window
     if stream is not None:
         o.cuda_stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     return o

@@ -50,14 +50,14 @@ def test_sm100a_code_only(gi):
 
 
 def test_version_status_strings_and_struct_layout(gi):
-    assert gi.version() == 200
+    assert gi.version() == 201
     lib = gi.lib()
     for code, name in gi.STATUS.items():
         assert lib.gi_status_string(code).decode() == name
     o = gi.gi_options()
     lib.gi_options_default(ctypes.byref(o))
     assert o.struct_size == ctypes.sizeof(gi.gi_options)
-    assert o.fusion == 1 and o.fusion_threshold == 0 and o.max_ctas == 0
+    assert o.fusion == 1 and o.fusion_threshold == 0 and o.max_ctas == 0 and o.window == 0
 
 
 def test_error_paths_without_gpu(gi):

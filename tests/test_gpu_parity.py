@@ -500,6 +500,55 @@ def test_expand_mirror_filter(gi, monkeypatch):
     monkeypatch.delenv("GI_MIRROR")
 
 
+def test_bucket_window(gi, monkeypatch, config_graph):
+    """The bucket window of expand queries (gi_options.window buckets): far entries
+    beyond the open window wait in the later pile and are rescanned only when the window
+    advances. Widths 1 (an advance per bucket), 2, 8 and off; extractions in the persistent
+    kernel and in extract_kernel; fused / unfused / lazy; PPSP (its stop clears the later
+    pile's bits) and A*; config 3 at full size. Exact distances and bucket counts."""
+    rng = np.random.default_rng(59)
+    for t in range(3):
+        n = int(rng.integers(4_000, 30_000))
+        deg = np.minimum(rng.zipf(1.6, size=n), n - 1)
+        deg[rng.integers(0, n, 2)] = rng.integers(1_000, max(1_001, n // 3), 2)
+        wmax = int(rng.choice([9, 300]))
+        edges = [(u, int(v), int(w)) for u in range(n) for v, w in
+                 zip(rng.integers(0, n, deg[u]), rng.integers(1, wmax, deg[u]))]
+        g = gen.from_edges(n, edges)
+        G = gi.Graph.from_csr(g)
+        s = int(np.argmax(deg))
+        ref, _ = oracle.dijkstra(g, s)
+        tgt = int(rng.integers(0, n))
+        for win in (1, 2, 8, 0):
+            for split_min, xsplit_min in (("1", "1"), ("1", str(1 << 30)), (str(1 << 40), "1")):
+                monkeypatch.setenv("GI_SPLIT_MIN", split_min)
+                monkeypatch.setenv("GI_XSPLIT_MIN", xsplit_min)
+                for o, delta in ((dict(expand="on"), 1), (dict(expand="on"), 5), (dict(expand="on", fusion=False), 2),
+                                 (dict(expand="on", fusion=False, lazy=True), 3), (dict(expand="on", max_ctas=3), 1)):
+                    d, st = run(gi, G, s, delta, window=win, **o)
+                    assert np.array_equal(d, ref), (t, win, split_min, xsplit_min, o, delta)
+                    assert st["buckets"] == oracle.bucket_count(ref, delta), (t, win, o, delta)
+                assert gi.ppsp(G, s, tgt, 2, expand="on", window=win)[0] == int(ref[tgt]), (t, win)
+                h = np.zeros(n, np.uint32)
+                assert gi.astar(G, s, tgt, 2, h, expand="on", window=win)[0] == int(ref[tgt]), (t, win)
+                # the workspace ends clean after the PPSP stop: a full query still matches
+                d, _ = run(gi, G, s, 1, expand="on", window=win)
+                assert np.array_equal(d, ref), (t, win, "after ppsp")
+    monkeypatch.setenv("GI_SPLIT_MIN", str(1 << 20))
+    monkeypatch.setenv("GI_XSPLIT_MIN", "4096")
+    g = config_graph(3)
+    G = gi.Graph.from_csr(g)
+    src = gen.config_source(3, g)
+    ref, _ = oracle.dijkstra(g, src)
+    for win in (1, 4):
+        for delta in (1, 2):
+            d, st = run(gi, G, src, delta, expand="on", window=win)
+            assert np.array_equal(d, ref), (win, delta)
+            assert st["buckets"] == oracle.bucket_count(ref, delta), (win, delta)
+    with pytest.raises(gi.GiError):
+        run(gi, G, src, 1, window=-1)
+
+
 def test_extract_split_segments(gi, monkeypatch, config_graph):
     """Split extraction (single queries on skewed graphs with expand): an EXTRACT phase whose
     far pile holds >= GI_XSPLIT_MIN entries stops the persistent kernel (KState, pending 2);
