@@ -1679,6 +1679,11 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
     bool xprev = false;  // the previous phase's extraction ran outside (its bucket went to q)
     if (resuming) {
       const KState* ks = ws.kst;
+      // the host enqueues [expand, extract, resume] rounds ahead of knowing whether the
+      // query stopped again: a resume with nothing pending (the query finished) is a no-op.
+      // Every CTA reads the flag here; it is rewritten only at this segment's next stop or
+      // at the query's end, both after group barriers.
+      if (*reinterpret_cast<const volatile uint32_t*>(&ks->pending) == 0) return;
       p = ks->p; j = ks->j; b = ks->b; prev = ks->prev; last_b = ks->last_b;
       t = ks->t; wend = ks->wend;
       xmid = ks->rkind == 2;
@@ -2338,6 +2343,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
       }
     }
     if (rank == 0 && tid == 0) ctl->next_si = a.ngroups + (int32_t)atomicAdd(a.src_next, 1u);
+    if (XP && rank == 0 && tid == 0) ws.kst->pending = 0;  // the split query is finished
     group_barrier_r(ctl, G, a.rung);  // the next query re-initialises ctl
     if (tid == 0) s.cnt = (uint32_t)__ldcg(&ctl->next_si);
     __syncthreads();
@@ -2448,6 +2454,9 @@ __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
   extern __shared__ __align__(16) unsigned char x_dyn[];
   XShared& xs = *reinterpret_cast<XShared*>(x_dyn);
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // enqueued speculatively (see the host's segment loop): a no-op unless the persistent
+  // kernel stopped for an expand (KState.pending == 1, cleared by the resumed kernel)
+  if (*reinterpret_cast<const volatile uint32_t*>(&a.groups[0].kst->pending) != 1) return;
   if (tid == 0) {
     const GroupWs& ws = a.groups[0];
     const KState* ks = ws.kst;
@@ -2636,7 +2645,6 @@ __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
   flush_cur();
   const uint32_t fm = __reduce_min_sync(0xffffffffu, my_fmin);
   if (lane == 0 && fm != kInf) atomicMin(&a.groups[0].ctl->fmin[ks->j % 3], fm);
-  if (blockIdx.x == 0 && tid == 0) a.groups[0].kst->pending = 0;
 }
 
 // The external extraction of a split query (KState.pending == 2): phase p's partition of
@@ -2658,6 +2666,8 @@ __global__ void __launch_bounds__(kEBlock) extract_kernel(KArgs a) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const GroupWs& ws = a.groups[0];
   const KState* ks = ws.kst;
+  // enqueued speculatively: a no-op unless the persistent kernel stopped for an extraction
+  if (*reinterpret_cast<const volatile uint32_t*>(&ks->pending) != 2) return;
   const uint32_t p = ks->p, j = ks->j, b = ks->b, cnt = ks->xn;
   // bucket window: entries of buckets >= wend go to the later pile of advance t
   const uint32_t wend = ks->wend, t = ks->t;
@@ -2758,7 +2768,6 @@ __global__ void __launch_bounds__(kEBlock) extract_kernel(KArgs a) {
     if (s_fmin != kInf) atomicMin(&ws.ctl->fmin[j % 3], s_fmin);
     if (s_lmin != kInf) atomicMin(&ws.ctl->lmin[t % 3], s_lmin);
     if (s_nlive) atomicAdd(&ws.ctl->xlive[j % 3], s_nlive);
-    if (blockIdx.x == 0) ws.kst->pending = 0;
   }
 }
 #endif
@@ -2943,17 +2952,38 @@ cudaError_t query_clusters(int kind, int cluster, int* max_clusters) {
 }
 
 #if GI_BLOCK >= 1024
+// Launch geometry of the split kernels, computed once per (device, kernel): the host's
+// segment loop enqueues these kernels every round, so no attribute or occupancy query may
+// sit on that path. Grid sizes are cached per device; the max-dynamic-smem attribute is set
+// before the first query on each device (the attribute is per context).
+constexpr int kMaxDev = 64;
+static std::atomic<int> g_xgrid[kMaxDev][5];  // 4 expand variants + extract_kernel; 0 = unknown
+static cudaError_t split_grid(int slot, const void* fn, int threads, int smem, int* grid) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < kMaxDev) {
+    const int g = g_xgrid[dev][slot].load(std::memory_order_acquire);
+    if (g > 0) { *grid = g; return cudaSuccess; }
+  }
+  int sms = 0, bps = 0;
+  if (smem > 0) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, threads, smem);
+  if (e != cudaSuccess) return e;
+  *grid = sms * (bps > 0 ? bps : 1);
+  if (dev < kMaxDev) g_xgrid[dev][slot].store(*grid, std::memory_order_release);
+  return cudaSuccess;
+}
+
 cudaError_t launch_expand(const KArgs& a, cudaStream_t st, int* grid_used) {
+  const int slot = (a.pedges ? 2 : 0) + (a.mirror ? 1 : 0);
   const void* fn = a.pedges ? (a.mirror ? (const void*)expand_kernel<true, true> : (const void*)expand_kernel<true, false>)
                             : (a.mirror ? (const void*)expand_kernel<false, true> : (const void*)expand_kernel<false, false>);
   const int smem = (int)sizeof(XShared);
-  int dev = 0, sms = 0, bps = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, kBlock, smem);
+  int grid = 0;
+  cudaError_t e = split_grid(slot, fn, kBlock, smem, &grid);
   if (e != cudaSuccess) return e;
-  const int grid = sms * (bps > 0 ? bps : 1);
   if (grid_used) *grid_used = grid;
   KArgs args = a;
   void* params[] = {&args};
@@ -2961,13 +2991,11 @@ cudaError_t launch_expand(const KArgs& a, cudaStream_t st, int* grid_used) {
 }
 
 cudaError_t launch_extract(const KArgs& a, cudaStream_t st) {
-  int dev = 0, sms = 0, bps = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, extract_kernel, kEBlock, 0);
+  int grid = 0;
+  cudaError_t e = split_grid(4, (const void*)extract_kernel, kEBlock, 0, &grid);
   if (e != cudaSuccess) return e;
   // the pile size is read by the kernel (KState.xn): one resident wave, tiles grid-strided
-  extract_kernel<<<sms * (bps > 0 ? bps : 1), kEBlock, 0, st>>>(a);
+  extract_kernel<<<grid, kEBlock, 0, st>>>(a);
   return cudaGetLastError();
 }
 #endif
