@@ -44,6 +44,12 @@ constexpr int kKcChunk = 2048;  // frontier vertices staged per claim / per loca
 #ifndef GI_KC_LANE_PUSH
 #define GI_KC_LANE_PUSH 1
 #endif
+// slot path (low-degree graphs): combine a warp's decrements of one vertex first
+// (__match_any_sync) or send one atomic per edge — on a grid two frontier vertices of a
+// warp rarely share a neighbour, so the match is mostly overhead
+#ifndef GI_KC_SLOT_MATCH
+#define GI_KC_SLOT_MATCH 0
+#endif
 #ifndef GI_KCT
 #define GI_KCT 1024
 #endif
@@ -293,6 +299,23 @@ __device__ __forceinline__ void kc_relax_entries(const KcArgs& a, KcShared& s, c
 //   - no CAS claim: in the slot path the extraction and the drains of a phase are separated
 //     by a group barrier, so the one crossing subtraction is the vertex's only claimant and
 //     writes its coreness with a plain store.
+// the column of an ELL slot entry, optionally with an L2 evict-first policy (the slots
+// stream through once per peel; the priorities should stay in L2)
+#ifndef GI_KC_SLOT_EF
+#define GI_KC_SLOT_EF 1
+#endif
+__device__ __forceinline__ uint32_t kc_ld_slot(const uint2* p) {
+#if GI_KC_SLOT_EF
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  uint32_t x;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(x) : "l"(p), "l"(pol));
+  return x;
+#else
+  return __ldg(p).x;
+#endif
+}
+
 // Called by all threads; ends with a CTA barrier.
 template <int U>
 __device__ __forceinline__ void kc_relax_slots(const KcArgs& a, KcCtx& c, const int32_t* list, uint32_t cnt) {
@@ -305,7 +328,7 @@ __device__ __forceinline__ void kc_relax_slots(const KcArgs& a, KcCtx& c, const 
     for (int u = 0; u < U; ++u) {
       const uint32_t item = base + u * kKcBlock + tid;
       tv[u] = kColEmpty;
-      if (item < nitems) tv[u] = __ldg(a.slots + 8 * (size_t)list[item >> 3] + sub).x;
+      if (item < nitems) tv[u] = kc_ld_slot(a.slots + 8 * (size_t)list[item >> 3] + sub);
     }
     uint32_t lead = 0, cntp[U], old[U];
     unsigned ne = 0;
@@ -313,9 +336,14 @@ __device__ __forceinline__ void kc_relax_slots(const KcArgs& a, KcCtx& c, const 
     for (int u = 0; u < U; ++u) {
       const bool want = tv[u] != kColEmpty;
       ne += want;
-      const uint32_t peers = __match_any_sync(0xffffffffu, tv[u]);
-      cntp[u] = __popc(peers);
-      if (want && (__ffs(peers) - 1) == (int)lane) lead |= 1u << u;
+      if (GI_KC_SLOT_MATCH) {
+        const uint32_t peers = __match_any_sync(0xffffffffu, tv[u]);
+        cntp[u] = __popc(peers);
+        if (want && (__ffs(peers) - 1) == (int)lane) lead |= 1u << u;
+      } else {  // one decrement per edge: the crossing test holds per atomic all the same
+        cntp[u] = 1;
+        if (want) lead |= 1u << u;
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) old[u] = (lead & (1u << u)) ? atomicSub(a.prio + tv[u], cntp[u]) : 0u;
