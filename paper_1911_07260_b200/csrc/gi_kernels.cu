@@ -163,6 +163,23 @@ __device__ __forceinline__ void red_min(uint32_t* p, uint32_t v) {
 // never through the non-coherent/L1 path (SURVEY §7 hard part 1).
 __device__ __forceinline__ uint32_t ld_dist(const uint32_t* p) { return __ldcg(p); }
 
+// extraction reads of dist (one random read per far entry): optionally evict-first, so the
+// pile scan does not push the bitmaps and the mirror out of L2 (investigation flag)
+#ifndef GI_X_XDIST_EF
+#define GI_X_XDIST_EF 0
+#endif
+__device__ __forceinline__ uint32_t ld_dist_x(const uint32_t* p) {
+#if GI_X_XDIST_EF
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  uint32_t v;
+  asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+#else
+  return __ldcg(p);
+#endif
+}
+
 // L2 eviction-priority policies (createpolicy; the policy travels with the access).
 __device__ __forceinline__ uint64_t pol_evict_last() {
   uint64_t p;
@@ -176,6 +193,9 @@ __device__ __forceinline__ uint64_t pol_evict_first() {
 }
 #ifndef GI_X_DIST_EL
 #define GI_X_DIST_EL 0
+#endif
+#ifndef GI_X_PMIR
+#define GI_X_PMIR 1  // the persistent kernel's pre-reads use the expand mirror too (R17)
 #endif
 #ifndef GI_X_WSKIP
 #define GI_X_WSKIP 0
@@ -335,6 +355,7 @@ struct Shared {
   uint32_t xhn;             // expand: entries of the group list after collection
   uint32_t wend, ws;        // bucket window: end of the open window, start of a new one (ADVANCE)
   uint32_t lcnt;            // bucket window: later-pile entries (PPSP stop cleanup)
+  uint8_t* mirror;          // expand queries: the dist mirror (KArgs.mirror, R17) for the pre-reads
   unsigned long long xS[kMaxGroupCtas + 1];  // expand: exclusive prefix of the CTA slice totals
 };
 
@@ -541,11 +562,40 @@ __device__ __forceinline__ void warp_flush_far(Ctx& c, const int32_t* seg, uint3
   __syncwarp();
 }
 
+// R17 in the persistent kernel (expand queries): the pre-read is the vertex's byte of the
+// dist mirror; a candidate it does not rule out takes atomicMin, whose old value decides
+// the push exactly, and the byte is set to the new distance or tightened to the old one.
+// Returns false (nothing done) when the query has no mirror.
+template <int K>
+__device__ __forceinline__ bool relax_mirrored(Ctx& c, const uint2 (&e)[K], const uint32_t (&nd)[K], uint32_t& ok,
+                                               uint32_t (&old)[K]) {
+  uint8_t* mir = c.s->mirror;
+  if (!mir) return false;
+  uint32_t mb[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) mb[k] = (ok & (1u << k)) ? ld_mirror(mir + e[k].x) : 0u;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (!(mb[k] == 0xFFu || nd[k] < mb[k])) ok &= ~(1u << k);
+#pragma unroll
+  for (int k = 0; k < K; ++k) old[k] = (ok & (1u << k)) ? atomicMin(c.dist + e[k].x, nd[k]) : 0u;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if (!(ok & (1u << k))) continue;
+    if (nd[k] < old[k]) {
+      if (nd[k] < 0xFFu) st_mirror(mir + e[k].x, nd[k]);
+    } else if (old[k] < mb[k]) {
+      st_mirror(mir + e[k].x, old[k]);  // tighten (old < 0xFF)
+    }
+  }
+  return true;
+}
+
 // Relax K edges per thread (u -> e[k].x, weight e[k].y, from du[k]); lanes with
 // bit k of `valid` clear do nothing. Every load and atomic of the batch is issued
 // before any result is consumed (memory-level parallelism on the critical chain).
 // Must be called by all 32 lanes of the warp (the appends are warp-aggregated).
-template <bool FUSED, int K, bool LD = false>
+template <bool FUSED, int K, bool LD = false, bool MIR = false>
 __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], const uint32_t (&du)[K],
                                                 uint32_t valid, const uint32_t* cur = nullptr) {
   uint32_t nd[K], old[K];
@@ -559,7 +609,12 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
     }
   }
   TRACE(29);  // the slots have arrived (nd consumed them)
-  if (!LD && c.pre_read) {
+  // expand queries (XP kernels): the candidates the dist mirror rules out touch no dist
+  bool mirrored = false;
+  if constexpr (MIR && !LD && GI_X_PMIR) mirrored = relax_mirrored<K>(c, e, nd, ok, old);
+  if (mirrored) {
+    // ok and old are what the atomic path below would leave
+  } else if (!LD && c.pre_read) {
     // pre-read dist[v]; only an improving candidate is written, with a fire-and-forget
     // red.min, and the pre-read value stands for the atomic's old value. Two threads that
     // both improve on the same pre-read may both push v: a duplicate entry, which the
@@ -728,7 +783,7 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
 // the 8 lanes of an octet share one entry and lane k relaxes entry k of its 64-byte
 // ELL slot (one coalesced 64 B load per octet). Each thread holds U items in flight.
 // Vertices with deg > 8 are appended to the CTA's high-degree list for stage B.
-template <bool FUSED, int U, bool LD = false>
+template <bool FUSED, int U, bool LD = false, bool MIR = false>
 __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t nin, bool check_stale,
                                             uint32_t& nv, uint32_t& ne) {
   const uint32_t nitems = nin * 8;
@@ -818,7 +873,7 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
         nv += mine;
       }
     }
-    const uint32_t stale = relax_batch<FUSED, U, LD>(c, e, du, valid, (check_stale && !GI_X_NOSTALE) ? cur : nullptr);
+    const uint32_t stale = relax_batch<FUSED, U, LD, MIR>(c, e, du, valid, (check_stale && !GI_X_NOSTALE) ? cur : nullptr);
     // counters: non-stale entries and their edges (stale is per lane; each lane saw
     // its own probe of the same word)
     nv += __popc(heads & ~stale);
@@ -830,7 +885,7 @@ __device__ __forceinline__ void stage_small(Ctx& c, const uint2* in, uint32_t ni
 // Stage B — vertices with deg > 8: their edges are concatenated (exclusive prefix of
 // the degrees) and split evenly over all threads of the CTA, 4 edges per thread per
 // iteration; an edge finds its vertex by binary search in the prefix array.
-template <bool FUSED>
+template <bool FUSED, bool MIR = false>
 __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32_t& ne) {
   constexpr int PER = kBigCap / kBlock;
   unsigned long long loc[PER];
@@ -916,7 +971,7 @@ __device__ __forceinline__ void stage_big(Ctx& c, Shared& s, uint32_t nb, uint32
     uint32_t valid;
     fetch(k0, e, du, valid);
     TRACE(16);
-    relax_batch<FUSED, kBigK>(c, e, du, valid);
+    relax_batch<FUSED, kBigK, false, MIR>(c, e, du, valid);
     TRACE(17);
   }
   TRACE(13);
@@ -1174,11 +1229,11 @@ __device__ __forceinline__ void expand_relax(Ctx& c, const HubEnt* X, const unsi
 
 // Relax every entry of a CTA-local bin (stage A, then stage B when high-degree
 // vertices were found). Starts after and ends with a CTA barrier.
-template <bool FUSED, bool LD = false>
+template <bool FUSED, bool LD = false, bool MIR = false>
 __device__ __forceinline__ void process_bin(Ctx& c, Shared& s, const uint2* in, uint32_t nin,
                                             bool check_stale, uint32_t& nv, uint32_t& ne) {
-  if (nin * 8 <= (uint32_t)kBlock) stage_small<FUSED, 1, LD>(c, in, nin, check_stale, nv, ne);
-  else stage_small<FUSED, 4, LD>(c, in, nin, check_stale, nv, ne);
+  if (nin * 8 <= (uint32_t)kBlock) stage_small<FUSED, 1, LD, MIR>(c, in, nin, check_stale, nv, ne);
+  else stage_small<FUSED, 4, LD, MIR>(c, in, nin, check_stale, nv, ne);
   __syncthreads();
   TRACE(4);
   if constexpr (LD) return;  // no high-degree list on a low-degree graph
@@ -1218,7 +1273,7 @@ __device__ __forceinline__ void process_bin(Ctx& c, Shared& s, const uint2* in, 
         if (fit + i < nb) c.big[i] = t[k];
       }
       __syncthreads();
-      stage_big<FUSED>(c, s, nb - fit, ne);
+      stage_big<FUSED, MIR>(c, s, nb - fit, ne);
     }
     __syncthreads();  // c.big is refilled by the next chunk
     TRACE(24);
@@ -1227,7 +1282,7 @@ __device__ __forceinline__ void process_bin(Ctx& c, Shared& s, const uint2* in, 
   if (nb) {
     __syncthreads();  // everyone has read bigtail
     if (threadIdx.x == 0) s.bigtail = 0;
-    stage_big<FUSED>(c, s, nb, ne);
+    stage_big<FUSED, MIR>(c, s, nb, ne);
     __syncthreads();
   }
 }
@@ -1602,6 +1657,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
   const int64_t n = a.n;
   const uint32_t T = a.T;
   TRACE_INIT();
+  if constexpr (XP) {  // the mirror pre-read runs only in the XP kernels (read after a barrier)
+    if (tid == 0) s.mirror = a.mirror;
+  }
 
   // Batch: each group runs one query at a time; after the first (static: source gid) it
   // CLAIMS the next source, so that groups that drew cheap sources run more of them.
@@ -1909,7 +1967,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
             v[x] = i < hi ? far_src[i] : -1;
           }
 #pragma unroll
-          for (int x = 0; x < kXtr; ++x) d[x] = v[x] >= 0 ? ld_dist(dist + v[x]) : kInf;
+          for (int x = 0; x < kXtr; ++x) d[x] = v[x] >= 0 ? ld_dist_x(dist + v[x]) : kInf;
           uint32_t keepm = 0;
           uint32_t livem = 0;
           uint32_t latm = 0;  // beyond the window and new to the later pile
@@ -2003,7 +2061,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
             v[x] = i < hi ? lsrc[i] : -1;
           }
 #pragma unroll
-          for (int x = 0; x < kXtr; ++x) d[x] = v[x] >= 0 ? ld_dist(dist + v[x]) : kInf;
+          for (int x = 0; x < kXtr; ++x) d[x] = v[x] >= 0 ? ld_dist_x(dist + v[x]) : kInf;
           uint32_t keepm = 0, movem = 0;
 #pragma unroll
           for (int x = 0; x < kXtr; ++x) {
@@ -2061,7 +2119,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
               c.big[i] = be;
             }
             __syncthreads();
-            stage_big<FUSED>(c, s, nh, ne);
+            stage_big<FUSED, XP>(c, s, nh, ne);
             __syncthreads();
             TRACE(15);
           }
@@ -2115,7 +2173,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           }
           __syncthreads();
           TRACE(14);
-          process_bin<FUSED, LOWDEG>(c, s, stage, chunk, false, nv, ne);  // ends with a barrier
+          process_bin<FUSED, LOWDEG, XP>(c, s, stage, chunk, false, nv, ne);  // ends with a barrier
           if (a.dyn_claim) {
             if (tid == 0) {
               s.claim = dyn ? next : cnt;
@@ -2204,7 +2262,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
                   c.big[i] = be;
                 }
                 __syncthreads();
-                stage_big<FUSED>(c, s, nh, ne);
+                stage_big<FUSED, XP>(c, s, nh, ne);
                 __syncthreads();
               }
             }
@@ -2237,7 +2295,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           if (tid == 0) { s.cnt3[(k + 1) % 3] = 0; ++subrounds; }
           c.out = s_dyn + (k & 1) * kBinCap;
           c.outcnt = &s.cnt3[k % 3];
-          process_bin<FUSED, LOWDEG>(c, s, in, nin, true, nv, ne);
+          process_bin<FUSED, LOWDEG, XP>(c, s, in, nin, true, nv, ne);
         }
       }
 
@@ -2690,7 +2748,7 @@ __global__ void __launch_bounds__(kEBlock) extract_kernel(KArgs a) {
       v[x] = i < cnt ? __ldcs(far_src + i) : -1;  // read once
     }
 #pragma unroll
-    for (int x = 0; x < kEPer; ++x) d[x] = v[x] >= 0 ? ld_dist(dist + v[x]) : kInf;
+    for (int x = 0; x < kEPer; ++x) d[x] = v[x] >= 0 ? ld_dist_x(dist + v[x]) : kInf;
 #pragma unroll
     for (int x = 0; x < kEPer; ++x) hv[x] = (a.h && v[x] >= 0) ? __ldg(a.h + v[x]) : 0u;
     uint32_t keepm = 0, livem = 0, latm = 0;
