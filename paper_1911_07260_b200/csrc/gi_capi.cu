@@ -574,9 +574,12 @@ gi_status run_queries(const gi_graph* cg_, const int32_t* srcs, int32_t nsrc, ui
   }
   // bucket window (split queries): far entries beyond the open window wait in a later pile
   a.window = 0;
+  a.window_pile = 0;
   if (a.split) {
     const char* wv = getenv("GI_WINDOW");  // investigation override (buckets; 0 = off)
     a.window = wv ? (uint32_t)strtoul(wv, nullptr, 10) : opt.window ? (uint32_t)opt.window : (uint32_t)kDefaultWindow;
+    const char* wp = getenv("GI_WINDOW_PILE");  // investigation: open the window late
+    a.window_pile = wp ? (uint32_t)strtoul(wp, nullptr, 10) : 0u;
     GroupWs& g0 = w->h_groups[0];
     if (a.window && !g0.laterbits) {
       const size_t nwords = (size_t)((g->n + 31) / 32);

@@ -197,6 +197,8 @@ struct KArgs {
   uint8_t* mirror;
   uint32_t window;         // bucket window width in buckets (0 = off: every far entry is
                            // rescanned at every extraction); needs GroupWs.laterbits
+  uint32_t window_pile;    // > 0: the window opens at the first extraction whose far pile holds
+                           // <= window_pile entries (the tail of a skewed query); 0 = from the start
 };
 
 // k-core (gi_kcore.cu): control block, statistics and arguments.

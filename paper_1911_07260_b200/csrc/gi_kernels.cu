@@ -1730,7 +1730,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
     uint32_t p = 0, j = 0, b = 0, prev = MODE_NONE;
     // bucket window (a.window buckets; off: wend = inf): t = advances so far, the later pile
     // of advance t is later[t & 1] with counters lcount / lmin [t % 3]
-    uint32_t t = 0, wend = (XP && a.window) ? a.window : kInf;  // constants outside the XP kernels
+    // (window_pile > 0: the window opens only once the far pile has shrunk to that size)
+    uint32_t t = 0, wend = (XP && a.window && !a.window_pile) ? a.window : kInf;  // constants outside XP
     uint32_t last_b = kInf;  // bucket of the last extraction with live vertices (rank 0, thread 0)
     bool mid = false;  // resuming inside phase p, after its external expand / extraction
     bool xmid = false;  // ... after its external extraction: phase p was an EXTRACT phase
@@ -1816,7 +1817,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
         const uint32_t lc = (XP && a.window) ? __ldcg(&ctl->lcount[t % 3]) : 0u;
         s.lcnt = lc;
         if (qn > 0 || hn > 0) { mode = MODE_ROUND; s.cnt = qn; }
-        else if (fc > 0 && fm < wend) { mode = MODE_EXTRACT; s.cnt = fc; s.b = fm; }
+        else if (XP && a.window && wend == kInf && fc > 0 && fc <= a.window_pile && fm < kInf - a.window) {
+          mode = MODE_EXTRACT; s.cnt = fc; s.b = fm;  // the window opens at this extraction
+          wend = fm + a.window;
+        } else if (fc > 0 && fm < wend) { mode = MODE_EXTRACT; s.cnt = fc; s.b = fm; }
         else if (XP && lc > 0) {
           const uint32_t lm = __ldcg(&ctl->lmin[t % 3]);
           const uint32_t ws0 = min(fc > 0 ? fm : kInf, lm);

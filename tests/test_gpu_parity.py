@@ -545,6 +545,16 @@ def test_bucket_window(gi, monkeypatch, config_graph):
             d, st = run(gi, G, src, delta, expand="on", window=win)
             assert np.array_equal(d, ref), (win, delta)
             assert st["buckets"] == oracle.bucket_count(ref, delta), (win, delta)
+    # the window opened late (GI_WINDOW_PILE: at the first extraction of a pile that small)
+    for pile in ("1000000", "50000"):
+        monkeypatch.setenv("GI_WINDOW_PILE", pile)
+        for win, delta in ((2, 1), (4, 2)):
+            d, st = run(gi, G, src, delta, expand="on", window=win)
+            assert np.array_equal(d, ref), (pile, win, delta)
+            assert st["buckets"] == oracle.bucket_count(ref, delta), (pile, win, delta)
+        assert gi.ppsp(G, src, int(np.argmax(ref != INF)), 1, expand="on", window=2)[0] == int(
+            ref[int(np.argmax(ref != INF))])
+    monkeypatch.delenv("GI_WINDOW_PILE")
     with pytest.raises(gi.GiError):
         run(gi, G, src, 1, window=-1)
 
