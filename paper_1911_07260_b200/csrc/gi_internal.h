@@ -139,6 +139,7 @@ struct KState {
                                 // 2 = for an external extraction of phase p (extract_kernel)
   uint32_t rkind;               // what the resumed segment continues after (1 expand, 2 extract)
   uint32_t t, wend;             // bucket window: advances so far, end of the open window
+  uint32_t wbig;                // bucket window: the far pile has exceeded window_pile
 };
 
 constexpr int kMaxGroupCtas = 1024;  // expand: largest group (CTAs) the slice totals are sized for
@@ -198,7 +199,8 @@ struct KArgs {
   uint32_t window;         // bucket window width in buckets (0 = off: every far entry is
                            // rescanned at every extraction); needs GroupWs.laterbits
   uint32_t window_pile;    // > 0: the window opens at the first extraction whose far pile holds
-                           // <= window_pile entries (the tail of a skewed query); 0 = from the start
+                           // <= window_pile entries after having held more (the tail of a skewed
+                           // query); 0 = from the start
 };
 
 // k-core (gi_kcore.cu): control block, statistics and arguments.

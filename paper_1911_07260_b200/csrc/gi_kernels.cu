@@ -1732,6 +1732,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
     // of advance t is later[t & 1] with counters lcount / lmin [t % 3]
     // (window_pile > 0: the window opens only once the far pile has shrunk to that size)
     uint32_t t = 0, wend = (XP && a.window && !a.window_pile) ? a.window : kInf;  // constants outside XP
+    bool wbig = false;  // window_pile: the far pile has been larger than window_pile (thread 0)
     uint32_t last_b = kInf;  // bucket of the last extraction with live vertices (rank 0, thread 0)
     bool mid = false;  // resuming inside phase p, after its external expand / extraction
     bool xmid = false;  // ... after its external extraction: phase p was an EXTRACT phase
@@ -1744,7 +1745,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
       // at the query's end, both after group barriers.
       if (*reinterpret_cast<const volatile uint32_t*>(&ks->pending) == 0) return;
       p = ks->p; j = ks->j; b = ks->b; prev = ks->prev; last_b = ks->last_b;
-      t = ks->t; wend = ks->wend;
+      t = ks->t; wend = ks->wend; wbig = ks->wbig != 0;
       xmid = ks->rkind == 2;
       if (rank == 0 && tid == 0) {
         phases = ks->phases; rounds = ks->rounds; buckets = ks->buckets; empty = ks->empty; critical = ks->critical;
@@ -1780,7 +1781,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           ks->p = p; ks->j = j; ks->b = b; ks->prev = prev; ks->last_b = last_b;
           ks->phases = phases; ks->rounds = rounds; ks->buckets = buckets; ks->empty = empty;
           ks->critical = critical; ks->E = E; ks->xn = xn; ks->rkind = kind;
-          ks->t = t; ks->wend = wend;
+          ks->t = t; ks->wend = wend; ks->wbig = wbig ? 1u : 0u;
           __threadfence();
           ks->pending = kind;
         }
@@ -1815,9 +1816,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
         // [ws, wend); else advance it (rescan the later pile) or, with nothing waiting
         // there, move it to the far pile's next bucket without a phase
         const uint32_t lc = (XP && a.window) ? __ldcg(&ctl->lcount[t % 3]) : 0u;
+        if (XP && a.window_pile && fc > a.window_pile) wbig = true;  // the tail comes after this
         s.lcnt = lc;
         if (qn > 0 || hn > 0) { mode = MODE_ROUND; s.cnt = qn; }
-        else if (XP && a.window && wend == kInf && fc > 0 && fc <= a.window_pile && fm < kInf - a.window) {
+        else if (XP && a.window && wend == kInf && wbig && fc > 0 && fc <= a.window_pile && fm < kInf - a.window) {
           mode = MODE_EXTRACT; s.cnt = fc; s.b = fm;  // the window opens at this extraction
           wend = fm + a.window;
         } else if (fc > 0 && fm < wend) { mode = MODE_EXTRACT; s.cnt = fc; s.b = fm; }
