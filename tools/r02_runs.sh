@@ -1,0 +1,268 @@
+#!/bin/bash
+# Round-2 GPU runs, one arm per gpurun call of the round (each arm was a tools/run_r02<arm>.sh
+# script before they were folded here). Usage on the GPU box:
+#   bash tools/r02_runs.sh ARM [args]      (outputs under gpurun_out/, summaries in profiles/)
+# Variant libraries for the A/B arms are built here first with tools/ab_build.sh (AB_OUT=tools/abx).
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+arm=$1; shift
+case $arm in
+  aa)  # round 2 (session 4): k-core — slot path without the warp match + evict-first slots (now default), packed 4-byte edges on the CSR path (GI_KC_PACK=0: the 8-byte edges); k-core parity tests
+export AB_DIR=abm AB_ONLY=main
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "kcore" > gpurun_out/r02aa_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02aa_tests.log
+tail -2 gpurun_out/r02aa_tests.log
+for r in 1 2; do for pk in 1 0; do
+  GI_KC_PACK=$pk timeout 600 python tools/ab_kcore.py 3 2>&1 | grep libgi | sed "s/^/cfg 3 pack=$pk: /" >> gpurun_out/r02aa_ab.log
+done; done
+timeout 600 python tools/ab_kcore.py 2 2>&1 | grep libgi | sed "s/^/cfg 2: /" >> gpurun_out/r02aa_ab.log
+;;
+  ab)  # round 2 (session 4): extraction dist reads with an L2 evict-first policy (A/B on configs 4 and 3)
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+for r in 1 2; do for v in xd0 xd1; do
+  for cd in "4 2" "3 2" "2 65536"; do AB_ONLY=$v timeout 600 python tools/ab_time.py $cd 2>&1 | grep libgi | sed "s/^/cfg $cd: /" >> gpurun_out/r02ab_ab.log; done
+done; done
+;;
+  ac)  # round 2 (session 4): the persistent kernel's pre-reads through the expand mirror — tests, A/B
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+timeout 1500 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "window or mirror or split or expand or stress or ppsp or astar or hubs" > gpurun_out/r02ac_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02ac_tests.log
+tail -2 gpurun_out/r02ac_tests.log
+for r in 1 2; do for v in pm0 pm1; do
+  AB_ONLY=$v timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg 4: /" >> gpurun_out/r02ac_ab.log
+done; done
+;;
+  ae)  # round 2 (session 4): the bucket window opened late (GI_WINDOW_PILE) — tests, config 4 A/B
+export GI_GEN_CACHE=/tmp/gcache
+timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "window" > gpurun_out/r02ae_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02ae_tests.log
+tail -2 gpurun_out/r02ae_tests.log
+for r in 1 2; do for wp in "0 0" "4 2000000" "4 8000000" "8 4000000" "2 1000000"; do
+  set -- $wp
+  GI_WINDOW=$1 GI_WINDOW_PILE=$2 timeout 600 python tools/time_cfg.py 4 2 '{}' 2>&1 | grep ms_median | cut -c1-330 | sed "s/^/window=$1 pile=$2 /" >> gpurun_out/r02ae_ab.log
+done; done
+;;
+  af)  # round 2 (session 4): fusion threshold T on config 4 (expand query)
+export GI_GEN_CACHE=/tmp/gcache
+for r in 1 2; do
+  timeout 900 python tools/time_cfg.py 4 2 '{}' '{"threshold": 16}' '{"threshold": 64}' '{"threshold": 1024}' '{"threshold": 4096}' '{"fusion": false}' 2>&1 | grep ms_median | cut -c1-260 >> gpurun_out/r02af_T4.log
+done
+;;
+  b)  # GPU tests after the cluster-flag fix, the fusion-threshold sweep and the eager/lazy table
+timeout 2400 python -m pytest tests -x -q -m gpu > gpurun_out/r02b_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02b_tests.log
+timeout 900 python tools/sweep_T.py 1 2 3 > gpurun_out/r02b_sweepT.md 2>&1
+timeout 900 python tools/lazy_table.py 1 2 3 4 > gpurun_out/r02b_lazy.md 2>&1
+;;
+  c)  # round-2 (session 2) check: GPU tests, default bench, config-4 launch list with DRAM bytes
+export GI_GEN_CACHE=/tmp/gcache
+timeout 2400 python -m pytest tests -x -q -m gpu > gpurun_out/r02c_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02c_tests.log
+( time timeout 1500 python bench.py ) > gpurun_out/r02c_bench.log 2> gpurun_out/r02c_bench.err
+CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-secondary --no-compare"
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"sssp|expand" --csv --log-file gpurun_out/r02c_launches.csv $CMD > gpurun_out/r02c_ncu1.log 2>&1
+;;
+  d)  # traces of config 4 (1024 threads) and config 2 (512), and the config-5 batch Δ / shape sweep
+export GI_GEN_CACHE=/tmp/gcache
+TRACE_W=1024 TRACE_SO=tools/ab/libgi_trace1024.so timeout 600 python tools/trace_async.py cfg4 2 bsp > gpurun_out/r02d_trace_cfg4.log 2>&1
+TRACE_W=512 TRACE_SO=tools/ab/libgi_trace512.so timeout 600 python tools/trace_async.py cfg2 65536 bsp > gpurun_out/r02d_trace_cfg2.log 2>&1
+timeout 900 python tools/batch_sweep.py 4096,8192,16384,32768,65536 '{}' > gpurun_out/r02d_batch_delta.log 2>&1
+timeout 600 python tools/batch_sweep.py 8192 '{"cta_threads": 512}' '{"group_ctas": 4, "cta_threads": 512}' '{"rung": 3}' > gpurun_out/r02d_batch_shape.log 2>&1
+;;
+  e)  # traces of config 4 (fused and unfused, 1024-thread trace build) and config 4 fusion thresholds
+export GI_GEN_CACHE=/tmp/gcache
+TRACE_W=1024 TRACE_SO=tools/ab/libgi_trace1024.so timeout 600 python tools/trace_async.py cfg4 2 bsp > gpurun_out/r02e_trace_cfg4.log 2>&1
+TRACE_W=1024 TRACE_SO=tools/ab/libgi_trace1024.so timeout 600 python tools/trace_async.py cfg4 2 unfused > gpurun_out/r02e_trace_cfg4u.log 2>&1
+timeout 900 python tools/time_cfg.py 4 2 '{}' '{"fusion": false}' '{"threshold": 64}' '{"threshold": 1024}' '{"threshold": 2048}' > gpurun_out/r02e_cfg4_T.log 2>&1
+;;
+  f)  # extraction split: parity (new test + split tests + config 4 full), timing on config 4
+export GI_GEN_CACHE=/tmp/gcache
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "extract_split or expand_split or expand_edge or hand_examples or lazy or config3_full" > gpurun_out/r02f_tests.log 2>&1
+echo "rc=$?" >> gpurun_out/r02f_tests.log
+timeout 900 python tools/time_cfg.py 4 2 '{}' '{"fusion": false}' '{"threshold": 1024}' > gpurun_out/r02f_cfg4.log 2>&1
+GI_XSPLIT_MIN=0 timeout 600 python tools/time_cfg.py 4 2 '{}' > gpurun_out/r02f_cfg4_nox.log 2>&1
+GI_XSPLIT_MIN=500000 timeout 600 python tools/time_cfg.py 4 2 '{}' > gpurun_out/r02f_cfg4_x500k.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "config4_full" > gpurun_out/r02f_cfg4_parity.log 2>&1
+echo "rc=$?" >> gpurun_out/r02f_cfg4_parity.log
+;;
+  g)  # k-core slot path vs CSR path on configs 1-3 (tests + timings), config-4 launch list
+export GI_GEN_CACHE=/tmp/gcache
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "kcore" > gpurun_out/r02g_tests.log 2>&1
+echo "rc=$?" >> gpurun_out/r02g_tests.log
+for c in 2 3 1; do
+  timeout 300 python tools/profile_run.py --config $c --kcore --reps 5 > gpurun_out/r02g_kc$c.log 2>&1
+  GI_KC_SLOTS=0 timeout 300 python tools/profile_run.py --config $c --kcore --reps 5 > gpurun_out/r02g_kc${c}_csr.log 2>&1
+done
+timeout 300 python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02g_plain4.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"sssp|expand|extract" --csv --log-file gpurun_out/r02g_launches4.csv python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02g_ncu4.log 2>&1
+;;
+  h)  # L1-cached expand pre-reads (variant l1) vs base on configs 4 and 3
+export GI_GEN_CACHE=/tmp/gcache
+for r in 1 2; do for v in base l1; do
+  AB_ONLY=$v timeout 600 python tools/ab_time.py 4 2 >> gpurun_out/r02h_ab4.log 2>&1
+done; done
+for v in base l1; do AB_ONLY=$v timeout 600 python tools/ab_time.py 3 2 >> gpurun_out/r02h_ab3.log 2>&1; done
+;;
+  m)  # round 2 (session 4): expand's mirror filter — parity of the split paths, then config 4 A/B
+export GI_GEN_CACHE=/tmp/gcache
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "mirror or split or expand" > gpurun_out/r02m_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02m_tests.log
+for r in 1 2; do for mv in 1 0; do
+  GI_MIRROR=$mv timeout 600 python tools/time_cfg.py 4 2 '{}' >> gpurun_out/r02m_ab4.log 2>&1; echo "mirror=$mv" >> gpurun_out/r02m_ab4.log
+done; done
+;;
+  n)  # round 2 (session 4): mirror test, config-4 launch list with DRAM bytes (mirror on), config-2 level trace
+export GI_GEN_CACHE=/tmp/gcache
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "mirror" > gpurun_out/r02n_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02n_tests.log
+python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02n_plain.log 2>&1 &&
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"sssp|expand|extract" --csv --log-file gpurun_out/r02n_launches.csv python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02n_ncu1.log 2>&1
+TRACE_W=512 timeout 900 python tools/trace_async.py cfg2 65536 bsp > gpurun_out/r02n_trace_cfg2.log 2>&1
+;;
+  o)  # round 2 (session 4): stage-A warp skip A/B (tools/abx/libgi_{base,wskip}.so) and the finer cfg2 level trace
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+TRACE_W=512 TRACE_SO=$GRAFT_REPO_ROOT/tools/abx/libgi_trace512.so timeout 600 python tools/trace_async.py cfg2 65536 bsp > gpurun_out/r02o_trace_cfg2.log 2>&1
+for r in 1 2; do for v in base wskip; do
+  for cd in "2 65536" "1 1000" "3 2" "5 8192"; do
+    AB_ONLY=$v timeout 600 python tools/ab_time.py $cd 2>&1 | grep libgi | sed "s/^/cfg $cd: /" >> gpurun_out/r02o_ab.log
+  done
+done; done
+for v in base wskip; do AB_ONLY=$v timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg 4: /" >> gpurun_out/r02o_ab.log; done
+;;
+  p)  # round 2 (session 4): L2 policies for the wavefront's dist lines vs the slot stream (A/B)
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+for r in 1 2; do for v in base el ef elef persist; do
+  for cd in "2 65536" "1 1000" "5 8192" "3 2"; do
+    if [ $v = persist ]; then
+      GI_L2_PERSIST=1 AB_ONLY=base timeout 600 python tools/ab_time.py $cd 2>&1 | grep -E "libgi|L2 window" | sed "s/^/cfg $cd persist: /" >> gpurun_out/r02p_ab.log
+    else
+      AB_ONLY=$v timeout 600 python tools/ab_time.py $cd 2>&1 | grep libgi | sed "s/^/cfg $cd: /" >> gpurun_out/r02p_ab.log
+    fi
+  done
+done; done
+;;
+  q)  # round 2 (session 4): expand fast block path + 32-bit edge positions (A/B on config 4), split-path parity
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx2
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "mirror or split or expand" > gpurun_out/r02q_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02q_tests.log
+for r in 1 2; do
+  GI_IDX32=0 AB_ONLY=fb0 timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg4 fb0 idx64: /" >> gpurun_out/r02q_ab.log
+  AB_ONLY=fb0 timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg4 fb0 idx32: /" >> gpurun_out/r02q_ab.log
+  AB_ONLY=fb1 timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg4 fb1 idx32: /" >> gpurun_out/r02q_ab.log
+done
+;;
+  r)  # round 2 (session 4): bucket window — parity of the split/window paths, then config 4 per width
+export GI_GEN_CACHE=/tmp/gcache
+timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "window or mirror or split or expand" > gpurun_out/r02r_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02r_tests.log
+tail -3 gpurun_out/r02r_tests.log
+for r in 1 2; do for w in 0 4 8 16; do
+  GI_WINDOW=$w timeout 600 python tools/time_cfg.py 4 2 '{}' 2>&1 | grep ms_median | sed "s/^/window=$w /" >> gpurun_out/r02r_ab4.log
+done; done
+;;
+  s)  # round 2 (session 4): slot-load L2 policy A/B on every config (c0 = the mirror commit's build)
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+for r in 1 2; do for v in c0 ef0 ef1; do
+  for cd in "4 2" "2 65536" "5 8192" "3 2"; do
+    AB_ONLY=$v timeout 600 python tools/ab_time.py $cd 2>&1 | grep libgi | sed "s/^/cfg $cd: /" >> gpurun_out/r02s_ab.log
+  done
+done; done
+;;
+  t)  # round 2 (session 4) evidence run: full GPU tests, default bench (config 4 headline), reference arm, the config-4 launch list with DRAM bytes, then configs 1-3, 5 and the apps
+T=${1:-r02t}
+timeout 2400 python -m pytest tests -x -q -m gpu > gpurun_out/${T}_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/${T}_tests.log
+( time timeout 1500 python bench.py ) > gpurun_out/${T}_bench.log 2> gpurun_out/${T}_bench.err
+( time timeout 1500 python bench.py --impl reference --steps 3 --warmup 1 ) > gpurun_out/${T}_ref.log 2> gpurun_out/${T}_ref.err
+export GI_GEN_CACHE=/tmp/gcache
+python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/${T}_plain.log 2>&1 &&
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"sssp|expand|extract" --csv --log-file gpurun_out/${T}_launches_cfg4.csv python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/${T}_ncu1.log 2>&1
+for c in 1 2 3; do timeout 600 python bench.py --config $c --steps 10 --warmup 3; done > gpurun_out/${T}_cfgs.log 2>&1
+timeout 900 python bench.py --config 5 --steps 5 --warmup 2 > gpurun_out/${T}_cfg5.log 2>&1
+for app in ppsp astar kcore; do timeout 600 python bench.py --config 2 --app $app --steps 10 --warmup 3; done > gpurun_out/${T}_apps.log 2>&1
+timeout 600 python bench.py --config 3 --app kcore --steps 10 --warmup 3 >> gpurun_out/${T}_apps.log 2>&1
+;;
+  u)  # round 2 (session 4): expand rows-in-flight sweep (kXRows) with the mirror, and a --set full capture of config 4's hub-phase expand_kernel (the second expand launch of the query)
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+for r in 1 2; do for v in xr4 xr8 xr12 xr16; do
+  AB_ONLY=$v timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg4: /" >> gpurun_out/r02u_ab.log
+done; done
+ncu --set full --clock-control none --import-source on -k regex:expand_kernel -s 1 -c 1 -o gpurun_out/r02u_expand -f python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02u_ncu.log 2>&1
+;;
+  v)  # round 2 (session 4): batched host segment loop (speculative [expand, extract, resume] rounds)
+export GI_GEN_CACHE=/tmp/gcache
+timeout 1500 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "window or mirror or split or expand or ppsp or astar or stress" > gpurun_out/r02v_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02v_tests.log
+tail -3 gpurun_out/r02v_tests.log
+for r in 1 2 3; do timeout 600 python tools/time_cfg.py 4 2 '{}' '{"fusion": false}' 2>&1 | grep ms_median | cut -c1-300 >> gpurun_out/r02v_cfg4.log; done
+;;
+  w)  # round 2 (session 4): config-5 batch group shapes (CTAs per group, threads per CTA, rung) at Δ=2^13
+timeout 1500 python tools/batch_sweep.py 8192 '{}' '{"group_ctas": 1}' '{"group_ctas": 2}' '{"group_ctas": 4}' \
+  '{"group_ctas": 2, "cta_threads": 512}' '{"group_ctas": 4, "cta_threads": 512}' '{"group_ctas": 1, "cta_threads": 512}' \
+  '{"group_ctas": 2, "threshold": 4096}' '{"group_ctas": 2, "threshold": 1024}' '{"group_ctas": 2, "rung": "grid"}' > gpurun_out/r02w_batch.log 2>&1
+;;
+  x)  # round 2 (session 4): the parent-edge skip of the low-degree fused kernels — GPU tests, then A/B
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+GI_SKIP_CFG4=1 timeout 1800 python -m pytest tests -x -q -m gpu > gpurun_out/r02x_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02x_tests.log
+tail -3 gpurun_out/r02x_tests.log
+for r in 1 2; do for v in par0 par1; do
+  for cd in "2 65536" "1 1000" "5 8192" "2 16384"; do
+    AB_ONLY=$v timeout 600 python tools/ab_time.py $cd 2>&1 | grep libgi | sed "s/^/cfg $cd: /" >> gpurun_out/r02x_ab.log
+  done
+done; done
+;;
+  y)  # round 2 (session 4): --set full captures of config 4's persistent segments (the post-hub-phase segment and the tail segment) for the stall and traffic breakdown
+export GI_GEN_CACHE=/tmp/gcache
+python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02y_plain.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:sssp_persistent -s 5 -c 1 -o gpurun_out/r02y_seg5 -f python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02y_ncu5.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:sssp_persistent -s 17 -c 1 -o gpurun_out/r02y_seg17 -f python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02y_ncu17.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:extract_kernel -s 1 -c 1 -o gpurun_out/r02y_extract -f python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02y_ncux.log 2>&1
+;;
+  z)  # round 2 (session 4): k-core slot path — warp match vs one atomic per edge, slot evict-first (A/B)
+export AB_DIR=abx
+for r in 1 2; do for v in kb knm kef knmef; do
+  for c in 2 1; do AB_ONLY=$v timeout 600 python tools/ab_kcore.py $c 2>&1 | grep libgi | sed "s/^/cfg $c: /" >> gpurun_out/r02z_ab.log; done
+done; done
+;;
+  all)  # round-2 full run: GPU tests, the default bench (no generator cache, as the driver runs it), the reference arm, and the secondary app lines. Usage: run_all_r02.sh [tag] (default r02aj)
+T=${1:-r02aj}
+timeout 2400 python -m pytest tests -x -q -m gpu > gpurun_out/${T}_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/${T}_tests.log
+( time timeout 1500 python bench.py ) > gpurun_out/${T}_bench.log 2> gpurun_out/${T}_bench.err
+( time timeout 1500 python bench.py --impl reference --steps 3 --warmup 1 ) > gpurun_out/${T}_ref.log 2> gpurun_out/${T}_ref.err
+for c in 1 2 3; do timeout 600 python bench.py --config $c --steps 10 --warmup 3; done > gpurun_out/${T}_cfgs.log 2>&1
+timeout 900 python bench.py --config 5 --steps 5 --warmup 2 > gpurun_out/${T}_cfg5.log 2>&1
+for app in ppsp astar kcore; do timeout 600 python bench.py --config 2 --app $app --steps 10 --warmup 3; done > gpurun_out/${T}_apps.log 2>&1
+timeout 600 python bench.py --config 3 --app kcore --steps 10 --warmup 3 >> gpurun_out/${T}_apps.log 2>&1
+;;
+  profile_cfg4)  # round-2 profiles of the config-4 headline: the bench launch list (time + DRAM bytes per launch), then ncu --set full of the hub-phase expand_kernel and the heaviest persistent segment
+export GI_GEN_CACHE=/tmp/gcache
+CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-secondary --no-compare"
+$CMD > gpurun_out/r02ad_plain.log 2>&1 &&
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"sssp|expand" --csv --log-file gpurun_out/r02ad_launches.csv $CMD > gpurun_out/r02ad_ncu1.log 2>&1
+python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02ad_plain2.log 2>&1 &&
+ncu --set full --clock-control none --import-source on -k regex:expand_kernel -s 1 -c 1 -o gpurun_out/r02ad_expand -f python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02ad_ncu2.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:sssp_persistent -s 3 -c 1 -o gpurun_out/r02ad_persist -f python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02ad_ncu3.log 2>&1
+;;
+  rung)  # execution-group rungs (CTA / cluster / grid) on configs 1, 2, 3 and the config-5 batch
+export GI_GEN_CACHE=/tmp/gcache
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "rungs or hand or path or capi" > gpurun_out/rung_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/rung_tests.log
+timeout 600 python tools/time_cfg.py 1 1000 '{}' '{"rung": "cta"}' '{"rung": "cluster", "group_ctas": 4}' '{"rung": "cluster", "group_ctas": 8}' '{"rung": "cluster", "group_ctas": 16}' '{"max_ctas": 16}' > gpurun_out/rung_time1.log 2>&1
+timeout 600 python tools/time_cfg.py 2 65536 '{}' '{"rung": "cluster", "group_ctas": 16}' > gpurun_out/rung_time2.log 2>&1
+timeout 600 python tools/time_cfg.py 3 2 '{}' '{"rung": "cluster", "group_ctas": 16}' > gpurun_out/rung_time3.log 2>&1
+timeout 900 python - > gpurun_out/rung_time5.log 2>&1 <<'PY'
+import sys, json, statistics; sys.path.insert(0, '.')
+import torch, gen
+from paper_1911_07260_b200 import gi
+g = gen.config_graph(5); G = gi.Graph.from_csr(g); srcs = gen.config_sources(5, g, 64)
+out = torch.empty((64, g.n), dtype=torch.int32, device="cuda")
+for o in ({}, {"rung": "cta"}, {"rung": "cluster", "group_ctas": 2}, {"rung": "cluster", "group_ctas": 4}, {"group_ctas": 4}):
+    ts = []
+    for i in range(3):
+        st = gi.gi_sssp_batch(G, srcs, 8192, out, gi.make_options(**o)); ts.append(st[0].gpu_ms)
+    print(json.dumps({"opts": o, "ms": statistics.median(ts), "groups": st[0].groups, "ctas": st[0].ctas, "rung": st[0].rung}), flush=True)
+PY
+;;
+  *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
+esac
