@@ -197,6 +197,9 @@ __device__ __forceinline__ uint64_t pol_evict_first() {
 #ifndef GI_X_PMIR
 #define GI_X_PMIR 1  // the persistent kernel's pre-reads use the expand mirror too (R17)
 #endif
+#ifndef GI_X_XSKIP
+#define GI_X_XSKIP 1  // expand rows with no candidate past the mirror skip the atomics and pushes
+#endif
 #ifndef GI_X_WSKIP
 #define GI_X_WSKIP 0
 #endif
@@ -2646,19 +2649,25 @@ __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
         uint32_t mb[kXRows];
 #pragma unroll
         for (int k = 0; k < kXRows; ++k) mb[k] = (valid >> k) & 1u ? ld_mirror(a.mirror + v[k]) : 0u;
+        uint32_t passm = 0, keep = 0;  // candidates to atomicMin; those plus overflows
 #pragma unroll
         for (int k = 0; k < kXRows; ++k) {
           const uint32_t nd = du[k] + wt[k];
           const bool ovf = nd < du[k] || nd == kInf;
-          const bool pass = ((valid >> k) & 1u) && !ovf && (mb[k] == 0xFFu || nd < mb[k]);
-          old[k] = pass ? atomicMin(dist + v[k], nd) : 0u;
-          if (!pass) valid &= ~(((valid >> k) & 1u && !ovf) ? 1u << k : 0u);  // filtered: done
+          if ((valid >> k) & 1u) {
+            if (ovf) keep |= 1u << k;
+            else if (mb[k] == 0xFFu || nd < mb[k]) passm |= 1u << k;
+          }
         }
+        valid = keep | passm;
+        // most rows of a hub phase end here: no lane holds a candidate the mirror lets through
+        if (GI_X_XSKIP && !__any_sync(0xffffffffu, valid != 0u)) goto rows_done;
+#pragma unroll
+        for (int k = 0; k < kXRows; ++k) old[k] = (passm >> k) & 1u ? atomicMin(dist + v[k], du[k] + wt[k]) : 0u;
 #pragma unroll
         for (int k = 0; k < kXRows; ++k) {
-          if (!((valid >> k) & 1u)) continue;
+          if (!((passm >> k) & 1u)) continue;
           const uint32_t nd = du[k] + wt[k];
-          if (nd < du[k] || nd == kInf) continue;
           if (nd < old[k]) {
             if (nd < 0xFFu) st_mirror(a.mirror + v[k], nd);
           } else {
@@ -2700,6 +2709,7 @@ __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
           }
         }
       }
+    rows_done:
       __syncwarp();
       if (xs.nfar[warp] > (uint32_t)(kXSeg / 2)) flush_far();
       if (xs.ncur[warp] > (uint32_t)(kXCur / 2)) flush_cur();
