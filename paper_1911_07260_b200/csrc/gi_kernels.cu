@@ -200,6 +200,9 @@ __device__ __forceinline__ uint64_t pol_evict_first() {
 #ifndef GI_X_XSKIP
 #define GI_X_XSKIP 1  // expand rows with no candidate past the mirror skip the atomics and pushes
 #endif
+#ifndef GI_X_XCOMPACT
+#define GI_X_XCOMPACT 1  // expand: a block's candidates past the mirror relaxed densely
+#endif
 #ifndef GI_X_WSKIP
 #define GI_X_WSKIP 0
 #endif
@@ -2455,6 +2458,7 @@ struct XPtrs {
 struct XShared {
   int32_t far[kBlock / 32][kXSeg];
   int32_t cur[kBlock / 32][kXCur];
+  uint2 cand[kBlock / 32][32 * kXRows];  // a block's candidates past the mirror, compacted (v, nd)
   uint32_t nfar[kBlock / 32], ncur[kBlock / 32];
   XPtrs ps;
 };
@@ -2604,6 +2608,26 @@ __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
     };
     window();
     const uint32_t lanemask = (2u << lane) - 2u;
+    // an improved vertex: staged per warp — future buckets for the far pile, the current
+    // bucket for the global frontier; a full segment (at most one iteration past half)
+    // takes the lane's own dedup push to the global list
+    auto push_one = [&](uint32_t vv, uint32_t nd) {
+      const XPtrs& ps = xs.ps;
+      const uint32_t bk = ps.h ? max(prio_bucket(nd, __ldg(ps.h + vv), ps.div), ps.bcur) : fdiv(nd, ps.div);
+      const bool cur = bk == ps.bcur && !lazy;
+      if (!cur) my_fmin = min(my_fmin, bk);
+      const uint32_t pos = atomicAdd(cur ? &xs.ncur[warp] : &xs.nfar[warp], 1u);
+      if (pos < (uint32_t)(cur ? kXCur : kXSeg)) {
+        (cur ? xs.cur[warp] : xs.far[warp])[pos] = (int32_t)vv;
+      } else {
+        uint32_t* bits = cur ? ps.qbits : ps.farbits;
+        const uint32_t bit = 1u << (vv & 31);
+        if (!(atomicOr(&bits[vv >> 5], bit) & bit)) {
+          const uint32_t q = atomicAdd(cur ? ps.qcount : ps.fcount, 1u);
+          (cur ? ps.q : ps.far_live)[q] = (int32_t)vv;
+        }
+      }
+    };
     for (uint32_t it0 = 0; it0 < len; it0 += 32 * kXRows) {
       int64_t ei[kXRows];
       uint32_t du[kXRows], valid = 0;
@@ -2662,6 +2686,45 @@ __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
         valid = keep | passm;
         // most rows of a hub phase end here: no lane holds a candidate the mirror lets through
         if (GI_X_XSKIP && !__any_sync(0xffffffffu, valid != 0u)) goto rows_done;
+        if constexpr (GI_X_XCOMPACT) {
+          // the block's candidates (a few of its 32 x kXRows edges) are compacted into the
+          // warp's buffer and relaxed densely, instead of kXRows predicated passes
+          if (__any_sync(0xffffffffu, keep != 0u)) {  // overflowing candidates (rare)
+            const XPtrs& ps = xs.ps;
+#pragma unroll
+            for (int k = 0; k < kXRows; ++k)
+              if ((keep >> k) & 1u) {
+                atomicOr(&ps.ovfbits[v[k] >> 5], 1u << (v[k] & 31));
+                atomicOr(ps.ovf_cand, 1u);
+              }
+          }
+          const uint32_t lt = (1u << lane) - 1u;
+          uint32_t nc = 0;
+#pragma unroll
+          for (int k = 0; k < kXRows; ++k) {
+            const uint32_t m = __ballot_sync(0xffffffffu, (passm >> k) & 1u);
+            if ((passm >> k) & 1u) xs.cand[warp][nc + __popc(m & lt)] = make_uint2(v[k], du[k] + wt[k]);
+            nc += __popc(m);
+          }
+          __syncwarp();
+          for (uint32_t i0 = 0; i0 < nc; i0 += 64) {  // two candidates per lane in flight
+            const bool h0 = i0 + lane < nc, h1 = i0 + 32 + lane < nc;
+            const uint2 c0 = h0 ? xs.cand[warp][i0 + lane] : make_uint2(0, 0);
+            const uint2 c1 = h1 ? xs.cand[warp][i0 + 32 + lane] : make_uint2(0, 0);
+            const uint32_t o0 = h0 ? atomicMin(dist + c0.x, c0.y) : 0u;
+            const uint32_t o1 = h1 ? atomicMin(dist + c1.x, c1.y) : 0u;
+            if (h0 && c0.y < o0) {
+              if (c0.y < 0xFFu) st_mirror(a.mirror + c0.x, c0.y);
+              push_one(c0.x, c0.y);
+            }
+            if (h1 && c1.y < o1) {
+              if (c1.y < 0xFFu) st_mirror(a.mirror + c1.x, c1.y);
+              push_one(c1.x, c1.y);
+            }
+          }
+          __syncwarp();  // the buffer is refilled by the next block
+          goto rows_done;
+        }
 #pragma unroll
         for (int k = 0; k < kXRows; ++k) old[k] = (passm >> k) & 1u ? atomicMin(dist + v[k], du[k] + wt[k]) : 0u;
 #pragma unroll
@@ -2691,22 +2754,7 @@ __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
             continue;
           }
           if constexpr (!MIRROR) red_min(dist + v[k], nd);
-          const uint32_t bk = ps.h ? max(prio_bucket(nd, __ldg(ps.h + v[k]), ps.div), ps.bcur) : fdiv(nd, ps.div);
-          // staged per warp; a full segment (at most one iteration past half) takes the
-          // lane's own dedup push to the global list
-          const bool cur = bk == ps.bcur && !lazy;
-          if (!cur) my_fmin = min(my_fmin, bk);
-          const uint32_t pos = atomicAdd(cur ? &xs.ncur[warp] : &xs.nfar[warp], 1u);
-          if (pos < (uint32_t)(cur ? kXCur : kXSeg)) {
-            (cur ? xs.cur[warp] : xs.far[warp])[pos] = (int32_t)v[k];
-          } else {
-            uint32_t* bits = cur ? ps.qbits : ps.farbits;
-            const uint32_t bit = 1u << (v[k] & 31);
-            if (!(atomicOr(&bits[v[k] >> 5], bit) & bit)) {
-              const uint32_t q = atomicAdd(cur ? ps.qcount : ps.fcount, 1u);
-              (cur ? ps.q : ps.far_live)[q] = (int32_t)v[k];
-            }
-          }
+          push_one(v[k], nd);
         }
       }
     rows_done:

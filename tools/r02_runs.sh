@@ -273,5 +273,14 @@ for r in 1 2 3; do for v in xs0 xs1; do
 AB_ONLY=$v timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg 4: /" >> gpurun_out/r02ag_ab.log
 done; done
 ;;
+  ah)  # expand: a block's candidates past the mirror compacted and relaxed densely (GI_X_XCOMPACT) — tests, config 4 A/B
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+timeout 1500 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "window or mirror or split or expand or stress or hubs" > gpurun_out/r02ah_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02ah_tests.log
+tail -2 gpurun_out/r02ah_tests.log
+for r in 1 2 3; do for v in xc0 xc1; do
+AB_ONLY=$v timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg 4: /" >> gpurun_out/r02ah_ab.log
+done; done
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
