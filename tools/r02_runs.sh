@@ -282,5 +282,11 @@ for r in 1 2 3; do for v in xc0 xc1; do
 AB_ONLY=$v timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg 4: /" >> gpurun_out/r02ah_ab.log
 done; done
 ;;
+  ai)  # expand: a block inside one list entry mapped once (GI_X_FASTBLK), after the compaction — config 4 A/B
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+for r in 1 2 3; do for v in fb0 fb1; do
+AB_ONLY=$v timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg 4: /" >> gpurun_out/r02ai_ab.log
+done; done
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
