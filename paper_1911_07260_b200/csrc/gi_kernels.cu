@@ -200,6 +200,9 @@ __device__ __forceinline__ uint64_t pol_evict_first() {
 #ifndef GI_X_XSKIP
 #define GI_X_XSKIP 1  // expand rows with no candidate past the mirror skip the atomics and pushes
 #endif
+#ifndef GI_X_RSKIP
+#define GI_X_RSKIP 1  // relax_batch: warps with no lowering after the pre-read skip the pushes
+#endif
 #ifndef GI_X_XCOMPACT
 #define GI_X_XCOMPACT 1  // expand: a block's candidates past the mirror relaxed densely
 #endif
@@ -647,6 +650,11 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
     for (int k = 0; k < K; ++k)
       if (cur[k] < du[k]) stale |= 1u << k;
     ok &= ~stale;
+  }
+  // pre-read / mirror filters (skewed graphs): a warp none of whose lanes lowered anything
+  // skips the classification and the pushes with one vote
+  if constexpr (!LD && GI_X_RSKIP) {
+    if ((mirrored || c.pre_read) && !__any_sync(0xffffffffu, ok != 0u)) return stale;
   }
   // classify the successful lowerings: current bucket (bin) or a future one (far pile).
   // A*: priority bucket of nd + h(v), raised to the current bucket if an inconsistent

@@ -288,5 +288,14 @@ for r in 1 2 3; do for v in fb0 fb1; do
 AB_ONLY=$v timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg 4: /" >> gpurun_out/r02ai_ab.log
 done; done
 ;;
+  aj)  # relax_batch: warps with no lowering after the pre-read / mirror filter skip the pushes (GI_X_RSKIP) — tests, A/B
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+timeout 1500 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "config3 or hubs or split or expand or mirror or stress or astar" > gpurun_out/r02aj_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02aj_tests.log
+tail -2 gpurun_out/r02aj_tests.log
+for r in 1 2 3; do for v in rs0 rs1; do
+for cd in "4 2" "3 2"; do AB_ONLY=$v timeout 600 python tools/ab_time.py $cd 2>&1 | grep libgi | sed "s/^/cfg $cd: /" >> gpurun_out/r02aj_ab.log; done
+done; done
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
