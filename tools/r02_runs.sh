@@ -297,5 +297,10 @@ for r in 1 2 3; do for v in rs0 rs1; do
 for cd in "4 2" "3 2"; do AB_ONLY=$v timeout 600 python tools/ab_time.py $cd 2>&1 | grep libgi | sed "s/^/cfg $cd: /" >> gpurun_out/r02aj_ab.log; done
 done; done
 ;;
+  ak)  # ncu --set full of config 4's hub-phase expand_kernel after the vote-skip and compaction
+export GI_GEN_CACHE=/tmp/gcache
+python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02ak_plain.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:expand_kernel -s 1 -c 1 -o gpurun_out/r02ak_expand -f python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02ak_ncu.log 2>&1
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
