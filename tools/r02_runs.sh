@@ -302,5 +302,8 @@ export GI_GEN_CACHE=/tmp/gcache
 python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02ak_plain.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:expand_kernel -s 1 -c 1 -o gpurun_out/r02ak_expand -f python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02ak_ncu.log 2>&1
 ;;
+  al)  # config-5 batch: pre-read on, async drain, unfused (option sweep at Δ=2^13)
+timeout 1500 python tools/batch_sweep.py 8192 '{}' '{"pre_read": 1}' '{"drain": "async"}' '{"fusion": false}' '{"pre_read": 1, "group_ctas": 4}' > gpurun_out/r02al_batch.log 2>&1
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
