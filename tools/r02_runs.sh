@@ -305,5 +305,14 @@ ncu --set full --clock-control none --import-source on -k regex:expand_kernel -s
   al)  # config-5 batch: pre-read on, async drain, unfused (option sweep at Δ=2^13)
 timeout 1500 python tools/batch_sweep.py 8192 '{}' '{"pre_read": 1}' '{"drain": "async"}' '{"fusion": false}' '{"pre_read": 1, "group_ctas": 4}' > gpurun_out/r02al_batch.log 2>&1
 ;;
+  am)  # expand: one window-coverage test per block (GI_X_WCOVER) — split/expand tests, config 4 A/B
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+timeout 1500 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "window or mirror or split or expand" > gpurun_out/r02am_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02am_tests.log
+tail -2 gpurun_out/r02am_tests.log
+for r in 1 2 3; do for v in wc0 wc1; do
+AB_ONLY=$v timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg 4: /" >> gpurun_out/r02am_ab.log
+done; done
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
