@@ -314,5 +314,21 @@ for r in 1 2 3; do for v in wc0 wc1; do
 AB_ONLY=$v timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg 4: /" >> gpurun_out/r02am_ab.log
 done; done
 ;;
+  an)  # round 2 (session 5): evidence run at HEAD from the re-created container, config-4 parity JSON, config-5 chain-vs-work probe
+timeout 2400 python -m pytest tests -x -q -m gpu > gpurun_out/r02an_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02an_tests.log
+( time timeout 1500 python bench.py ) > gpurun_out/r02an_bench.log 2> gpurun_out/r02an_bench.err
+timeout 600 python tools/batch_ecc.py > gpurun_out/r02an_batch_ecc.log 2>&1
+timeout 1500 python tests/run_cfg4.py --reps 2 > gpurun_out/r02an_cfg4_parity.json 2> gpurun_out/r02an_cfg4_parity.err
+;;
+  ao)  # round 2 (session 5): slot prefetches of big extractions' live vertices (GI_X_PFX, GI_X_PFAGG) and extract_kernel at 4 entries per thread, 2 CTAs per SM (e4) — config 4 / 3 A/B
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+for r in 1 2 3; do for v in pf11 pf01 pf00 e4; do
+AB_ONLY=$v timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg 4: /" >> gpurun_out/r02ao_ab.log
+done; done
+for v in pf11 pf01 pf00 e4; do
+AB_ONLY=$v timeout 600 python tools/ab_time.py 3 2 2>&1 | grep libgi | sed "s/^/cfg 3: /" >> gpurun_out/r02ao_ab.log
+done
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
