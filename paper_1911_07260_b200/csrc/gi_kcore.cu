@@ -53,6 +53,12 @@ constexpr int kKcChunk = 2048;  // frontier vertices staged per claim / per loca
 #ifndef GI_KCT
 #define GI_KCT 1024
 #endif
+// slot path: prefetch a finished vertex's slot into L1 only when it lands below T in this
+// CTA's bin (drained here); otherwise (spilled, or a bin that will spill) the slots of a big
+// layer only flush the L2
+#ifndef GI_KC_PFLOCAL
+#define GI_KC_PFLOCAL 0
+#endif
 constexpr uint32_t kKcT = GI_KCT; // bucket fusion threshold: a local bin of >= T vertices spills
 constexpr uint32_t kKcHub = 1024;  // out-degree >= this: edges split over every CTA in the next round
 constexpr uint32_t kUnset = 0xFFFFFFFFu;
@@ -82,6 +88,7 @@ struct KcCtx {
   uint32_t* qcount_next;
   int32_t* out;                 // local bin receiving crossings (shared memory)
   uint32_t* outcnt;
+  const uint2* pf;              // slot path with GI_KC_PFLOCAL: slots prefetched on local pushes
   HubEnt* hub_next;             // group hub list receiving this phase's hubs
   uint32_t* hcount_next;
   uint32_t hubcap;
@@ -115,6 +122,7 @@ __device__ __forceinline__ void kc_push(KcCtx& c, bool want, int32_t v) {
       const uint32_t pos = atomicAdd(c.outcnt, 1u);
       if (pos < (uint32_t)kKcChunk) {
         c.out[pos] = v;
+        if (GI_KC_PFLOCAL && c.pf && pos < kKcT) prefetch_l1(c.pf + 8 * (size_t)v);
       } else {
         cg::coalesced_group g = cg::coalesced_threads();
         uint32_t base = 0;
@@ -354,7 +362,7 @@ __device__ __forceinline__ void kc_relax_slots(const KcArgs& a, KcCtx& c, const 
         if (old[u] > k && old[u] - cntp[u] <= k) {
           cross = true;
           a.core[tv[u]] = k;
-          prefetch_l1(a.slots + 8 * (size_t)tv[u]);  // relaxed by this CTA next sub-round
+          if (!GI_KC_PFLOCAL) prefetch_l1(a.slots + 8 * (size_t)tv[u]);  // relaxed by this CTA next sub-round
         } else if (old[u] > k) {
           c.my_kmin = min(c.my_kmin, old[u] - cntp[u]);
         }
@@ -448,6 +456,7 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
     c.hub_next = (p & 1) ? a.hub[0] : a.hub[1];
     c.hcount_next = &ctl->hcount[(p + 1) % 3];
     c.hubcap = a.hubcap;
+    c.pf = a.ld ? a.slots : nullptr;
     c.my_kmin = kUnset;
     uint32_t* kmin_live = &ctl->kmin[j % 3];  // the min for the NEXT extraction
 
@@ -483,7 +492,7 @@ __global__ void __launch_bounds__(kKcBlock, 1) kcore_persistent(KcArgs a) {
           if (fin) {
             if (a.ld) {
               a.core[v[x]] = k;
-              prefetch_l1(a.slots + 8 * (size_t)v[x]);
+              if (!GI_KC_PFLOCAL) prefetch_l1(a.slots + 8 * (size_t)v[x]);
             } else {
               fin = atomicCAS(a.core + v[x], kUnset, k) == kUnset;
             }

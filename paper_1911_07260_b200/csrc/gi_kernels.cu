@@ -206,6 +206,25 @@ __device__ __forceinline__ uint64_t pol_evict_first() {
 #ifndef GI_X_XCOMPACT
 #define GI_X_XCOMPACT 1  // expand: a block's candidates past the mirror relaxed densely
 #endif
+// slot prefetches (L2) of the vertices a big extraction makes live: the streaming
+// extract_kernel (piles >= 2^21) and the persistent kernel's CTA-aggregated extraction.
+// Off: a big extraction makes millions of vertices live, whose 64-byte slots overflow the
+// L2 before the next round reads them (config 4: 20.04 -> 19.38 ms)
+#ifndef GI_X_PFX
+#define GI_X_PFX 0
+#endif
+#ifndef GI_X_PFAGG
+#define GI_X_PFAGG 0
+#endif
+// slot prefetches of expand's current-bucket pushes (GI_X_PFXC; off: config 4 19.37 -> 19.27
+// ms) and of the relaxations' pushes and bin spills to the global frontier (GI_X_PFG; on:
+// off measured within ±1 % on configs 2-5)
+#ifndef GI_X_PFXC
+#define GI_X_PFXC 0
+#endif
+#ifndef GI_X_PFG
+#define GI_X_PFG 1
+#endif
 #ifndef GI_X_WSKIP
 #define GI_X_WSKIP 0
 #endif
@@ -406,7 +425,7 @@ __device__ __forceinline__ void push_global(Ctx& c, int32_t v) {
   const uint32_t bit = 1u << (v & 31);
   const uint32_t old = atomicOr(&c.qbits_next[v >> 5], bit);
   if (!(old & bit)) {
-    prefetch_l2(c.slots + 8 * (size_t)v);
+    if (GI_X_PFG) prefetch_l2(c.slots + 8 * (size_t)v);
     cg::coalesced_group g = cg::coalesced_threads();
     uint32_t base = 0;
     if (g.thread_rank() == 0) base = atomicAdd(c.qcount_next, g.size());
@@ -746,7 +765,7 @@ __device__ __forceinline__ uint32_t relax_batch(Ctx& c, const uint2 (&e)[K], con
 #pragma unroll
     for (int k = 0; k < K; ++k)
       if (((ovm >> k) & 1u) && !(ob[k] & (1u << (e[k].x & 31)))) newm |= 1u << k;
-    warp_append(newm, vv, c.q_next, c.qcount_next, c.slots);
+    warp_append(newm, vv, c.q_next, c.qcount_next, GI_X_PFG ? c.slots : nullptr);
   }
   if (LD && GI_LANE_FAR) {
     // low-degree graphs: far pushes are few per warp; one shared atomic per pushing lane on
@@ -2048,7 +2067,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
 #pragma unroll
             for (int x = 0; x < kXtr; ++x)
               if (((ovm >> x) & 1u) && !(old[x] & (1u << (v[x] & 31)))) newm |= 1u << x;
-            if (agg) cta_append(newm, v, c.q_next, c.qcount_next, s.redw, c.slots);
+            if (agg) cta_append(newm, v, c.q_next, c.qcount_next, s.redw, GI_X_PFAGG ? c.slots : nullptr);
             else warp_append(newm, v, c.q_next, c.qcount_next, c.slots);
           }
           TRACE(28);
@@ -2308,7 +2327,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
           if (nin == 0) break;
           if (nin >= T) {
             bulk_append(nin, [&](uint32_t i) { return (int32_t)in[i].x; }, c.qbits_next, c.q_next,
-                        c.qcount_next, c.slots);
+                        c.qcount_next, GI_X_PFG ? c.slots : nullptr);
             if (tid == 0) ++spills;
             break;
           }
@@ -2576,7 +2595,7 @@ __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
   auto flush_cur = [&]() {
     __syncwarp();
     const XPtrs& ps = xs.ps;
-    xflush(xs.cur[warp], min(xs.ncur[warp], (uint32_t)kXCur), ps.qbits, ps.q, ps.qcount, ps.slots);
+    xflush(xs.cur[warp], min(xs.ncur[warp], (uint32_t)kXCur), ps.qbits, ps.q, ps.qcount, GI_X_PFXC ? ps.slots : nullptr);
     if (lane == 0) xs.ncur[warp] = 0;
     __syncwarp();
   };
@@ -2786,11 +2805,17 @@ __global__ void __launch_bounds__(kBlock, 1) expand_kernel(KArgs a) {
 // most once, so no dedup test is needed); a later bucket is kept in the live pile and
 // min-reduced into the next bucket bound; an earlier one is stale and dropped. The dedup
 // bit of every leaving entry is cleared.
+#ifndef GI_EPER
+#define GI_EPER 8
+#endif
+#ifndef GI_EMINB
+#define GI_EMINB 1
+#endif
 constexpr int kEBlock = 512;
-constexpr int kEPer = 8;
+constexpr int kEPer = GI_EPER;  // entries per thread per tile, all their loads in flight together
 constexpr uint32_t kETile = kEBlock * kEPer;
 
-__global__ void __launch_bounds__(kEBlock) extract_kernel(KArgs a) {
+__global__ void __launch_bounds__(kEBlock, GI_EMINB) extract_kernel(KArgs a) {
   __shared__ uint32_t s_keep[kEBlock / 32], s_live[kEBlock / 32], s_lat[kEBlock / 32];
   __shared__ uint32_t s_fmin, s_nlive, s_lmin;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -2883,7 +2908,7 @@ __global__ void __launch_bounds__(kEBlock) extract_kernel(KArgs a) {
       if ((keepm >> x) & 1u) far_live[kw + kpre[x] + __popc(km[x] & ltm)] = v[x];
       if ((latm >> x) & 1u) later[aw + apre[x] + __popc(am[x] & ltm)] = v[x];
       if ((livem >> x) & 1u) {
-        prefetch_l2(a.slots + 8 * (size_t)v[x]);  // read by the next ROUND phase
+        if (GI_X_PFX) prefetch_l2(a.slots + 8 * (size_t)v[x]);  // read by the next ROUND phase
         q_next[lw + lpre[x] + __popc(lm[x] & ltm)] = v[x];
       }
     }

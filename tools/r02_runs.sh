@@ -330,5 +330,31 @@ for v in pf11 pf01 pf00 e4; do
 AB_ONLY=$v timeout 600 python tools/ab_time.py 3 2 2>&1 | grep libgi | sed "s/^/cfg 3: /" >> gpurun_out/r02ao_ab.log
 done
 ;;
+  ap)  # round 2 (session 5): big-extraction slot prefetches off (new default, "old" = on); expand's current-bucket (xc0) and the global-frontier (pg0) prefetches — A/B on configs 4, 3, 2, 5, then the GPU tests
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+for r in 1 2; do for v in base old xc0 pg0; do
+AB_ONLY=$v timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg 4: /" >> gpurun_out/r02ap_ab.log
+done; done
+for cd in "3 2" "2 65536" "5 8192"; do for v in base old xc0 pg0; do
+AB_ONLY=$v timeout 600 python tools/ab_time.py $cd 2>&1 | grep libgi | sed "s/^/cfg $cd: /" >> gpurun_out/r02ap_ab.log
+done; done
+timeout 2400 python -m pytest tests -x -q -m gpu > gpurun_out/r02ap_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02ap_tests.log
+;;
+  aq)  # round 2 (session 5): evidence after the prefetch change — default bench, config-4 launch list with DRAM bytes, configs 1-3, 5 and the apps; k-core prefetch A/B
+T=${1:-r02aq}
+( time timeout 1500 python bench.py ) > gpurun_out/${T}_bench.log 2> gpurun_out/${T}_bench.err
+export GI_GEN_CACHE=/tmp/gcache
+python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/${T}_plain.log 2>&1 &&
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"sssp|expand|extract" --csv --log-file gpurun_out/${T}_launches_cfg4.csv python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/${T}_ncu1.log 2>&1
+for c in 1 2 3; do timeout 600 python bench.py --config $c --steps 10 --warmup 3; done > gpurun_out/${T}_cfgs.log 2>&1
+timeout 900 python bench.py --config 5 --steps 5 --warmup 2 > gpurun_out/${T}_cfg5.log 2>&1
+for app in ppsp astar kcore; do timeout 600 python bench.py --config 2 --app $app --steps 10 --warmup 3; done > gpurun_out/${T}_apps.log 2>&1
+timeout 600 python bench.py --config 3 --app kcore --steps 10 --warmup 3 >> gpurun_out/${T}_apps.log 2>&1
+# k-core slot prefetch only for vertices kept below T in the CTA's bin (GI_KC_PFLOCAL: kpf1) vs every finished vertex (kpf0)
+for r in 1 2; do for v in kpf0 kpf1; do for c in 2 3; do
+AB_DIR=abk AB_ONLY=$v timeout 600 python tools/ab_kcore.py $c 2>&1 | grep libgi | sed "s/^/cfg $c: /" >> gpurun_out/${T}_kcore_ab.log
+done; done; done
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
