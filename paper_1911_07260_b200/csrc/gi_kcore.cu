@@ -57,7 +57,7 @@ constexpr int kKcChunk = 2048;  // frontier vertices staged per claim / per loca
 // CTA's bin (drained here); otherwise (spilled, or a bin that will spill) the slots of a big
 // layer only flush the L2
 #ifndef GI_KC_PFLOCAL
-#define GI_KC_PFLOCAL 0
+#define GI_KC_PFLOCAL 1  // config 2: 8.65 -> 7.80 ms, config 3 9.46 -> 9.42 ms (profiles/r02aq_kcore_ab.txt)
 #endif
 constexpr uint32_t kKcT = GI_KCT; // bucket fusion threshold: a local bin of >= T vertices spills
 constexpr uint32_t kKcHub = 1024;  // out-degree >= this: edges split over every CTA in the next round

@@ -216,6 +216,11 @@ __device__ __forceinline__ uint64_t pol_evict_first() {
 #ifndef GI_X_PFAGG
 #define GI_X_PFAGG 0
 #endif
+// the init's stores of Dist = {inf} with the streaming (evict-first) hint: the row is first
+// touched again when the wavefront reaches it, so it need not displace the L2's working set
+#ifndef GI_INIT_CS
+#define GI_INIT_CS 0
+#endif
 // slot prefetches of expand's current-bucket pushes (GI_X_PFXC; off: config 4 19.37 -> 19.27
 // ms) and of the relaxations' pushes and bin spills to the global frontier (GI_X_PFG; on:
 // off measured within ±1 % on configs 2-5)
@@ -1715,7 +1720,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
             val.x = k == 0 ? 0u : kInf; val.y = k == 1 ? 0u : kInf;
             val.z = k == 2 ? 0u : kInf; val.w = k == 3 ? 0u : kInf;
           }
-          d4[i] = val;
+          if (GI_INIT_CS) __stcs(d4 + i, val); else d4[i] = val;
         }
         done = n4 * 4;
       }

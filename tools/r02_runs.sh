@@ -356,5 +356,17 @@ for r in 1 2; do for v in kpf0 kpf1; do for c in 2 3; do
 AB_DIR=abk AB_ONLY=$v timeout 600 python tools/ab_kcore.py $c 2>&1 | grep libgi | sed "s/^/cfg $c: /" >> gpurun_out/${T}_kcore_ab.log
 done; done; done
 ;;
+  ar)  # round 2 (session 5): the init's Dist = {inf} stores with the streaming hint (GI_INIT_CS: ics1) vs plain (ics0) — A/B on configs 5, 4, 2, 3
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+for r in 1 2; do for v in ics0 ics1; do for cd in "5 8192" "4 2"; do
+AB_ONLY=$v timeout 600 python tools/ab_time.py $cd 2>&1 | grep libgi | sed "s/^/cfg $cd: /" >> gpurun_out/r02ar_ab.log
+done; done; done
+for v in ics0 ics1; do for cd in "2 65536" "3 2"; do
+AB_ONLY=$v timeout 600 python tools/ab_time.py $cd 2>&1 | grep libgi | sed "s/^/cfg $cd: /" >> gpurun_out/r02ar_ab.log
+done; done
+# the GPU tests with the new defaults (k-core GI_KC_PFLOCAL=1, expand GI_X_PFXC=0)
+timeout 2400 python -m pytest tests -x -q -m gpu > gpurun_out/r02ar_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/r02ar_tests.log
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
