@@ -368,5 +368,13 @@ done; done
 timeout 2400 python -m pytest tests -x -q -m gpu > gpurun_out/r02ar_tests.log 2>&1
 echo "tests rc=$?" >> gpurun_out/r02ar_tests.log
 ;;
+  as)  # round 2 (session 5): k-core app lines with GI_KC_PFLOCAL=1, and ncu --set full of config 2's persistent kernel and of config 2's k-core kernel at the final build
+export GI_GEN_CACHE=/tmp/gcache
+for c in 2 3; do timeout 600 python bench.py --config $c --app kcore --steps 10 --warmup 3; done > gpurun_out/r02as_apps.log 2>&1
+python tools/profile_run.py --config 2 --delta 65536 --reps 1 > gpurun_out/r02as_plain.log 2>&1 &&
+ncu --set full --clock-control none --import-source on -k regex:sssp_persistent -c 1 -o gpurun_out/r02as_cfg2 -f python tools/profile_run.py --config 2 --delta 65536 --reps 1 > gpurun_out/r02as_ncu.log 2>&1
+python tools/profile_run.py --config 2 --kcore --reps 1 > gpurun_out/r02as_kplain.log 2>&1 &&
+ncu --set full --clock-control none --import-source on -k regex:kcore_persistent -c 1 -o gpurun_out/r02as_kcore2 -f python tools/profile_run.py --config 2 --kcore --reps 1 > gpurun_out/r02as_kncu.log 2>&1
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
