@@ -222,13 +222,17 @@ __device__ __forceinline__ uint64_t pol_evict_first() {
 #define GI_INIT_CS 0
 #endif
 // slot prefetches of expand's current-bucket pushes (GI_X_PFXC; off: config 4 19.37 -> 19.27
-// ms) and of the relaxations' pushes and bin spills to the global frontier (GI_X_PFG; on:
-// off measured within ±1 % on configs 2-5)
+// ms) and of the relaxations' pushes and bin spills to the global frontier (GI_X_PFG) and of
+// small in-kernel extractions (GI_X_PFXS); the last two off together: config 5 143.97 ->
+// 142.95 ms, config 3 1.875 -> 1.850 ms, configs 1, 2, 4 within ±0.2 %
 #ifndef GI_X_PFXC
 #define GI_X_PFXC 0
 #endif
 #ifndef GI_X_PFG
-#define GI_X_PFG 1
+#define GI_X_PFG 0
+#endif
+#ifndef GI_X_PFXS
+#define GI_X_PFXS 0
 #endif
 #ifndef GI_X_WSKIP
 #define GI_X_WSKIP 0
@@ -2073,7 +2077,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocksPerSm) sssp_persistent(KArgs
             for (int x = 0; x < kXtr; ++x)
               if (((ovm >> x) & 1u) && !(old[x] & (1u << (v[x] & 31)))) newm |= 1u << x;
             if (agg) cta_append(newm, v, c.q_next, c.qcount_next, s.redw, GI_X_PFAGG ? c.slots : nullptr);
-            else warp_append(newm, v, c.q_next, c.qcount_next, c.slots);
+            else warp_append(newm, v, c.q_next, c.qcount_next, GI_X_PFXS ? c.slots : nullptr);
           }
           TRACE(28);
         }

@@ -376,5 +376,25 @@ ncu --set full --clock-control none --import-source on -k regex:sssp_persistent 
 python tools/profile_run.py --config 2 --kcore --reps 1 > gpurun_out/r02as_kplain.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:kcore_persistent -c 1 -o gpurun_out/r02as_kcore2 -f python tools/profile_run.py --config 2 --kcore --reps 1 > gpurun_out/r02as_kncu.log 2>&1
 ;;
+  at)  # round 2 (session 5): slot prefetches of small in-kernel extractions (xs0: off) and of every global-frontier push too (np) — A/B on configs 5, 2, 3, 4
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+for r in 1 2; do for v in base xs0 np; do for cd in "5 8192" "2 65536"; do
+AB_ONLY=$v timeout 600 python tools/ab_time.py $cd 2>&1 | grep libgi | sed "s/^/cfg $cd: /" >> gpurun_out/r02at_ab.log
+done; done; done
+for v in base xs0 np; do for cd in "3 2" "4 2" "1 1000"; do
+AB_ONLY=$v timeout 600 python tools/ab_time.py $cd 2>&1 | grep libgi | sed "s/^/cfg $cd: /" >> gpurun_out/r02at_ab.log
+done; done
+;;
+  au)  # round 2 (session 5): final evidence — GPU tests at the final defaults (all big-list slot prefetches off), default bench, config-4 launch list with DRAM bytes, configs 2, 3, 5
+T=${1:-r02au}
+timeout 2400 python -m pytest tests -x -q -m gpu > gpurun_out/${T}_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/${T}_tests.log
+( time timeout 1500 python bench.py ) > gpurun_out/${T}_bench.log 2> gpurun_out/${T}_bench.err
+export GI_GEN_CACHE=/tmp/gcache
+python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/${T}_plain.log 2>&1 &&
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"sssp|expand|extract" --csv --log-file gpurun_out/${T}_launches_cfg4.csv python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/${T}_ncu1.log 2>&1
+for c in 2 3; do timeout 600 python bench.py --config $c --steps 10 --warmup 3; done > gpurun_out/${T}_cfgs.log 2>&1
+timeout 900 python bench.py --config 5 --steps 5 --warmup 2 > gpurun_out/${T}_cfg5.log 2>&1
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
