@@ -396,5 +396,13 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 for c in 2 3; do timeout 600 python bench.py --config $c --steps 10 --warmup 3; done > gpurun_out/${T}_cfgs.log 2>&1
 timeout 900 python bench.py --config 5 --steps 5 --warmup 2 > gpurun_out/${T}_cfg5.log 2>&1
 ;;
+  av)  # round 2 (session 6): ncu --set full of config 4's hub-phase expand_kernel at the final build (all big-list slot prefetches off), then the app lines
+export GI_GEN_CACHE=/tmp/gcache
+python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02av_plain.log 2>&1 &&
+ncu --set full --clock-control none --import-source on -k regex:expand_kernel -s 1 -c 1 -o gpurun_out/r02av_expand -f python tools/profile_run.py --config 4 --delta 2 --reps 1 > gpurun_out/r02av_ncu.log 2>&1
+for app in ppsp astar kcore; do timeout 600 python bench.py --config 2 --app $app --steps 10 --warmup 3; done > gpurun_out/r02av_apps.log 2>&1
+timeout 600 python bench.py --config 3 --app kcore --steps 10 --warmup 3 >> gpurun_out/r02av_apps.log 2>&1
+timeout 600 python bench.py --config 1 --steps 10 --warmup 3 > gpurun_out/r02av_cfg1.log 2>&1
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
