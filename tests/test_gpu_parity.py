@@ -319,14 +319,16 @@ def test_stress_repeated_full_size(gi, config_graph):
     """Race stress at full size (compute-sanitizer is closed on this pool): 20 runs each of
     config 3 at Δ=8 (skewed; pre-read / red.min protocol, R11; the late staleness gate, R12)
     and config 2 with the async drain (ring protocol, R10), with random CTA counts,
-    thresholds and pre-read settings, every run compared with the oracle element by element."""
-    rng = np.random.default_rng(2024)
+    thresholds and pre-read settings, every run compared with the oracle element by element.
+    GI_STRESS_SEED / GI_STRESS_ITERS lengthen it into a soak (tools/r02_runs.sh arm aw)."""
+    rng = np.random.default_rng(int(os.environ.get("GI_STRESS_SEED", "2024")))
+    iters = int(os.environ.get("GI_STRESS_ITERS", "20"))
     for cfg, delta, base in ((3, 8, dict()), (2, 1 << 14, dict(drain="async"))):
         g = config_graph(cfg)
         G = gi.Graph.from_csr(g)
         src = gen.config_source(cfg, g)
         ref, _ = oracle.dijkstra(g, src)
-        for it in range(20):
+        for it in range(iters):
             o = dict(base)
             o["max_ctas"] = int(rng.choice([0, 0, 1, 7, 64, 147]))
             o["threshold"] = int(rng.choice([0, 1, 16, 256, 1000]))

@@ -404,5 +404,14 @@ for app in ppsp astar kcore; do timeout 600 python bench.py --config 2 --app $ap
 timeout 600 python bench.py --config 3 --app kcore --steps 10 --warmup 3 >> gpurun_out/r02av_apps.log 2>&1
 timeout 600 python bench.py --config 1 --steps 10 --warmup 3 > gpurun_out/r02av_cfg1.log 2>&1
 ;;
+  aw)  # round 2 (session 6): race soak at the final build — the full-size stress test with 4 more seeds x 40 runs per leg, two of them with every expand / extraction split into its own kernels (GI_SPLIT_MIN=1, GI_XSPLIT_MIN=1)
+export GI_GEN_CACHE=/tmp/gcache GI_STRESS_ITERS=40
+for seed in 11 12 13 14; do
+  if [ $seed -ge 13 ]; then export GI_SPLIT_MIN=1 GI_XSPLIT_MIN=1; fi
+  echo "== seed $seed iters $GI_STRESS_ITERS split_min=${GI_SPLIT_MIN:-default}" >> gpurun_out/r02aw_soak.log
+  GI_STRESS_SEED=$seed timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "stress_repeated" >> gpurun_out/r02aw_soak.log 2>&1
+  echo "rc=$?" >> gpurun_out/r02aw_soak.log
+done
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
