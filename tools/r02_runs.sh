@@ -413,5 +413,11 @@ for seed in 11 12 13 14; do
   echo "rc=$?" >> gpurun_out/r02aw_soak.log
 done
 ;;
+  ax)  # round 2 (session 6): expand rows in flight per warp re-swept at the final build (GI_XROWS 6 / 8 = base / 10) — config 4 A/B, three alternating rounds
+export GI_GEN_CACHE=/tmp/gcache AB_DIR=abx
+for r in 1 2 3; do for v in base xr6 xr10; do
+AB_ONLY=$v timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg 4 2: /" >> gpurun_out/r02ax_ab.log
+done; done
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
