@@ -419,5 +419,11 @@ for r in 1 2 3; do for v in base xr6 xr10; do
 AB_ONLY=$v timeout 600 python tools/ab_time.py 4 2 2>&1 | grep libgi | sed "s/^/cfg 4 2: /" >> gpurun_out/r02ax_ab.log
 done; done
 ;;
+  ay)  # round 2 (session 6): the config-4 placement effect re-measured at the final build (tools/placement_test.py, tools/ab/libgi_cs.so = the default build), one mode per process
+export GI_GEN_CACHE=/tmp/gcache
+for m in single torch_mb_256 out_first torch_mb_256_free torch_mb_2048 single torch_mb_256; do
+timeout 600 python tools/placement_test.py $m 2>&1 | tail -1 >> gpurun_out/r02ay_placement.log
+done
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
