@@ -425,5 +425,12 @@ for m in single torch_mb_256 out_first torch_mb_256_free torch_mb_2048 single to
 timeout 600 python tools/placement_test.py $m 2>&1 | tail -1 >> gpurun_out/r02ay_placement.log
 done
 ;;
+  az)  # round 2 (session 6): DRAM bytes per query of configs 2, 3 and 5 at the final build (ncu metrics-only launch lists → profiles/ncu_traffic.json)
+export GI_GEN_CACHE=/tmp/gcache
+for cd in "2 65536" "3 2" "5 8192"; do set -- $cd
+python tools/profile_run.py --config $1 --delta $2 --reps 1 > gpurun_out/r02az_plain_cfg$1.log 2>&1 &&
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"sssp|expand|extract" --csv --log-file gpurun_out/r02az_launches_cfg$1.csv python tools/profile_run.py --config $1 --delta $2 --reps 1 > gpurun_out/r02az_ncu_cfg$1.log 2>&1
+done
+;;
   *) echo "usage: bash tools/r02_runs.sh ARM [args]; arms:"; grep -E "^  [a-z0-9_]+\)" "$0"; exit 2 ;;
 esac
